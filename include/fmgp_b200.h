@@ -1,0 +1,160 @@
+/* fmgp_b200.h — the drop-in boundary: a C ABI over the B200 (sm_100a)
+ * implementation of the FastMuyGPs posterior-mean path.
+ *
+ * The reference exposes this path only as a C++ API in namespace fastmuygps
+ * (paths relative to /root/reference/proj):
+ *   precompute            core/include/fastmuygps/fast_predict.hpp:38-41
+ *   fast_predict_one      core/include/fastmuygps/fast_predict.hpp:45-46
+ *   fast_predict_batch    core/include/fastmuygps/fast_predict.hpp:48-49
+ *   NeighborIndex (Exact) core/include/fastmuygps/nn_index.hpp:34-51
+ *   kernel_value / cov_matrix / cov_matrix_self  core/include/fastmuygps/kernel.hpp:39-55
+ *   cholesky_with_jitter / solve_spd             core/include/fastmuygps/linalg.hpp:13-20
+ * The C++ facade in paper_2205_10879_b200/cpp re-exports those exact headers
+ * and calls the functions below; any other FFI (ctypes, cgo, JNI) binds them
+ * directly — see INTEGRATION.md.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Matrices are ROW-MAJOR: X n*d, Y n*m,
+ *    Z nz*d, S n*k int32 (the reference's NeighborTable layout,
+ *    fast_predict.hpp:15-18), C n*k*m f64 (m = 1 is the reference's
+ *    RowMajor n*k table, fast_predict.hpp:27).
+ *  - Functions without `_device` take HOST buffers owned by the caller and
+ *    do every host<->device copy internally (synchronous on return).
+ *    Functions with `_device` take DEVICE pointers on the current CUDA device
+ *    and a cudaStream_t passed as void*; they are stream-ordered and return
+ *    after enqueueing, except where a status must be read back (noted).
+ *  - No exceptions cross the ABI. Return codes map to the reference's
+ *    exceptions (the facade re-throws them with the reference's messages):
+ *      FMGP_OK        0
+ *      FMGP_EINVAL    1  std::domain_error   (argument/precondition errors)
+ *      FMGP_ENUMERIC  2  fastmuygps::NumericError (jitter ladder exhausted,
+ *                        linalg.cpp:28-30; *failed_row = lowest failing row,
+ *                        matching the reference run with threads = 1)
+ *      FMGP_ECUDA     3  CUDA error or no usable device (never a CPU fallback)
+ *    fmgp_last_error() returns the calling thread's last message.
+ *  - Results do not depend on how rows are sharded (row_begin/row_end) or on
+ *    the number of GPUs: every row is computed by the same arithmetic.
+ */
+#ifndef FMGP_B200_H
+#define FMGP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMGP_ABI_VERSION 1
+
+enum fmgp_status { FMGP_OK = 0, FMGP_EINVAL = 1, FMGP_ENUMERIC = 2, FMGP_ECUDA = 3 };
+
+/* KernelKind (kernel.hpp:7); the numeric values are the model-file tag
+ * (fast_predict.cpp:179). */
+enum fmgp_kernel_kind { FMGP_MATERN = 0, FMGP_RBF = 1 };
+
+/* KernelParams (kernel.hpp:12-33) + KernelKind. Validated like the
+ * reference constructor (kernel.cpp:13-28): sigma, rho, nu > 0 and finite,
+ * tau >= 0 and finite. The device path evaluates Matern for nu in
+ * {0.5, 1.5, 2.5} (the closed forms of kernel.cpp:63-71) and RBF for any nu. */
+typedef struct fmgp_kernel_params {
+  int32_t kind;
+  double sigma;
+  double rho;
+  double nu;
+  double tau;
+} fmgp_kernel_params;
+
+int fmgp_abi_version(void);
+const char* fmgp_last_error(void);
+/* Diagnostics: number of CUDA kernels this library has launched (process-wide). */
+int64_t fmgp_launch_count(void);
+/* Number of visible CUDA devices (0 when none: every compute call then
+ * returns FMGP_ECUDA). */
+int fmgp_device_count(void);
+
+/* KernelParams constructor checks (kernel.cpp:13-28) plus the device path's
+ * nu support. */
+int fmgp_validate_kernel(const fmgp_kernel_params* p);
+
+/* ---- precompute (fast_predict.cpp:70-130) ---------------------------------
+ * S_out[i,0] = i; S_out[i,1..k-1] = the k-1 nearest training points of x_i,
+ * excluding i by index, ascending by (dist_sq, index) — bit-exact with the
+ * reference's Exact NeighborIndex. C_out[i] = K(X_S_i, X_S_i)^-1 Y_S_i with
+ * the nugget/jitter conventions of kernel.cpp:58-60 and linalg.cpp:10-31.
+ * Errors: k not in [1, n] or n < 1 or d < 1 or m < 1 or non-finite X
+ * (fast_predict.cpp:74-76, nn_index.cpp:56-62) -> FMGP_EINVAL. */
+int fmgp_precompute(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                    const fmgp_kernel_params* params, int32_t k, int32_t* S_out, double* C_out,
+                    int64_t* failed_row);
+
+/* Row shard [row_begin, row_end) of precompute with everything in HBM:
+ * X (n*d) and Y (n*m) are the full, replicated training set; S_out and C_out
+ * hold (row_end-row_begin) rows. Reads back one status word, so it returns
+ * after the shard is finished. X is not re-validated here. */
+int fmgp_precompute_device(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                           const fmgp_kernel_params* params, int32_t k, int64_t row_begin,
+                           int64_t row_end, int32_t* S_out, double* C_out, int64_t* failed_row,
+                           void* stream);
+
+/* ---- neighbour search (nn_index.cpp:254-287, :351-366) --------------------
+ * For each of nq queries, the k nearest of the np points by (dist_sq, index);
+ * exclude (nullable, nq entries) removes one point index per query (-1: none),
+ * by index identity (nn_index.cpp:268). idx_out nq*k; dist_out (nullable)
+ * nq*k receives sqrt(dist_sq) like NeighborList::distances (:337-340).
+ * Errors: k < 1 or k > np - (exclude >= 0) -> FMGP_EINVAL (:260-263). */
+int fmgp_query_knn(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq, int32_t k,
+                   const int32_t* exclude, int32_t* idx_out, double* dist_out);
+int fmgp_query_knn_device(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq,
+                          int32_t k, int64_t self_offset, int32_t* idx_out, double* dist_sq_out,
+                          void* stream);
+/* nearest_training_point for nq queries: ties go to the lower index. */
+int fmgp_nearest(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq, int32_t* idx_out);
+int fmgp_nearest_device(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq,
+                        int32_t* idx_out, void* stream);
+
+/* ---- predict (fast_predict.cpp:132-156) -----------------------------------
+ * out[t*m + c] = sum_s kernel(||z_t - x_{S[j,s]}||) C[j,s,c] + mean_offset[c],
+ * j = nearest training point of z_t (nn_out, nullable, receives j). */
+int fmgp_predict(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d, int32_t k,
+                 int32_t m, const fmgp_kernel_params* params, const double* mean_offset, const double* Z,
+                 int64_t nz, double* out, int32_t* nn_out);
+/* Same with X, S, C, Z, out, nn_out in HBM; mean_offset is a host array of m. */
+int fmgp_predict_device(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d,
+                        int32_t k, int32_t m, const fmgp_kernel_params* params, const double* mean_offset,
+                        const double* Z, int64_t nz, double* out, int32_t* nn_out, void* stream);
+
+/* ---- PrecomputedModel handle (fast_predict.hpp:25-33) ---------------------
+ * Device-resident, immutable copy of X, S, C, kernel and mean offsets on
+ * `device`. fmgp_model_predict is safe to call concurrently from several host
+ * threads on one handle (fast_predict.hpp:20-24). */
+typedef struct fmgp_model fmgp_model;
+int fmgp_model_create(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d,
+                      int32_t k, int32_t m, const fmgp_kernel_params* params, const double* mean_offset,
+                      int32_t device, fmgp_model** out);
+int fmgp_model_predict(const fmgp_model* model, const double* Z, int64_t nz, double* out,
+                       int32_t* nn_out);
+void fmgp_model_destroy(fmgp_model* model);
+
+/* ---- kernel arithmetic on device (kernel.cpp:88-119) ----------------------
+ * K_out (na*nb row-major) = kernel(||A_i - B_j||); with B == NULL computes
+ * cov_matrix_self(A) (exact symmetric fill, diagonal kernel(0)). */
+int fmgp_cov_matrix(const double* A, int64_t na, const double* B, int64_t nb, int32_t d,
+                    const fmgp_kernel_params* params, double* K_out);
+/* kernel_value at ndist distances (check_distance, kernel.cpp:32-36:
+ * negative or non-finite -> FMGP_EINVAL). */
+int fmgp_kernel_values(const double* dist, int64_t ndist, const fmgp_kernel_params* params, double* out);
+
+/* ---- batched SPD solve (linalg.cpp:10-36) ---------------------------------
+ * For each of `batch` symmetric k*k matrices K (row-major, lower triangle
+ * used), solve K X = B (B: k*m row-major) under the jitter ladder
+ * {0, 1e-10, 1e-8, 1e-6}. X_out may alias B. applied_jitter (nullable,
+ * batch) receives the rung that succeeded. On failure returns FMGP_ENUMERIC
+ * with *failed_index = the lowest failing matrix. */
+int fmgp_solve_spd_batched(const double* K, const double* B, int64_t batch, int32_t k, int32_t m,
+                           double* X_out, double* applied_jitter, int64_t* failed_index);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMGP_B200_H */

@@ -1,0 +1,229 @@
+// ORACLE TEST INFRASTRUCTURE — not product code.
+//
+// C-callable harness around the *reference's own* public C++ API
+// (proj/core/include/fastmuygps/*.hpp), linked with the reference TUs
+// compiled unmodified (oracle/Makefile `ref`). Used only by tests/ (golden
+// fixture generation, cross-checks of the C restatement) and by bench.py's
+// `--impl reference` / cpu_baseline legs. Every entry point makes exactly the
+// public calls the reference makes:
+//   fmgp_ref_precompute      -> fastmuygps::precompute            (fast_predict.cpp:70-130)
+//   fmgp_ref_precompute_rows -> the do_rows body on a row subset   (fast_predict.cpp:89-107):
+//                               NeighborIndex::query_knn, cov_matrix_self, solve_spd
+//   fmgp_ref_predict         -> fast_predict_batch / fast_predict_one (fast_predict.cpp:132-156)
+//   fmgp_ref_query_knn, fmgp_ref_nearest, fmgp_ref_kernel_value -> nn_index.cpp / kernel.cpp
+// Multi-output (BASELINE cfg3, m > 1): the reference is single-output
+// (dataset.hpp:14); the harness shares S and passes the k x m right-hand
+// sides to the reference's own solve_spd (linalg.hpp:19-20), which solves
+// them column by column with one factorisation.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fastmuygps/errors.hpp"
+#include "fastmuygps/fast_predict.hpp"
+#include "fastmuygps/kernel.hpp"
+#include "fastmuygps/linalg.hpp"
+#include "fastmuygps/nn_index.hpp"
+
+using namespace fastmuygps;
+
+namespace {
+
+thread_local std::string g_err;
+
+Eigen::MatrixXd from_rm(const double* a, int64_t n, int d) {
+  Eigen::MatrixXd X(n, d);
+  for (int64_t i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j) X(i, j) = a[i * d + j];
+  return X;
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const NumericError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+KernelKind kind_of(int kind) { return kind == 1 ? KernelKind::RBF : KernelKind::Matern; }
+
+}  // namespace
+
+extern "C" {
+
+const char* fmgp_ref_last_error() { return g_err.c_str(); }
+
+double fmgp_ref_kernel_value(double d, int kind, double sigma, double rho,
+                             double nu, double tau) {
+  return kernel_value(d, kind_of(kind), KernelParams(sigma, rho, nu, tau));
+}
+
+// Full reference precompute (single output). S_out n*k int32, C_out n*k f64.
+int fmgp_ref_precompute(const double* X_rm, const double* Y, int64_t n, int d,
+                        int kind, double sigma, double rho, double nu,
+                        double tau, int k, int threads, int32_t* S_out,
+                        double* C_out) {
+  return guard([&] {
+    TrainingSet train;
+    train.X = from_rm(X_rm, n, d);
+    train.Y = Eigen::VectorXd(n);
+    for (int64_t i = 0; i < n; ++i) train.Y(i) = Y[i];
+    train.mean_offset = 0.0;
+    FittedParams fitted{KernelParams(sigma, rho, nu, tau), kind_of(kind), 0.0, 0, false};
+    NeighborIndex index = NeighborIndex::build(train.X, IndexMode::Exact);
+    PrecomputedModel model = precompute(train, fitted, index, k, threads);
+    std::memcpy(S_out, model.table.S.data(), sizeof(int32_t) * n * k);
+    std::memcpy(C_out, model.C.data(), sizeof(double) * n * k);
+  });
+}
+
+// The do_rows body (fast_predict.cpp:89-107) for an arbitrary row subset,
+// spread over `threads` std::threads in contiguous chunks like :110-125.
+// Y_rm is n x m row-major; C_out is nrows x k x m. The first NumericError's
+// row is reported through fmgp_ref_last_error().
+int fmgp_ref_precompute_rows(const double* X_rm, const double* Y_rm, int64_t n,
+                             int d, int m, int kind, double sigma, double rho,
+                             double nu, double tau, int k, const int64_t* rows,
+                             int64_t nrows, int threads, int32_t* S_out,
+                             double* C_out) {
+  return guard([&] {
+    Eigen::MatrixXd X = from_rm(X_rm, n, d);
+    KernelParams p(sigma, rho, nu, tau);
+    KernelKind kk = kind_of(kind);
+    NeighborIndex index = NeighborIndex::build(X, IndexMode::Exact);
+    std::vector<std::exception_ptr> errs(std::max(1, threads));
+    auto work = [&](int w, int64_t b, int64_t e) {
+      try {
+        Eigen::MatrixXd xs(k, d);
+        Eigen::MatrixXd ys(k, m);
+        std::vector<int32_t> srow(k);
+        for (int64_t r = b; r < e; ++r) {
+          const int64_t i = rows[r];
+          srow[0] = static_cast<int32_t>(i);
+          if (k > 1) {
+            NeighborList nl = index.query_knn(X.row(i).transpose(), k - 1, static_cast<int>(i));
+            for (int t = 0; t < k - 1; ++t) srow[t + 1] = nl.indices[t];
+          }
+          for (int t = 0; t < k; ++t) {
+            xs.row(t) = X.row(srow[t]);
+            for (int c = 0; c < m; ++c) ys(t, c) = Y_rm[static_cast<int64_t>(srow[t]) * m + c];
+          }
+          Eigen::MatrixXd kss = cov_matrix_self(xs, kk, p);
+          Eigen::MatrixXd sol = solve_spd(kss, ys, "precompute row " + std::to_string(i));
+          for (int t = 0; t < k; ++t) {
+            S_out[r * k + t] = srow[t];
+            for (int c = 0; c < m; ++c) C_out[(r * k + t) * m + c] = sol(t, c);
+          }
+        }
+      } catch (...) {
+        errs[w] = std::current_exception();
+      }
+    };
+    if (threads <= 1 || nrows < 2 * threads) {
+      work(0, 0, nrows);
+    } else {
+      std::vector<std::thread> ws;
+      int64_t chunk = (nrows + threads - 1) / threads;
+      for (int w = 0; w < threads; ++w) {
+        int64_t b = w * chunk, e = std::min<int64_t>(nrows, b + chunk);
+        if (b < e) ws.emplace_back(work, w, b, e);
+      }
+      for (auto& t : ws) t.join();
+    }
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+  });
+}
+
+// Posterior means for Z through the reference model built from X, S, C
+// (m outputs: C is n x k x m, out is nz x m). threads <= 1 calls
+// fast_predict_batch exactly; threads > 1 splits rows over fast_predict_one,
+// which the reference documents as safe for concurrent callers
+// (fast_predict.hpp:20-24). nn_out (optional) receives the 1-NN index.
+int fmgp_ref_predict(const double* X_rm, const int32_t* S, const double* C,
+                     int64_t n, int d, int k, int m, int kind, double sigma,
+                     double rho, double nu, double tau, double mean_offset,
+                     const double* Z_rm, int64_t nz, int threads, double* out,
+                     int32_t* nn_out) {
+  return guard([&] {
+    Eigen::MatrixXd X = from_rm(X_rm, n, d);
+    NeighborIndex index = NeighborIndex::build(X, IndexMode::Exact);
+    NeighborTable table;
+    table.S.resize(n, k);
+    std::memcpy(table.S.data(), S, sizeof(int32_t) * n * k);
+    std::vector<PrecomputedModel> models;
+    models.reserve(m);
+    for (int c = 0; c < m; ++c) {
+      Eigen::Matrix<double, Eigen::Dynamic, Eigen::Dynamic, Eigen::RowMajor> Cc(n, k);
+      for (int64_t i = 0; i < n * k; ++i) Cc.data()[i] = C[i * m + c];
+      models.push_back(PrecomputedModel{X, table, std::move(Cc), KernelParams(sigma, rho, nu, tau),
+                                        kind_of(kind), mean_offset, index});
+    }
+    Eigen::MatrixXd Z = from_rm(Z_rm, nz, d);
+    if (threads <= 1) {
+      for (int c = 0; c < m; ++c) {
+        Eigen::VectorXd v = fast_predict_batch(models[c], Z);
+        for (int64_t t = 0; t < nz; ++t) out[t * m + c] = v(t);
+      }
+      if (nn_out != nullptr)
+        for (int64_t t = 0; t < nz; ++t) nn_out[t] = index.nearest_training_point(Z.row(t).transpose());
+      return;
+    }
+    std::vector<std::thread> ws;
+    int64_t chunk = (nz + threads - 1) / threads;
+    for (int w = 0; w < threads; ++w) {
+      int64_t b = w * chunk, e = std::min<int64_t>(nz, b + chunk);
+      if (b >= e) continue;
+      ws.emplace_back([&, b, e] {
+        for (int64_t t = b; t < e; ++t) {
+          Eigen::VectorXd z = Z.row(t).transpose();
+          for (int c = 0; c < m; ++c) out[t * m + c] = fast_predict_one(models[c], z);
+          if (nn_out != nullptr) nn_out[t] = index.nearest_training_point(z);
+        }
+      });
+    }
+    for (auto& t : ws) t.join();
+  });
+}
+
+int fmgp_ref_query_knn(const double* X_rm, int64_t n, int d, const double* q,
+                       int k, int exclude, int32_t* idx_out, double* dist_out) {
+  return guard([&] {
+    NeighborIndex index = NeighborIndex::build(from_rm(X_rm, n, d), IndexMode::Exact);
+    Eigen::VectorXd qq(d);
+    for (int j = 0; j < d; ++j) qq(j) = q[j];
+    NeighborList nl = index.query_knn(qq, k, exclude);
+    for (int t = 0; t < k; ++t) {
+      idx_out[t] = nl.indices[t];
+      dist_out[t] = nl.distances[t];
+    }
+  });
+}
+
+int fmgp_ref_nearest(const double* X_rm, int64_t n, int d, const double* Q_rm,
+                     int64_t nq, int32_t* out) {
+  return guard([&] {
+    NeighborIndex index = NeighborIndex::build(from_rm(X_rm, n, d), IndexMode::Exact);
+    Eigen::VectorXd qq(d);
+    for (int64_t t = 0; t < nq; ++t) {
+      for (int j = 0; j < d; ++j) qq(j) = Q_rm[t * d + j];
+      out[t] = index.nearest_training_point(qq);
+    }
+  });
+}
+
+}  // extern "C"

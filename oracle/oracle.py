@@ -1,0 +1,245 @@
+"""ORACLE TEST INFRASTRUCTURE — ctypes front-ends of the two CPU checkers.
+
+  Port       oracle/build/libfmgp_oracle.so  the C restatement (fmgp_oracle.c)
+  Reference  oracle/_ref/libfmgp_ref.so      the reference's own TUs compiled
+                                             unmodified against the shims, driven
+                                             through its public API (harness/ref_harness.cpp)
+
+Both take/return row-major numpy arrays. Used only as the checker (tests/,
+__graft_entry__.smoke()) and as the CPU baseline (bench.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+PORT_PATH = HERE / "build" / "libfmgp_oracle.so"
+REF_PATH = HERE / "_ref" / "libfmgp_ref.so"
+
+_V = C.c_void_p
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg, failed_row=-1):
+        super().__init__(msg)
+        self.code = code
+        self.failed_row = failed_row
+
+
+class Port:
+    """The C restatement (fmgp_oracle.c)."""
+
+    kind = "port"
+
+    def __init__(self, path: Path = PORT_PATH):
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing; run make -C oracle")
+        L = C.CDLL(str(path))
+        L.fmgp_oracle_dist_sq.restype = C.c_double
+        L.fmgp_oracle_dist_sq.argtypes = [_V, _V, C.c_int]
+        L.fmgp_oracle_kernel_value.restype = C.c_double
+        L.fmgp_oracle_kernel_value.argtypes = [C.c_double, C.c_int] + [C.c_double] * 4
+        L.fmgp_oracle_query_knn.restype = C.c_int
+        L.fmgp_oracle_query_knn.argtypes = [_V, C.c_int64, C.c_int, _V, C.c_int, C.c_int64, _V, _V]
+        L.fmgp_oracle_nearest.restype = C.c_int32
+        L.fmgp_oracle_nearest.argtypes = [_V, C.c_int64, C.c_int, _V]
+        L.fmgp_oracle_cov_self.restype = None
+        L.fmgp_oracle_cov_self.argtypes = [_V, C.c_int, C.c_int, C.c_int] + [C.c_double] * 4 + [_V]
+        L.fmgp_oracle_cholesky_jitter.restype = C.c_int
+        L.fmgp_oracle_cholesky_jitter.argtypes = [_V, C.c_int, _V]
+        L.fmgp_oracle_precompute_rows.restype = C.c_int
+        L.fmgp_oracle_precompute_rows.argtypes = ([_V, _V, C.c_int64, C.c_int, C.c_int, C.c_int] + [C.c_double] * 4 +
+                                                  [C.c_int, _V, C.c_int64, C.c_int, _V, _V, _V])
+        L.fmgp_oracle_predict.restype = C.c_int
+        L.fmgp_oracle_predict.argtypes = ([_V, _V, _V, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int] +
+                                          [C.c_double] * 5 + [_V, C.c_int64, C.c_int, _V, _V])
+        self.L = L
+
+    def kernel_value(self, dist, kind, sigma, rho, nu, tau):
+        return self.L.fmgp_oracle_kernel_value(dist, kind, sigma, rho, nu, tau)
+
+    def query_knn(self, X, q, k, exclude=-1):
+        X = _f64(X)
+        q = _f64(q)
+        idx = np.empty(k, dtype=np.int32)
+        dsq = np.empty(k, dtype=np.float64)
+        rc = self.L.fmgp_oracle_query_knn(_p(X), X.shape[0], X.shape[1], _p(q), k, exclude, _p(idx), _p(dsq))
+        if rc != 0:
+            raise OracleError(1, "query_knn: k out of range")
+        return idx, dsq
+
+    def nearest(self, X, Q):
+        X = _f64(X)
+        Q = _f64(Q).reshape(-1, X.shape[1])
+        return np.array([self.L.fmgp_oracle_nearest(_p(X), X.shape[0], X.shape[1], _p(Q[i]))
+                         for i in range(Q.shape[0])], dtype=np.int32)
+
+    def cov_self(self, xs, kind, sigma, rho, nu, tau):
+        xs = _f64(xs)
+        K = np.empty((xs.shape[0], xs.shape[0]))
+        self.L.fmgp_oracle_cov_self(_p(xs), xs.shape[0], xs.shape[1], kind, sigma, rho, nu, tau, _p(K))
+        return K
+
+    def precompute_rows(self, X, Y, kind, sigma, rho, nu, tau, k, rows=None, threads=1):
+        X = _f64(X)
+        Y = _f64(Y)
+        Y2 = Y.reshape(Y.shape[0], -1)
+        n, d = X.shape
+        m = Y2.shape[1]
+        rows = np.arange(n, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+        S = np.empty((rows.size, k), dtype=np.int32)
+        Cm = np.empty((rows.size, k, m), dtype=np.float64)
+        failed = C.c_int64(-1)
+        rc = self.L.fmgp_oracle_precompute_rows(_p(X), _p(Y2), n, d, m, kind, sigma, rho, nu, tau, k, _p(rows),
+                                                rows.size, threads, _p(S), _p(Cm), C.byref(failed))
+        if rc == 1:
+            raise OracleError(1, "precompute: k out of range")
+        if rc == 2:
+            raise OracleError(2, f"Cholesky factorization failed in precompute row {failed.value} after jitter "
+                                 "escalation up to 1e-6", failed.value)
+        return S, Cm
+
+    def predict(self, X, S, Cm, kind, sigma, rho, nu, tau, mean_offset, Z, threads=1):
+        X = _f64(X)
+        Z = _f64(Z)
+        S = np.ascontiguousarray(S, dtype=np.int32)
+        n, d = X.shape
+        k = S.shape[1]
+        C3 = _f64(Cm).reshape(n, k, -1)
+        m = C3.shape[2]
+        out = np.empty((Z.shape[0], m))
+        nn = np.empty(Z.shape[0], dtype=np.int32)
+        mo = float(np.asarray(mean_offset).reshape(-1)[0]) if m == 1 else None
+        if m == 1:
+            self.L.fmgp_oracle_predict(_p(X), _p(S), _p(C3), n, d, k, 1, kind, sigma, rho, nu, tau, mo, _p(Z),
+                                       Z.shape[0], threads, _p(out), _p(nn))
+        else:
+            mos = np.asarray(mean_offset, dtype=np.float64).reshape(-1)
+            for c in range(m):
+                Cc = np.ascontiguousarray(C3[:, :, c])
+                oc = np.empty((Z.shape[0], 1))
+                self.L.fmgp_oracle_predict(_p(X), _p(S), _p(Cc), n, d, k, 1, kind, sigma, rho, nu, tau,
+                                           float(mos[c]), _p(Z), Z.shape[0], threads, _p(oc), _p(nn))
+                out[:, c] = oc[:, 0]
+        return out, nn
+
+
+class Reference:
+    """The reference's own TUs (oracle/_ref), through its public C++ API."""
+
+    kind = "reference"
+
+    def __init__(self, path: Path = REF_PATH):
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing; run make -C oracle ref (needs /root/reference)")
+        L = C.CDLL(str(path))
+        L.fmgp_ref_last_error.restype = C.c_char_p
+        L.fmgp_ref_kernel_value.restype = C.c_double
+        L.fmgp_ref_kernel_value.argtypes = [C.c_double, C.c_int] + [C.c_double] * 4
+        L.fmgp_ref_precompute.restype = C.c_int
+        L.fmgp_ref_precompute.argtypes = ([_V, _V, C.c_int64, C.c_int, C.c_int] + [C.c_double] * 4 +
+                                          [C.c_int, C.c_int, _V, _V])
+        L.fmgp_ref_precompute_rows.restype = C.c_int
+        L.fmgp_ref_precompute_rows.argtypes = ([_V, _V, C.c_int64, C.c_int, C.c_int, C.c_int] + [C.c_double] * 4 +
+                                               [C.c_int, _V, C.c_int64, C.c_int, _V, _V])
+        L.fmgp_ref_predict.restype = C.c_int
+        L.fmgp_ref_predict.argtypes = ([_V, _V, _V, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int] +
+                                       [C.c_double] * 5 + [_V, C.c_int64, C.c_int, _V, _V])
+        L.fmgp_ref_query_knn.restype = C.c_int
+        L.fmgp_ref_query_knn.argtypes = [_V, C.c_int64, C.c_int, _V, C.c_int, C.c_int, _V, _V]
+        L.fmgp_ref_nearest.restype = C.c_int
+        L.fmgp_ref_nearest.argtypes = [_V, C.c_int64, C.c_int, _V, C.c_int64, _V]
+        self.L = L
+
+    def _check(self, rc):
+        if rc != 0:
+            msg = self.L.fmgp_ref_last_error().decode()
+            row = -1
+            if rc == 2 and "precompute row " in msg:
+                row = int(msg.split("precompute row ")[1].split()[0])
+            raise OracleError(rc, msg, row)
+
+    def kernel_value(self, dist, kind, sigma, rho, nu, tau):
+        return self.L.fmgp_ref_kernel_value(dist, kind, sigma, rho, nu, tau)
+
+    def precompute(self, X, Y, kind, sigma, rho, nu, tau, k, threads=1):
+        X = _f64(X)
+        Y = _f64(Y).reshape(-1)
+        n, d = X.shape
+        S = np.empty((n, k), dtype=np.int32)
+        Cm = np.empty((n, k), dtype=np.float64)
+        self._check(self.L.fmgp_ref_precompute(_p(X), _p(Y), n, d, kind, sigma, rho, nu, tau, k, threads, _p(S),
+                                               _p(Cm)))
+        return S, Cm
+
+    def precompute_rows(self, X, Y, kind, sigma, rho, nu, tau, k, rows=None, threads=1):
+        X = _f64(X)
+        Y2 = _f64(Y).reshape(X.shape[0], -1)
+        n, d = X.shape
+        m = Y2.shape[1]
+        rows = np.arange(n, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+        S = np.empty((rows.size, k), dtype=np.int32)
+        Cm = np.empty((rows.size, k, m), dtype=np.float64)
+        self._check(self.L.fmgp_ref_precompute_rows(_p(X), _p(Y2), n, d, m, kind, sigma, rho, nu, tau, k,
+                                                    _p(rows), rows.size, threads, _p(S), _p(Cm)))
+        return S, Cm
+
+    def predict(self, X, S, Cm, kind, sigma, rho, nu, tau, mean_offset, Z, threads=1):
+        X = _f64(X)
+        Z = _f64(Z)
+        S = np.ascontiguousarray(S, dtype=np.int32)
+        n, d = X.shape
+        k = S.shape[1]
+        C3 = _f64(Cm).reshape(n, k, -1)
+        m = C3.shape[2]
+        mos = np.broadcast_to(np.asarray(mean_offset, dtype=np.float64).reshape(-1), (m,))
+        out = np.empty((Z.shape[0], m))
+        nn = np.empty(Z.shape[0], dtype=np.int32)
+        for c in range(m):  # one reference model per output; mean offset is per model
+            Cc = np.ascontiguousarray(C3[:, :, c])
+            oc = np.empty(Z.shape[0])
+            self._check(self.L.fmgp_ref_predict(_p(X), _p(S), _p(Cc), n, d, k, 1, kind, sigma, rho, nu, tau,
+                                                float(mos[c]), _p(Z), Z.shape[0], threads, _p(oc), _p(nn)))
+            out[:, c] = oc
+        return out, nn
+
+    def query_knn(self, X, q, k, exclude=-1):
+        X = _f64(X)
+        q = _f64(q)
+        idx = np.empty(k, dtype=np.int32)
+        dist = np.empty(k, dtype=np.float64)
+        self._check(self.L.fmgp_ref_query_knn(_p(X), X.shape[0], X.shape[1], _p(q), k, exclude, _p(idx), _p(dist)))
+        return idx, dist
+
+    def nearest(self, X, Q):
+        X = _f64(X)
+        Q = _f64(Q).reshape(-1, X.shape[1])
+        out = np.empty(Q.shape[0], dtype=np.int32)
+        self._check(self.L.fmgp_ref_nearest(_p(X), X.shape[0], X.shape[1], _p(Q), Q.shape[0], _p(out)))
+        return out
+
+
+def best_available():
+    """oracle/_ref when it was built (reference-compiled), else the C port."""
+    if REF_PATH.exists():
+        return Reference()
+    return Port()
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1

@@ -1,0 +1,104 @@
+"""ctypes binding of the C ABI in include/fmgp_b200.h (libfmgp_b200.so).
+
+The library is loaded from this package's lib/ directory only; if it is
+missing the import fails loudly — there is no Python or CPU fallback for any
+compute entry point.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_DIR = Path(__file__).resolve().parent / "lib"
+LIB_PATH = LIB_DIR / "libfmgp_b200.so"
+
+FMGP_OK, FMGP_EINVAL, FMGP_ENUMERIC, FMGP_ECUDA = 0, 1, 2, 3
+
+
+class KernelParamsC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("sigma", C.c_double), ("rho", C.c_double),
+                ("nu", C.c_double), ("tau", C.c_double)]
+
+
+_d = C.POINTER(C.c_double)
+_i32 = C.POINTER(C.c_int32)
+_i64 = C.POINTER(C.c_int64)
+_kp = C.POINTER(KernelParamsC)
+_vp = C.c_void_p
+
+# name -> (restype, argtypes); exactly the symbols include/fmgp_b200.h declares.
+SIGNATURES: dict[str, tuple] = {
+    "fmgp_abi_version": (C.c_int, []),
+    "fmgp_last_error": (C.c_char_p, []),
+    "fmgp_launch_count": (C.c_int64, []),
+    "fmgp_device_count": (C.c_int, []),
+    "fmgp_validate_kernel": (C.c_int, [_kp]),
+    "fmgp_precompute": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _kp, C.c_int32, _vp, _vp, _i64]),
+    "fmgp_precompute_device": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _kp, C.c_int32, C.c_int64,
+                                         C.c_int64, _vp, _vp, _i64, _vp]),
+    "fmgp_query_knn": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, C.c_int32, _vp, _vp, _vp]),
+    "fmgp_query_knn_device": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, C.c_int32, C.c_int64, _vp,
+                                        _vp, _vp]),
+    "fmgp_nearest": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp]),
+    "fmgp_nearest_device": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp, _vp]),
+    "fmgp_predict": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _kp, _vp, _vp,
+                               C.c_int64, _vp, _vp]),
+    "fmgp_predict_device": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _kp, _vp, _vp,
+                                      C.c_int64, _vp, _vp, _vp]),
+    "fmgp_model_create": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _kp, _vp,
+                                    C.c_int32, C.POINTER(_vp)]),
+    "fmgp_model_predict": (C.c_int, [_vp, _vp, C.c_int64, _vp, _vp]),
+    "fmgp_model_destroy": (None, [_vp]),
+    "fmgp_cov_matrix": (C.c_int, [_vp, C.c_int64, _vp, C.c_int64, C.c_int32, _kp, _vp]),
+    "fmgp_kernel_values": (C.c_int, [_vp, C.c_int64, _kp, _vp]),
+    "fmgp_solve_spd_batched": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _vp, _vp, _i64]),
+}
+
+
+class FmgpError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class DomainError(FmgpError, ValueError):
+    """std::domain_error in the reference."""
+
+
+class NumericError(FmgpError, ArithmeticError):
+    """fastmuygps::NumericError (errors.hpp:11-14)."""
+
+    def __init__(self, code: int, msg: str, failed_row: int = -1):
+        super().__init__(code, msg)
+        self.failed_row = failed_row
+
+
+class CudaError(FmgpError):
+    """No usable device or a CUDA failure (never silently falls back)."""
+
+
+def load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2205_10879_b200.build` "
+            "(the FastMuyGPs B200 path has no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+LIB = load()
+
+
+def check(rc: int, failed_row: int = -1) -> None:
+    if rc == FMGP_OK:
+        return
+    msg = LIB.fmgp_last_error().decode()
+    if rc == FMGP_EINVAL:
+        raise DomainError(rc, msg)
+    if rc == FMGP_ENUMERIC:
+        raise NumericError(rc, msg, failed_row)
+    raise CudaError(rc, msg)

@@ -1,0 +1,102 @@
+"""Build every native artefact in-tree (no JIT cache), for sm_100a only.
+
+    python -m paper_2205_10879_b200.build            # product + oracle checker
+    python -m paper_2205_10879_b200.build --product  # product only
+
+Outputs (git-ignored, but they travel to the GPU box with the snapshot):
+    paper_2205_10879_b200/lib/libfmgp_b200.so      CUDA kernels + C ABI (include/fmgp_b200.h)
+    paper_2205_10879_b200/lib/libfmgp_datagen.so   seeded host workload generators
+    paper_2205_10879_b200/lib/libfastmuygps_b200.so the C++ facade (reference headers)
+    oracle/build/libfmgp_oracle.so                 C restatement (checker only)
+    oracle/_ref/*                                  reference TUs, when /root/reference exists
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+REPO = PKG.parent
+LIB = PKG / "lib"
+CSRC = PKG / "csrc"
+CPP = PKG / "cpp"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_SOURCES = ["knn.cu", "solve.cu", "predict.cu", "misc.cu", "capi.cu"]
+FACADE_SOURCES = ["kernel.cpp", "linalg.cpp", "nn_index.cpp", "fast_predict.cpp", "dataset.cpp"]
+
+
+def _run(cmd: list[str], cwd: Path | None = None) -> None:
+    print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, cwd=cwd)
+
+
+def _stale(out: Path, deps: list[Path]) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in deps)
+
+
+def build_cuda(force: bool = False) -> Path:
+    out = LIB / "libfmgp_b200.so"
+    deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
+    deps.append(REPO / "include" / "fmgp_b200.h")
+    if force or _stale(out, deps):
+        LIB.mkdir(exist_ok=True)
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+              "-Xptxas", "-O3", "-o", str(out), *[str(CSRC / s) for s in CUDA_SOURCES]])
+    return out
+
+
+def build_datagen(force: bool = False) -> Path:
+    out = LIB / "libfmgp_datagen.so"
+    src = PKG / "datagen" / "datagen.cpp"
+    if force or _stale(out, [src]):
+        LIB.mkdir(exist_ok=True)
+        _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-o", str(out), str(src)])
+    return out
+
+
+def build_facade(force: bool = False) -> Path | None:
+    srcs = [CPP / "src" / s for s in FACADE_SOURCES]
+    if not all(s.exists() for s in srcs):
+        return None
+    out = LIB / "libfastmuygps_b200.so"
+    deps = srcs + list((CPP / "include" / "fastmuygps").glob("*.hpp")) + [LIB / "libfmgp_b200.so"]
+    if force or _stale(out, deps):
+        _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{CPP / 'include'}", f"-I{CPP / 'shim'}",
+              f"-I{REPO / 'include'}", "-o", str(out), *[str(s) for s in srcs],
+              f"-L{LIB}", "-lfmgp_b200", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
+def build_oracle() -> None:
+    """The checker: C restatement always; reference TUs when the reference is mounted."""
+    _run(["make", "-s", "-C", str(REPO / "oracle")])
+    if Path("/root/reference/proj/core/src/fast_predict.cpp").exists():
+        _run(["make", "-s", "-C", str(REPO / "oracle"), "ref"])
+
+
+def build(product_only: bool = False, force: bool = False) -> None:
+    if shutil.which(NVCC) is None and not Path(NVCC).exists():
+        raise RuntimeError(f"nvcc not found at {NVCC}; the B200 path cannot be built")
+    build_cuda(force)
+    build_datagen(force)
+    build_facade(force)
+    if not product_only:
+        build_oracle()
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--product", action="store_true")
+    ap.add_argument("--force", action="store_true")
+    a = ap.parse_args()
+    build(product_only=a.product, force=a.force)
+    sys.exit(0)

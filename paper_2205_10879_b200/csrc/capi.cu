@@ -1,0 +1,515 @@
+// The C ABI (include/fmgp_b200.h): argument checks with the reference's
+// error conventions, device memory and streams, and the stage launchers.
+// There is no CPU compute path: without a usable CUDA device every compute
+// entry point returns FMGP_ECUDA.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fmgp_b200.h"
+#include "fmgp_common.cuh"
+#include "fmgp_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FMGP_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define FMGP_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t fmgp_e_ = (call);                         \
+    if (fmgp_e_ != cudaSuccess) return cuda_fail(fmgp_e_, #call); \
+  } while (0)
+
+int num_sms_current() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+int require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n < 1)
+    return fail(FMGP_ECUDA, std::string("no usable CUDA device (") + cudaGetErrorString(e) +
+                                "); the FastMuyGPs B200 path has no CPU fallback");
+  return FMGP_OK;
+}
+
+// KernelParams (kernel.cpp:13-28) + the device path's nu support; fills KParams.
+int make_kparams(const fmgp_kernel_params* p, fmgp::KParams* kp) {
+  if (p == nullptr) return fail(FMGP_EINVAL, "kernel params must not be null");
+  if (!(std::isfinite(p->sigma) && p->sigma > 0.0))
+    return fail(FMGP_EINVAL, "KernelParams: sigma must be positive and finite");
+  if (!(std::isfinite(p->rho) && p->rho > 0.0))
+    return fail(FMGP_EINVAL, "KernelParams: rho must be positive and finite");
+  if (!(std::isfinite(p->nu) && p->nu > 0.0))
+    return fail(FMGP_EINVAL, "KernelParams: nu must be positive and finite");
+  if (!(std::isfinite(p->tau) && p->tau >= 0.0))
+    return fail(FMGP_EINVAL, "KernelParams: tau must be non-negative and finite");
+  if (p->kind != FMGP_MATERN && p->kind != FMGP_RBF) return fail(FMGP_EINVAL, "unknown kernel kind");
+  kp->kind = p->kind;
+  kp->nu_code = 0;
+  if (p->kind == FMGP_MATERN) {
+    if (p->nu == 0.5) kp->nu_code = 0;
+    else if (p->nu == 1.5) kp->nu_code = 1;
+    else if (p->nu == 2.5) kp->nu_code = 2;
+    else
+      return fail(FMGP_EINVAL,
+                  "Matern nu outside {0.5, 1.5, 2.5} (the reference's GSL Bessel branch, kernel.cpp:40-51) "
+                  "is not implemented on the device path");
+  }
+  kp->s2 = p->sigma * p->sigma;
+  kp->rho = p->rho;
+  kp->diag = kp->s2 * (1.0 + p->tau * p->tau);
+  static const double jit[4] = {0.0, 1e-10, 1e-8, 1e-6};
+  kp->diag_jit[0] = kp->diag;
+  for (int a = 1; a < 4; ++a) kp->diag_jit[a] = kp->diag_jit[a - 1] + (jit[a] - jit[a - 1]);
+  return FMGP_OK;
+}
+
+int check_points(const double* X, int64_t n, int32_t d) {
+  if (n < 1) return fail(FMGP_EINVAL, "NeighborIndex: empty point set");
+  if (d < 1) return fail(FMGP_EINVAL, "NeighborIndex: point dimension must be >= 1");
+  if (n > INT32_MAX) return fail(FMGP_EINVAL, "NeighborIndex: more than 2^31-1 points (int32 indices)");
+  if (X != nullptr) {
+    const int64_t total = n * d;
+    for (int64_t i = 0; i < total; ++i)
+      if (!std::isfinite(X[i])) return fail(FMGP_EINVAL, "NeighborIndex: non-finite coordinates");
+  }
+  return FMGP_OK;
+}
+
+// RAII device buffer on a stream (stream-ordered allocator).
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t alloc(size_t count, cudaStream_t stream) {
+    s = stream;
+    if (count == 0) count = 1;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream);
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+struct Stream {
+  cudaStream_t s = nullptr;
+  cudaError_t create() { return cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); }
+  ~Stream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+
+int precompute_device_impl(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                           const fmgp::KParams& kp, int32_t k, int64_t row_begin, int64_t row_end, int32_t* S_out,
+                           double* C_out, int64_t* failed_row, cudaStream_t stream) {
+  const int64_t nrows = row_end - row_begin;
+  if (failed_row) *failed_row = -1;
+  if (nrows <= 0) return FMGP_OK;
+  const int sms = num_sms_current();
+  if (k > 1) {
+    FMGP_CUDA(fmgp::knn_bruteforce(X + row_begin * d, nrows, X, n, d, k - 1, row_begin, nullptr, 1, S_out, nullptr,
+                                   sms, stream));
+  } else {
+    FMGP_CUDA(fmgp::self_rows_launch(S_out, nrows, row_begin, stream));
+  }
+  DevBuf<unsigned long long> fmin;
+  FMGP_CUDA(fmin.alloc(1, stream));
+  FMGP_CUDA(cudaMemsetAsync(fmin.p, 0xFF, sizeof(unsigned long long), stream));
+  FMGP_CUDA(fmgp::fused_solve(X, Y, d, m, S_out, nrows, row_begin, k, kp, C_out, nullptr, fmin.p, sms, stream));
+  unsigned long long host_min = ~0ull;
+  FMGP_CUDA(cudaMemcpyAsync(&host_min, fmin.p, sizeof(host_min), cudaMemcpyDeviceToHost, stream));
+  FMGP_CUDA(cudaStreamSynchronize(stream));
+  if (host_min != ~0ull) {
+    if (failed_row) *failed_row = static_cast<int64_t>(host_min);
+    return fail(FMGP_ENUMERIC, "Cholesky factorization failed in precompute row " + std::to_string(host_min) +
+                                   " after jitter escalation up to 1e-6");
+  }
+  return FMGP_OK;
+}
+
+int check_solve_shape(int32_t k, int32_t d, int32_t m) {
+  if (m < 1) return fail(FMGP_EINVAL, "number of outputs m must be >= 1");
+  int ld, dchunk;
+  size_t per_warp = fmgp::solve_smem_per_warp(k, d, m, &ld, &dchunk);
+  if (k > fmgp::kMaxK || per_warp > 200 * 1024)
+    return fail(FMGP_EINVAL, "k = " + std::to_string(k) + " with m = " + std::to_string(m) +
+                                 " exceeds the fused solve's shared-memory neighbourhood limit (k <= " +
+                                 std::to_string(fmgp::kMaxK) + ")");
+  return FMGP_OK;
+}
+
+int predict_device_impl(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d, int32_t k,
+                        int32_t m, const fmgp::KParams& kp, const double* mean_offset_dev, const double* Z,
+                        int64_t nz, double* out, int32_t* nn_out, cudaStream_t stream) {
+  if (nz <= 0) return FMGP_OK;
+  const int sms = num_sms_current();
+  DevBuf<int32_t> nn_tmp;
+  int32_t* nn = nn_out;
+  if (nn == nullptr) {
+    FMGP_CUDA(nn_tmp.alloc(static_cast<size_t>(nz), stream));
+    nn = nn_tmp.p;
+  }
+  FMGP_CUDA(fmgp::knn_bruteforce(Z, nz, X, n, d, 1, -1, nullptr, 0, nn, nullptr, sms, stream));
+  FMGP_CUDA(fmgp::predict_gather(X, S, C, d, k, m, kp, mean_offset_dev, Z, nz, nn, out, sms, stream));
+  return FMGP_OK;
+}
+
+}  // namespace
+
+namespace fmgp {
+static std::atomic<int64_t> g_launches{0};
+void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace fmgp
+
+struct fmgp_model {
+  int device = 0;
+  int64_t n = 0;
+  int32_t d = 0, k = 0, m = 0;
+  fmgp::KParams kp{};
+  double* X = nullptr;
+  int32_t* S = nullptr;
+  double* C = nullptr;
+  double* mo = nullptr;
+};
+
+extern "C" {
+
+int fmgp_abi_version(void) { return FMGP_ABI_VERSION; }
+const char* fmgp_last_error(void) { return g_err.c_str(); }
+int64_t fmgp_launch_count(void) { return fmgp::g_launches.load(); }
+
+int fmgp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int fmgp_validate_kernel(const fmgp_kernel_params* p) {
+  fmgp::KParams kp;
+  return make_kparams(p, &kp);
+}
+
+int fmgp_precompute(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                    const fmgp_kernel_params* params, int32_t k, int32_t* S_out, double* C_out,
+                    int64_t* failed_row) {
+  if (failed_row) *failed_row = -1;
+  fmgp::KParams kp;
+  int rc;
+  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
+  if (k < 1 || k > n) return fail(FMGP_EINVAL, "precompute: k out of range");
+  if ((rc = check_points(X, n, d)) != FMGP_OK) return rc;
+  if ((rc = check_solve_shape(k, d, m)) != FMGP_OK) return rc;
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dX, dY, dC;
+  DevBuf<int32_t> dS;
+  FMGP_CUDA(dX.alloc(static_cast<size_t>(n) * d, st.s));
+  FMGP_CUDA(dY.alloc(static_cast<size_t>(n) * m, st.s));
+  FMGP_CUDA(dS.alloc(static_cast<size_t>(n) * k, st.s));
+  FMGP_CUDA(dC.alloc(static_cast<size_t>(n) * k * m, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * n * d, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dY.p, Y, sizeof(double) * n * m, cudaMemcpyHostToDevice, st.s));
+  rc = precompute_device_impl(dX.p, dY.p, n, d, m, kp, k, 0, n, dS.p, dC.p, failed_row, st.s);
+  if (rc != FMGP_OK) return rc;
+  FMGP_CUDA(cudaMemcpyAsync(S_out, dS.p, sizeof(int32_t) * n * k, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(C_out, dC.p, sizeof(double) * n * k * m, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
+int fmgp_precompute_device(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                           const fmgp_kernel_params* params, int32_t k, int64_t row_begin, int64_t row_end,
+                           int32_t* S_out, double* C_out, int64_t* failed_row, void* stream) {
+  if (failed_row) *failed_row = -1;
+  fmgp::KParams kp;
+  int rc;
+  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
+  if (k < 1 || k > n) return fail(FMGP_EINVAL, "precompute: k out of range");
+  if ((rc = check_points(nullptr, n, d)) != FMGP_OK) return rc;
+  if ((rc = check_solve_shape(k, d, m)) != FMGP_OK) return rc;
+  if (row_begin < 0 || row_end > n || row_begin > row_end) return fail(FMGP_EINVAL, "precompute: bad row range");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  return precompute_device_impl(X, Y, n, d, m, kp, k, row_begin, row_end, S_out, C_out, failed_row,
+                                static_cast<cudaStream_t>(stream));
+}
+
+int fmgp_query_knn_device(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq, int32_t k,
+                          int64_t self_offset, int32_t* idx_out, double* dist_sq_out, void* stream) {
+  int rc;
+  if ((rc = check_points(nullptr, np, d)) != FMGP_OK) return rc;
+  if (k < 1 || k > np - (self_offset >= 0 ? 1 : 0)) return fail(FMGP_EINVAL, "query_knn: k out of range");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  FMGP_CUDA(fmgp::knn_bruteforce(Q, nq, P, np, d, k, self_offset, nullptr, 0, idx_out, dist_sq_out,
+                                 num_sms_current(), static_cast<cudaStream_t>(stream)));
+  return FMGP_OK;
+}
+
+int fmgp_query_knn(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq, int32_t k,
+                   const int32_t* exclude, int32_t* idx_out, double* dist_out) {
+  int rc;
+  if ((rc = check_points(P, np, d)) != FMGP_OK) return rc;
+  bool any_excl = false;
+  if (exclude != nullptr)
+    for (int64_t q = 0; q < nq; ++q) any_excl |= exclude[q] >= 0;
+  if (k < 1 || k > np - (any_excl ? 1 : 0)) return fail(FMGP_EINVAL, "query_knn: k out of range");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  if (nq <= 0) return FMGP_OK;
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dP, dQ, dD;
+  DevBuf<int32_t> dI, dE;
+  FMGP_CUDA(dP.alloc(static_cast<size_t>(np) * d, st.s));
+  FMGP_CUDA(dQ.alloc(static_cast<size_t>(nq) * d, st.s));
+  FMGP_CUDA(dI.alloc(static_cast<size_t>(nq) * k, st.s));
+  FMGP_CUDA(dD.alloc(static_cast<size_t>(nq) * k, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dP.p, P, sizeof(double) * np * d, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dQ.p, Q, sizeof(double) * nq * d, cudaMemcpyHostToDevice, st.s));
+  if (exclude != nullptr) {
+    FMGP_CUDA(dE.alloc(static_cast<size_t>(nq), st.s));
+    FMGP_CUDA(cudaMemcpyAsync(dE.p, exclude, sizeof(int32_t) * nq, cudaMemcpyHostToDevice, st.s));
+  }
+  FMGP_CUDA(fmgp::knn_bruteforce(dQ.p, nq, dP.p, np, d, k, -1, dE.p, 0, dI.p, dD.p, num_sms_current(), st.s));
+  FMGP_CUDA(fmgp::sqrt_inplace_launch(dD.p, nq * k, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(idx_out, dI.p, sizeof(int32_t) * nq * k, cudaMemcpyDeviceToHost, st.s));
+  if (dist_out) FMGP_CUDA(cudaMemcpyAsync(dist_out, dD.p, sizeof(double) * nq * k, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
+int fmgp_nearest_device(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq, int32_t* idx_out,
+                        void* stream) {
+  int rc;
+  if ((rc = check_points(nullptr, np, d)) != FMGP_OK) return rc;
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  FMGP_CUDA(fmgp::knn_bruteforce(Q, nq, P, np, d, 1, -1, nullptr, 0, idx_out, nullptr, num_sms_current(),
+                                 static_cast<cudaStream_t>(stream)));
+  return FMGP_OK;
+}
+
+int fmgp_nearest(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq, int32_t* idx_out) {
+  int rc;
+  if ((rc = check_points(P, np, d)) != FMGP_OK) return rc;
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  if (nq <= 0) return FMGP_OK;
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dP, dQ;
+  DevBuf<int32_t> dI;
+  FMGP_CUDA(dP.alloc(static_cast<size_t>(np) * d, st.s));
+  FMGP_CUDA(dQ.alloc(static_cast<size_t>(nq) * d, st.s));
+  FMGP_CUDA(dI.alloc(static_cast<size_t>(nq), st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dP.p, P, sizeof(double) * np * d, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dQ.p, Q, sizeof(double) * nq * d, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(fmgp::knn_bruteforce(dQ.p, nq, dP.p, np, d, 1, -1, nullptr, 0, dI.p, nullptr, num_sms_current(), st.s));
+  FMGP_CUDA(cudaMemcpyAsync(idx_out, dI.p, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
+int fmgp_predict_device(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d, int32_t k,
+                        int32_t m, const fmgp_kernel_params* params, const double* mean_offset, const double* Z,
+                        int64_t nz, double* out, int32_t* nn_out, void* stream) {
+  fmgp::KParams kp;
+  int rc;
+  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
+  if ((rc = check_points(nullptr, n, d)) != FMGP_OK) return rc;
+  if (k < 1 || k > n || m < 1) return fail(FMGP_EINVAL, "predict: bad k or m");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DevBuf<double> mo;
+  FMGP_CUDA(mo.alloc(static_cast<size_t>(m), s));
+  FMGP_CUDA(cudaMemcpyAsync(mo.p, mean_offset, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+  rc = predict_device_impl(X, S, C, n, d, k, m, kp, mo.p, Z, nz, out, nn_out, s);
+  if (rc != FMGP_OK) return rc;
+  // mean_offset may be a pageable stack array: make sure the copy finished.
+  FMGP_CUDA(cudaStreamSynchronize(s));
+  return FMGP_OK;
+}
+
+int fmgp_model_create(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d, int32_t k,
+                      int32_t m, const fmgp_kernel_params* params, const double* mean_offset, int32_t device,
+                      fmgp_model** out) {
+  if (out == nullptr) return fail(FMGP_EINVAL, "model output pointer is null");
+  *out = nullptr;
+  fmgp::KParams kp;
+  int rc;
+  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
+  if ((rc = check_points(X, n, d)) != FMGP_OK) return rc;
+  if (k < 1 || k > n || m < 1) return fail(FMGP_EINVAL, "model: bad k or m");
+  for (int64_t i = 0; i < n; ++i)
+    if (S[i * k] != static_cast<int32_t>(i))
+      return fail(FMGP_EINVAL, "neighbor table row does not start with its own index");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  FMGP_CUDA(cudaSetDevice(device));
+  auto* mdl = new fmgp_model();
+  mdl->device = device;
+  mdl->n = n;
+  mdl->d = d;
+  mdl->k = k;
+  mdl->m = m;
+  mdl->kp = kp;
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = cudaMalloc(&mdl->X, sizeof(double) * n * d);
+  if (e == cudaSuccess) e = cudaMalloc(&mdl->S, sizeof(int32_t) * n * k);
+  if (e == cudaSuccess) e = cudaMalloc(&mdl->C, sizeof(double) * n * k * m);
+  if (e == cudaSuccess) e = cudaMalloc(&mdl->mo, sizeof(double) * m);
+  if (e == cudaSuccess) e = cudaMemcpy(mdl->X, X, sizeof(double) * n * d, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(mdl->S, S, sizeof(int32_t) * n * k, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(mdl->C, C, sizeof(double) * n * k * m, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(mdl->mo, mean_offset, sizeof(double) * m, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    fmgp_model_destroy(mdl);
+    return cuda_fail(e, "fmgp_model_create");
+  }
+  *out = mdl;
+  return FMGP_OK;
+}
+
+int fmgp_model_predict(const fmgp_model* mdl, const double* Z, int64_t nz, double* out, int32_t* nn_out) {
+  if (mdl == nullptr) return fail(FMGP_EINVAL, "null model");
+  if (nz <= 0) return FMGP_OK;
+  FMGP_CUDA(cudaSetDevice(mdl->device));
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dZ, dO;
+  DevBuf<int32_t> dN;
+  FMGP_CUDA(dZ.alloc(static_cast<size_t>(nz) * mdl->d, st.s));
+  FMGP_CUDA(dO.alloc(static_cast<size_t>(nz) * mdl->m, st.s));
+  FMGP_CUDA(dN.alloc(static_cast<size_t>(nz), st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dZ.p, Z, sizeof(double) * nz * mdl->d, cudaMemcpyHostToDevice, st.s));
+  int rc = predict_device_impl(mdl->X, mdl->S, mdl->C, mdl->n, mdl->d, mdl->k, mdl->m, mdl->kp, mdl->mo, dZ.p, nz,
+                               dO.p, dN.p, st.s);
+  if (rc != FMGP_OK) return rc;
+  FMGP_CUDA(cudaMemcpyAsync(out, dO.p, sizeof(double) * nz * mdl->m, cudaMemcpyDeviceToHost, st.s));
+  if (nn_out) FMGP_CUDA(cudaMemcpyAsync(nn_out, dN.p, sizeof(int32_t) * nz, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
+void fmgp_model_destroy(fmgp_model* mdl) {
+  if (mdl == nullptr) return;
+  cudaSetDevice(mdl->device);
+  if (mdl->X) cudaFree(mdl->X);
+  if (mdl->S) cudaFree(mdl->S);
+  if (mdl->C) cudaFree(mdl->C);
+  if (mdl->mo) cudaFree(mdl->mo);
+  delete mdl;
+}
+
+int fmgp_predict(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d, int32_t k, int32_t m,
+                 const fmgp_kernel_params* params, const double* mean_offset, const double* Z, int64_t nz,
+                 double* out, int32_t* nn_out) {
+  int dev = 0;
+  if (require_device() != FMGP_OK) return FMGP_ECUDA;
+  FMGP_CUDA(cudaGetDevice(&dev));
+  fmgp_model* mdl = nullptr;
+  int rc = fmgp_model_create(X, S, C, n, d, k, m, params, mean_offset, dev, &mdl);
+  if (rc != FMGP_OK) return rc;
+  rc = fmgp_model_predict(mdl, Z, nz, out, nn_out);
+  fmgp_model_destroy(mdl);
+  return rc;
+}
+
+int fmgp_cov_matrix(const double* A, int64_t na, const double* B, int64_t nb, int32_t d,
+                    const fmgp_kernel_params* params, double* K_out) {
+  fmgp::KParams kp;
+  int rc;
+  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
+  if (d < 1) return fail(FMGP_EINVAL, "cov_matrix: point sets have mismatched dimension");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  if (B == nullptr) nb = na;
+  if (na * nb == 0) return FMGP_OK;
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dA, dB, dK;
+  FMGP_CUDA(dA.alloc(static_cast<size_t>(na) * d, st.s));
+  FMGP_CUDA(dK.alloc(static_cast<size_t>(na) * nb, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dA.p, A, sizeof(double) * na * d, cudaMemcpyHostToDevice, st.s));
+  if (B != nullptr) {
+    FMGP_CUDA(dB.alloc(static_cast<size_t>(nb) * d, st.s));
+    FMGP_CUDA(cudaMemcpyAsync(dB.p, B, sizeof(double) * nb * d, cudaMemcpyHostToDevice, st.s));
+  }
+  FMGP_CUDA(fmgp::cov_matrix_launch(dA.p, na, B ? dB.p : nullptr, nb, d, kp, dK.p, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(K_out, dK.p, sizeof(double) * na * nb, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
+int fmgp_kernel_values(const double* dist, int64_t ndist, const fmgp_kernel_params* params, double* out) {
+  fmgp::KParams kp;
+  int rc;
+  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
+  for (int64_t i = 0; i < ndist; ++i)
+    if (!(std::isfinite(dist[i]) && dist[i] >= 0.0))
+      return fail(FMGP_EINVAL, "kernel distance must be finite and non-negative");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  if (ndist <= 0) return FMGP_OK;
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dD, dO;
+  FMGP_CUDA(dD.alloc(static_cast<size_t>(ndist), st.s));
+  FMGP_CUDA(dO.alloc(static_cast<size_t>(ndist), st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dD.p, dist, sizeof(double) * ndist, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(fmgp::kernel_values_launch(dD.p, ndist, kp, dO.p, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(out, dO.p, sizeof(double) * ndist, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
+int fmgp_solve_spd_batched(const double* K, const double* B, int64_t batch, int32_t k, int32_t m, double* X_out,
+                           double* applied_jitter, int64_t* failed_index) {
+  if (failed_index) *failed_index = -1;
+  int rc;
+  if (k < 1 || m < 1) return fail(FMGP_EINVAL, "solve_spd: empty system");
+  if ((rc = check_solve_shape(k, 1, m)) != FMGP_OK) return rc;
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  if (batch <= 0) return FMGP_OK;
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dK, dB, dJ;
+  DevBuf<unsigned long long> fmin;
+  FMGP_CUDA(dK.alloc(static_cast<size_t>(batch) * k * k, st.s));
+  FMGP_CUDA(dB.alloc(static_cast<size_t>(batch) * k * m, st.s));
+  FMGP_CUDA(dJ.alloc(static_cast<size_t>(batch), st.s));
+  FMGP_CUDA(fmin.alloc(1, st.s));
+  FMGP_CUDA(cudaMemsetAsync(fmin.p, 0xFF, sizeof(unsigned long long), st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dK.p, K, sizeof(double) * batch * k * k, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dB.p, B, sizeof(double) * batch * k * m, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(fmgp::spd_solve_batched(dK.p, dB.p, batch, k, m, dB.p, dJ.p, fmin.p, num_sms_current(), st.s));
+  unsigned long long host_min = ~0ull;
+  FMGP_CUDA(cudaMemcpyAsync(&host_min, fmin.p, sizeof(host_min), cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(X_out, dB.p, sizeof(double) * batch * k * m, cudaMemcpyDeviceToHost, st.s));
+  if (applied_jitter)
+    FMGP_CUDA(cudaMemcpyAsync(applied_jitter, dJ.p, sizeof(double) * batch, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  if (host_min != ~0ull) {
+    if (failed_index) *failed_index = static_cast<int64_t>(host_min);
+    return fail(FMGP_ENUMERIC, "Cholesky factorization failed after jitter escalation up to 1e-6 (matrix " +
+                                   std::to_string(host_min) + ")");
+  }
+  return FMGP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+// Internal launchers shared by the C-ABI translation unit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+namespace fmgp {
+
+struct KParams;
+
+// Process-wide count of kernel launches (fmgp_launch_count).
+void note_launches(int n);
+
+// Exact kNN: for each query q in [0, nq) the kk smallest (dist_sq, idx) over
+// references [0, np), excluding reference q + self_offset when self_offset >= 0.
+// excl_arr (nullable, nq entries) overrides self_offset with a per-query
+// excluded index (-1: none). Writes nq rows of width kk (+1 when with_self, prefixed by q + self_offset).
+// out_d (optional) receives the kk sorted dist_sq values.
+cudaError_t knn_bruteforce(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk,
+                           int64_t self_offset, const int32_t* excl_arr, int with_self, int32_t* out,
+                           double* out_d, int num_sms, cudaStream_t stream);
+
+size_t solve_smem_per_warp(int k, int d, int m, int* ld, int* dchunk);
+
+cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
+                        int64_t row_begin, int k, const KParams& kp, double* C, int32_t* status,
+                        unsigned long long* fail_min, int num_sms, cudaStream_t stream);
+
+cudaError_t predict_gather(const double* X, const int32_t* S, const double* C, int d, int k, int m,
+                           const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz,
+                           const int32_t* nn, double* out, int num_sms, cudaStream_t stream);
+
+}  // namespace fmgp
+
+namespace fmgp {
+
+// solve_spd on `batch` given k x k matrices (row-major, lower triangle used).
+cudaError_t spd_solve_batched(const double* K, const double* B, int64_t batch, int k, int m, double* X,
+                              double* jit_out, unsigned long long* fail_min, int num_sms, cudaStream_t stream);
+
+// cov_matrix (B != nullptr) or cov_matrix_self (B == nullptr), kernel.cpp:92-119.
+cudaError_t cov_matrix_launch(const double* A, int64_t na, const double* B, int64_t nb, int d, const KParams& kp,
+                              double* K, cudaStream_t stream);
+cudaError_t kernel_values_launch(const double* dist, int64_t n, const KParams& kp, double* out, cudaStream_t stream);
+cudaError_t sqrt_inplace_launch(double* v, int64_t n, cudaStream_t stream);
+cudaError_t self_rows_launch(int32_t* S, int64_t nrows, int64_t row_begin, cudaStream_t stream);
+
+}  // namespace fmgp

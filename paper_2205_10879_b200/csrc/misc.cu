@@ -1,0 +1,93 @@
+// Small element-wise kernels behind the C ABI: the kernel-arithmetic entry
+// points (kernel.cpp:88-119) and helpers for the neighbour table.
+#include "fmgp_common.cuh"
+#include "fmgp_internal.h"
+
+namespace fmgp {
+
+namespace {
+
+// cov_matrix (kernel.cpp:92-104): K(i,j) = kernel(||A_i - B_j||), with the
+// nugget firing on exact coordinate equality. cov_matrix_self (:106-119):
+// diagonal kernel(0), off-diagonal computed once for i < j and mirrored, so
+// the fill is exactly symmetric.
+__global__ void cov_kernel(const double* __restrict__ A, int64_t na, const double* __restrict__ B, int64_t nb,
+                           int d, KParams kp, double* __restrict__ K) {
+  const int64_t total = na * nb;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / nb, j = e - i * nb;
+    double v;
+    if (B == nullptr) {
+      if (i == j) {
+        v = kernel_eval(0.0, kp);
+      } else {
+        const int64_t lo = i < j ? i : j, hi = i < j ? j : i;
+        v = kernel_eval(sqrt(dist_sq_dyn(A + lo * d, A + hi * d, d)), kp);
+      }
+    } else {
+      v = kernel_eval(sqrt(dist_sq_dyn(A + i * d, B + j * d, d)), kp);
+    }
+    K[e] = v;
+  }
+}
+
+__global__ void kernel_values_kernel(const double* __restrict__ dist, int64_t n, KParams kp,
+                                     double* __restrict__ out) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[e] = kernel_eval(dist[e], kp);
+}
+
+__global__ void sqrt_kernel(double* __restrict__ v, int64_t n) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    v[e] = sqrt(v[e]);
+}
+
+__global__ void self_rows_kernel(int32_t* __restrict__ S, int64_t nrows, int64_t row_begin) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nrows;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    S[e] = static_cast<int32_t>(row_begin + e);
+}
+
+unsigned grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace
+
+cudaError_t cov_matrix_launch(const double* A, int64_t na, const double* B, int64_t nb, int d, const KParams& kp,
+                              double* K, cudaStream_t stream) {
+  if (na * nb == 0) return cudaSuccess;
+  cov_kernel<<<grid_for(na * nb), 256, 0, stream>>>(A, na, B, nb, d, kp, K);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t kernel_values_launch(const double* dist, int64_t n, const KParams& kp, double* out,
+                                 cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  kernel_values_kernel<<<grid_for(n), 256, 0, stream>>>(dist, n, kp, out);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t sqrt_inplace_launch(double* v, int64_t n, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  sqrt_kernel<<<grid_for(n), 256, 0, stream>>>(v, n);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t self_rows_launch(int32_t* S, int64_t nrows, int64_t row_begin, cudaStream_t stream) {
+  if (nrows == 0) return cudaSuccess;
+  self_rows_kernel<<<grid_for(nrows), 256, 0, stream>>>(S, nrows, row_begin);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace fmgp

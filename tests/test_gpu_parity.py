@@ -1,0 +1,161 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Neighbour indices bit-exact; coefficients ||dC_i||/||C_i|| <= 1e-9 and
+posterior means |a-b|/(1+|b|) <= 1e-9 (north_star tolerance), on seeded
+inputs from the BASELINE configs at sizes the oracle finishes in seconds.
+"""
+import numpy as np
+import pytest
+
+from helpers import C_TOL, MEAN_TOL, kparams, mean_rel_err, row_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _fit(fm, info):
+    return fm.FittedParams(fm.KernelParams(info.sigma, info.rho, info.nu, info.tau), fm.KernelKind(info.kind))
+
+
+def _run(fm, X, Y, info, k, Z=None, mean_offset=0.0):
+    train = fm.TrainingSet(X, Y if Y.shape[1] > 1 else Y[:, 0], mean_offset)
+    index = fm.NeighborIndex.build(X, fm.IndexMode.Exact)
+    model = fm.precompute(train, _fit(fm, info), index, k)
+    pred = None if Z is None else fm.fast_predict_batch(model, Z)
+    return model, pred
+
+
+@pytest.mark.parametrize("cfg,n,nt", [(1, 10000, 2000), (2, 4000, 500), (3, 800, 100), (4, 1500, 200),
+                                      (5, 4000, 500)])
+def test_precompute_and_predict_match_oracle(fm, port, cfg, n, nt):
+    from paper_2205_10879_b200 import datagen
+    ds = datagen.generate(cfg, n, nt)
+    info = ds.info
+    k = info.k
+    model, pred = _run(fm, ds.X, ds.Y, info, k, ds.Z, ds.mean_offset if info.m > 1 else float(ds.mean_offset[0]))
+    rows = np.arange(n) if n <= 4000 else np.arange(0, n, 3)
+    S_o, C_o = port.precompute_rows(ds.X, ds.Y, *kparams(info), k, rows, threads=8)
+    S = model.S[rows]
+    assert S.dtype == np.int32
+    assert np.array_equal(S, S_o), f"neighbour table differs in {np.sum(np.any(S != S_o, axis=1))} rows"
+    Cg = model.C.reshape(n, k, -1)[rows]
+    err = row_rel_err(Cg, C_o)
+    assert err.max() <= C_TOL, err.max()
+    out_o, nn_o = port.predict(ds.X, model.S, model.C.reshape(n, k, -1), *kparams(info), ds.mean_offset, ds.Z,
+                               threads=8)
+    assert mean_rel_err(pred, out_o.reshape(pred.shape)).max() <= MEAN_TOL
+    nn = model.index.nearest_batch(ds.Z)
+    assert np.array_equal(nn, nn_o)
+
+
+def test_ties_resolve_by_ascending_index(fm):
+    # test_nn_index.cpp:57-70: four copies of one point plus fillers.
+    X = np.array([[0, 0], [0, 0], [0, 0], [0, 0], [5, 5], [6, 6]], dtype=np.float64)
+    index = fm.NeighborIndex.build(X, fm.IndexMode.Exact)
+    nl = index.query_knn([0.1, 0.0], 4)
+    assert nl.indices == [0, 1, 2, 3]
+    assert index.nearest_training_point([0.1, 0.0]) == 0
+
+
+def test_exclusion_is_by_index_identity(fm):
+    # test_nn_index.cpp:72-84
+    X = np.array([[1.0], [1.0], [2.0], [3.0]])
+    index = fm.NeighborIndex.build(X, fm.IndexMode.Exact)
+    nl = index.query_knn(X[0], 3, 0)
+    assert 0 not in nl.indices
+    assert nl.indices[0] == 1
+    assert nl.distances[0] == 0.0
+
+
+def test_exact_mode_matches_brute_force_sort(fm, port):
+    # test_nn_index.cpp:40-55 (300 pts, d=5, k=12, 25 queries) + an independent sort.
+    rng = np.random.default_rng(1)
+    X = rng.random((300, 5))
+    Q = rng.random((25, 5))
+    index = fm.NeighborIndex.build(X, fm.IndexMode.Exact)
+    idx, dist = index.query_knn_batch(Q, 12)
+    for r in range(25):
+        dsq = np.array([port.L.fmgp_oracle_dist_sq(Q[r].ctypes.data, X[i].ctypes.data, 5) for i in range(300)])
+        order = sorted(range(300), key=lambda i: (dsq[i], i))[:12]
+        assert idx[r].tolist() == order
+        assert np.all(np.diff(dist[r]) >= 0)
+
+
+def test_one_training_point_scalar_ratio(fm):
+    # test_fast_predict.cpp:46-59
+    X = np.array([[0.3, 0.4]])
+    train = fm.TrainingSet(X, np.array([2.0]), 0.5)
+    p = fm.KernelParams(1.0, 0.7, 0.5, 0.0)
+    model = fm.precompute(train, fm.FittedParams(p, fm.KernelKind.Matern), fm.NeighborIndex.build(X), 1)
+    z = np.array([0.6, 0.8])
+    d = np.linalg.norm(z - X[0])
+    expected = np.exp(-d / 0.7) * 2.0 + 0.5
+    got = fm.fast_predict_one(model, z)
+    assert abs(got - expected) < 1e-12 * (1 + abs(expected))
+
+
+def test_rows_solve_their_local_systems(fm, port):
+    # test_fast_predict.cpp:61-79 (n=120, d=3, k=12, Matern 1.5, tau=1e-6): residual <= 1e-8.
+    from paper_2205_10879_b200 import datagen
+    X, Y, mo = datagen.random_set(120, 3, 1)
+    p = fm.KernelParams(1.2, 0.5, 1.5, 1e-6)
+    model = fm.precompute(fm.TrainingSet(X, Y, mo), fm.FittedParams(p, fm.KernelKind.Matern),
+                          fm.NeighborIndex.build(X), 12)
+    for i in range(120):
+        assert model.S[i, 0] == i
+        xs = X[model.S[i]]
+        K = port.cov_self(xs, 0, 1.2, 0.5, 1.5, 1e-6)
+        res = K @ model.C[i] - Y[model.S[i]]
+        assert np.abs(res).max() <= 1e-8
+
+
+def test_k_equals_n_recovers_dense_posterior(fm):
+    # test_fast_predict.cpp:81-93: RBF, k = n = 50, dense GP via numpy fp64.
+    from paper_2205_10879_b200 import datagen
+    X, Y, mo = datagen.random_set(50, 2, 2)
+    Z, _, _ = datagen.random_set(25, 2, 3)
+    p = fm.KernelParams(1.0, 0.4, 2.5, 1e-6)
+    fit = fm.FittedParams(p, fm.KernelKind.RBF)
+    model = fm.precompute(fm.TrainingSet(X, Y, mo), fit, fm.NeighborIndex.build(X), 50)
+    fast = fm.fast_predict_batch(model, Z)
+    Kxx = fm.cov_matrix_self(X, fm.KernelKind.RBF, p)
+    Kzx = fm.cov_matrix(Z, X, fm.KernelKind.RBF, p)
+    dense = Kzx @ np.linalg.solve(Kxx, Y) + mo
+    assert np.all(np.abs(fast - dense) <= 1e-8 * (1 + np.abs(dense)))
+
+
+def test_linear_in_y_and_sigma_invariant(fm):
+    # test_fast_predict.cpp:107-134
+    from paper_2205_10879_b200 import datagen
+    X, Y, mo = datagen.random_set(150, 3, 5)
+    Z, _, _ = datagen.random_set(20, 3, 6)
+    p = fm.KernelParams(1.0, 0.5, 2.5, 1e-6)
+    idx = fm.NeighborIndex.build(X)
+    fit = fm.FittedParams(p, fm.KernelKind.Matern)
+    a = fm.fast_predict_batch(fm.precompute(fm.TrainingSet(X, Y, mo), fit, idx, 15), Z)
+    b = fm.fast_predict_batch(fm.precompute(fm.TrainingSet(X, -2.0 * Y, 0.0), fit, idx, 15), Z)
+    c = fm.fast_predict_batch(fm.precompute(fm.TrainingSet(X, Y, 0.0), fit, idx, 15), Z)
+    assert np.abs(b + 2.0 * c).max() <= 1e-10
+    s = fm.fast_predict_batch(fm.precompute(fm.TrainingSet(X, Y, mo), fm.FittedParams(p.with_sigma(10.0),
+                                                                                        fm.KernelKind.Matern),
+                                            idx, 15), Z)
+    assert np.abs(s - a).max() <= 1e-10
+
+
+def test_numeric_error_names_lowest_failing_row(fm, port):
+    # Exact duplicates with tau = 0 give an exactly singular block; with sigma = 1e6
+    # the jitter rungs (<= 1e-6) are below one ulp of the diagonal, so the ladder
+    # is exhausted -> NumericError naming the lowest failing row (linalg.cpp:28-30,
+    # fast_predict.cpp:105; threads = 1 semantics).
+    from oracle.oracle import OracleError
+    X = np.zeros((40, 2))
+    X[:, 0] = np.arange(40) * 10.0
+    X[21] = X[20]
+    Y = np.arange(40, dtype=np.float64)
+    p = fm.KernelParams(1e6, 1.0, 2.5, 0.0)
+    with pytest.raises(OracleError) as eo:
+        port.precompute_rows(X, Y, 1, 1e6, 1.0, 2.5, 0.0, 8)
+    with pytest.raises(fm.NumericError) as ei:
+        fm.precompute(fm.TrainingSet(X, Y, 0.0), fm.FittedParams(p, fm.KernelKind.RBF), fm.NeighborIndex.build(X), 8)
+    assert ei.value.failed_row == eo.value.failed_row
+    assert str(ei.value) == (f"Cholesky factorization failed in precompute row {eo.value.failed_row} "
+                             "after jitter escalation up to 1e-6")

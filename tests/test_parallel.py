@@ -1,0 +1,82 @@
+"""CPU, world_size 2 over gloo: the multi-GPU host logic (row shards ->
+all-gather) assembles the same S and C as a single rank, bit-exactly. The
+per-shard compute is the oracle here (stand-in for fmgp_precompute_device)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Port
+        from paper_2205_10879_b200 import datagen
+        from paper_2205_10879_b200.parallel import sharded_precompute, sharded_predict
+        orc = Port()
+        ds = datagen.generate(5, 301, 37)
+        i = ds.info
+        kp = (i.kind, i.sigma, i.rho, i.nu, i.tau)
+        k = 9
+
+        def shard(b, e):
+            S, C = orc.precompute_rows(ds.X, ds.Y, *kp, k, np.arange(b, e))
+            return torch.from_numpy(S), torch.from_numpy(C)
+
+        S, C = sharded_precompute(ds.X.shape[0], shard)
+
+        def pshard(b, e):
+            out, _ = orc.predict(ds.X, S.numpy(), C.numpy(), *kp, ds.mean_offset, ds.Z[b:e])
+            return torch.from_numpy(out)
+
+        P = sharded_predict(ds.Z.shape[0], pshard, gather=True)
+        if rank == 0:
+            q.put((S.numpy(), C.numpy(), P.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_bounds_cover_rows_once():
+    from paper_2205_10879_b200.parallel import shard_bounds
+    for total in (1, 7, 100, 301):
+        for world in (1, 2, 3, 8):
+            seen = []
+            for r in range(world):
+                b, e, per = shard_bounds(total, world, r)
+                assert e - b <= per
+                seen.extend(range(b, e))
+            assert seen == list(range(total))
+
+
+def test_two_rank_gloo_sharding_is_bit_identical_to_one_rank():
+    from oracle.oracle import Port
+    from paper_2205_10879_b200 import datagen
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    S2, C2, P2 = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    orc = Port()
+    ds = datagen.generate(5, 301, 37)
+    i = ds.info
+    S1, C1 = orc.precompute_rows(ds.X, ds.Y, i.kind, i.sigma, i.rho, i.nu, i.tau, 9)
+    P1, _ = orc.predict(ds.X, S1, C1, i.kind, i.sigma, i.rho, i.nu, i.tau, ds.mean_offset, ds.Z)
+    assert np.array_equal(S1, S2) and np.array_equal(C1, C2) and np.array_equal(P1, P2)
