@@ -113,6 +113,21 @@ int fmgp_nearest(const double* P, int64_t np, int32_t d, const double* Q, int64_
 int fmgp_nearest_device(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq,
                         int32_t* idx_out, void* stream);
 
+/* ---- NeighborIndex handle (nn_index.hpp:33-60, Exact mode) ---------------
+ * A device-resident copy of the points; queries upload only the query
+ * points. Immutable; safe for concurrent queries (nn_index.hpp:28-31).
+ * fmgp_index_distances: distance_to (nn_index.cpp:344-349) of one query q
+ * to cnt stored points idx[], i.e. sqrt(dist_sq); idx out of range ->
+ * FMGP_EINVAL ("distance_to: bad query or index"). */
+typedef struct fmgp_index fmgp_index;
+int fmgp_index_create(const double* P, int64_t np, int32_t d, int32_t device, fmgp_index** out);
+int fmgp_index_query_knn(const fmgp_index* index, const double* Q, int64_t nq, int32_t k,
+                         const int32_t* exclude, int32_t* idx_out, double* dist_out);
+int fmgp_index_nearest(const fmgp_index* index, const double* Q, int64_t nq, int32_t* idx_out);
+int fmgp_index_distances(const fmgp_index* index, const double* q, const int32_t* idx, int64_t cnt,
+                         double* out);
+void fmgp_index_destroy(fmgp_index* index);
+
 /* ---- predict (fast_predict.cpp:132-156) -----------------------------------
  * out[t*m + c] = sum_s kernel(||z_t - x_{S[j,s]}||) C[j,s,c] + mean_offset[c],
  * j = nearest training point of z_t (nn_out, nullable, receives j). */

@@ -41,6 +41,11 @@ SIGNATURES: dict[str, tuple] = {
                                         _vp, _vp]),
     "fmgp_nearest": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp]),
     "fmgp_nearest_device": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp, _vp]),
+    "fmgp_index_create": (C.c_int, [_vp, C.c_int64, C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "fmgp_index_query_knn": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp, _vp, _vp]),
+    "fmgp_index_nearest": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
+    "fmgp_index_distances": (C.c_int, [_vp, _vp, _vp, C.c_int64, _vp]),
+    "fmgp_index_destroy": (None, [_vp]),
     "fmgp_predict": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _kp, _vp, _vp,
                                C.c_int64, _vp, _vp]),
     "fmgp_predict_device": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _kp, _vp, _vp,

@@ -27,8 +27,9 @@ CPP = PKG / "cpp"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SOURCES = ["knn.cu", "solve.cu", "predict.cu", "misc.cu", "capi.cu"]
-FACADE_SOURCES = ["kernel.cpp", "linalg.cpp", "nn_index.cpp", "fast_predict.cpp", "dataset.cpp"]
+CUDA_SOURCES = ["knn.cu", "knn_grid.cu", "solve.cu", "solve_big.cu", "predict.cu", "misc.cu", "capi.cu"]
+FACADE_SOURCES = ["facade_kernel.cpp", "facade_linalg.cpp", "facade_nn_index.cpp", "facade_fast_predict.cpp",
+                  "facade_dataset.cpp"]
 
 
 def _run(cmd: list[str], cwd: Path | None = None) -> None:
@@ -46,7 +47,7 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 def build_cuda(force: bool = False) -> Path:
     out = LIB / "libfmgp_b200.so"
     deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
-    deps.append(REPO / "include" / "fmgp_b200.h")
+    deps += [REPO / "include" / "fmgp_b200.h", Path(__file__)]
     if force or _stale(out, deps):
         LIB.mkdir(exist_ok=True)
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
@@ -68,11 +69,12 @@ def build_facade(force: bool = False) -> Path | None:
     if not all(s.exists() for s in srcs):
         return None
     out = LIB / "libfastmuygps_b200.so"
-    deps = srcs + list((CPP / "include" / "fastmuygps").glob("*.hpp")) + [LIB / "libfmgp_b200.so"]
+    deps = srcs + list((CPP / "include" / "fastmuygps").glob("*.hpp")) + list((CPP / "src").glob("*.hpp"))
+    deps += [LIB / "libfmgp_b200.so", Path(__file__)]
     if force or _stale(out, deps):
         _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{CPP / 'include'}", f"-I{CPP / 'shim'}",
               f"-I{REPO / 'include'}", "-o", str(out), *[str(s) for s in srcs],
-              f"-L{LIB}", "-lfmgp_b200", "-Wl,-rpath,$ORIGIN"])
+              f"-L{LIB}", "-lfmgp_b200", "-lz", "-Wl,-rpath,$ORIGIN"])
     return out
 
 

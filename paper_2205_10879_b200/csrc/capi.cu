@@ -68,11 +68,11 @@ int make_kparams(const fmgp_kernel_params* p, fmgp::KParams* kp) {
     if (p->nu == 0.5) kp->nu_code = 0;
     else if (p->nu == 1.5) kp->nu_code = 1;
     else if (p->nu == 2.5) kp->nu_code = 2;
-    else
-      return fail(FMGP_EINVAL,
-                  "Matern nu outside {0.5, 1.5, 2.5} (the reference's GSL Bessel branch, kernel.cpp:40-51) "
-                  "is not implemented on the device path");
+    else kp->nu_code = 3;
   }
+  kp->nu = p->nu;
+  kp->sqrt2nu = std::sqrt(2.0 * p->nu);
+  kp->c0 = (1.0 - p->nu) * 0.69314718055994530942 - std::lgamma(p->nu);
   kp->s2 = p->sigma * p->sigma;
   kp->rho = p->rho;
   kp->diag = kp->s2 * (1.0 + p->tau * p->tau);
@@ -128,7 +128,7 @@ int precompute_device_impl(const double* X, const double* Y, int64_t n, int32_t 
   if (nrows <= 0) return FMGP_OK;
   const int sms = num_sms_current();
   if (k > 1) {
-    FMGP_CUDA(fmgp::knn_bruteforce(X + row_begin * d, nrows, X, n, d, k - 1, row_begin, nullptr, 1, S_out, nullptr,
+    FMGP_CUDA(fmgp::knn_exact(X + row_begin * d, nrows, X, n, d, k - 1, row_begin, nullptr, 1, S_out, nullptr,
                                    sms, stream));
   } else {
     FMGP_CUDA(fmgp::self_rows_launch(S_out, nrows, row_begin, stream));
@@ -149,13 +149,9 @@ int precompute_device_impl(const double* X, const double* Y, int64_t n, int32_t 
 }
 
 int check_solve_shape(int32_t k, int32_t d, int32_t m) {
+  (void)k;
+  (void)d;
   if (m < 1) return fail(FMGP_EINVAL, "number of outputs m must be >= 1");
-  int ld, dchunk;
-  size_t per_warp = fmgp::solve_smem_per_warp(k, d, m, &ld, &dchunk);
-  if (k > fmgp::kMaxK || per_warp > 200 * 1024)
-    return fail(FMGP_EINVAL, "k = " + std::to_string(k) + " with m = " + std::to_string(m) +
-                                 " exceeds the fused solve's shared-memory neighbourhood limit (k <= " +
-                                 std::to_string(fmgp::kMaxK) + ")");
   return FMGP_OK;
 }
 
@@ -170,7 +166,7 @@ int predict_device_impl(const double* X, const int32_t* S, const double* C, int6
     FMGP_CUDA(nn_tmp.alloc(static_cast<size_t>(nz), stream));
     nn = nn_tmp.p;
   }
-  FMGP_CUDA(fmgp::knn_bruteforce(Z, nz, X, n, d, 1, -1, nullptr, 0, nn, nullptr, sms, stream));
+  FMGP_CUDA(fmgp::knn_exact(Z, nz, X, n, d, 1, -1, nullptr, 0, nn, nullptr, sms, stream));
   FMGP_CUDA(fmgp::predict_gather(X, S, C, d, k, m, kp, mean_offset_dev, Z, nz, nn, out, sms, stream));
   return FMGP_OK;
 }
@@ -181,6 +177,13 @@ namespace fmgp {
 static std::atomic<int64_t> g_launches{0};
 void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 }  // namespace fmgp
+
+struct fmgp_index {
+  int device = 0;
+  int64_t n = 0;
+  int32_t d = 0;
+  double* P = nullptr;
+};
 
 struct fmgp_model {
   int device = 0;
@@ -261,7 +264,7 @@ int fmgp_query_knn_device(const double* P, int64_t np, int32_t d, const double* 
   if ((rc = check_points(nullptr, np, d)) != FMGP_OK) return rc;
   if (k < 1 || k > np - (self_offset >= 0 ? 1 : 0)) return fail(FMGP_EINVAL, "query_knn: k out of range");
   if ((rc = require_device()) != FMGP_OK) return rc;
-  FMGP_CUDA(fmgp::knn_bruteforce(Q, nq, P, np, d, k, self_offset, nullptr, 0, idx_out, dist_sq_out,
+  FMGP_CUDA(fmgp::knn_exact(Q, nq, P, np, d, k, self_offset, nullptr, 0, idx_out, dist_sq_out,
                                  num_sms_current(), static_cast<cudaStream_t>(stream)));
   return FMGP_OK;
 }
@@ -290,7 +293,7 @@ int fmgp_query_knn(const double* P, int64_t np, int32_t d, const double* Q, int6
     FMGP_CUDA(dE.alloc(static_cast<size_t>(nq), st.s));
     FMGP_CUDA(cudaMemcpyAsync(dE.p, exclude, sizeof(int32_t) * nq, cudaMemcpyHostToDevice, st.s));
   }
-  FMGP_CUDA(fmgp::knn_bruteforce(dQ.p, nq, dP.p, np, d, k, -1, dE.p, 0, dI.p, dD.p, num_sms_current(), st.s));
+  FMGP_CUDA(fmgp::knn_exact(dQ.p, nq, dP.p, np, d, k, -1, dE.p, 0, dI.p, dD.p, num_sms_current(), st.s));
   FMGP_CUDA(fmgp::sqrt_inplace_launch(dD.p, nq * k, st.s));
   FMGP_CUDA(cudaMemcpyAsync(idx_out, dI.p, sizeof(int32_t) * nq * k, cudaMemcpyDeviceToHost, st.s));
   if (dist_out) FMGP_CUDA(cudaMemcpyAsync(dist_out, dD.p, sizeof(double) * nq * k, cudaMemcpyDeviceToHost, st.s));
@@ -303,7 +306,7 @@ int fmgp_nearest_device(const double* P, int64_t np, int32_t d, const double* Q,
   int rc;
   if ((rc = check_points(nullptr, np, d)) != FMGP_OK) return rc;
   if ((rc = require_device()) != FMGP_OK) return rc;
-  FMGP_CUDA(fmgp::knn_bruteforce(Q, nq, P, np, d, 1, -1, nullptr, 0, idx_out, nullptr, num_sms_current(),
+  FMGP_CUDA(fmgp::knn_exact(Q, nq, P, np, d, 1, -1, nullptr, 0, idx_out, nullptr, num_sms_current(),
                                  static_cast<cudaStream_t>(stream)));
   return FMGP_OK;
 }
@@ -322,8 +325,103 @@ int fmgp_nearest(const double* P, int64_t np, int32_t d, const double* Q, int64_
   FMGP_CUDA(dI.alloc(static_cast<size_t>(nq), st.s));
   FMGP_CUDA(cudaMemcpyAsync(dP.p, P, sizeof(double) * np * d, cudaMemcpyHostToDevice, st.s));
   FMGP_CUDA(cudaMemcpyAsync(dQ.p, Q, sizeof(double) * nq * d, cudaMemcpyHostToDevice, st.s));
-  FMGP_CUDA(fmgp::knn_bruteforce(dQ.p, nq, dP.p, np, d, 1, -1, nullptr, 0, dI.p, nullptr, num_sms_current(), st.s));
+  FMGP_CUDA(fmgp::knn_exact(dQ.p, nq, dP.p, np, d, 1, -1, nullptr, 0, dI.p, nullptr, num_sms_current(), st.s));
   FMGP_CUDA(cudaMemcpyAsync(idx_out, dI.p, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
+int fmgp_index_create(const double* P, int64_t np, int32_t d, int32_t device, fmgp_index** out) {
+  if (out == nullptr) return fail(FMGP_EINVAL, "index output pointer is null");
+  *out = nullptr;
+  int rc;
+  if ((rc = check_points(P, np, d)) != FMGP_OK) return rc;
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  FMGP_CUDA(cudaSetDevice(device));
+  auto* ix = new fmgp_index();
+  ix->device = device;
+  ix->n = np;
+  ix->d = d;
+  cudaError_t e = cudaMalloc(&ix->P, sizeof(double) * np * d);
+  if (e == cudaSuccess) e = cudaMemcpy(ix->P, P, sizeof(double) * np * d, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    fmgp_index_destroy(ix);
+    return cuda_fail(e, "fmgp_index_create");
+  }
+  *out = ix;
+  return FMGP_OK;
+}
+
+void fmgp_index_destroy(fmgp_index* ix) {
+  if (ix == nullptr) return;
+  cudaSetDevice(ix->device);
+  if (ix->P) cudaFree(ix->P);
+  delete ix;
+}
+
+int fmgp_index_query_knn(const fmgp_index* ix, const double* Q, int64_t nq, int32_t k, const int32_t* exclude,
+                         int32_t* idx_out, double* dist_out) {
+  if (ix == nullptr) return fail(FMGP_EINVAL, "null index");
+  bool any_excl = false;
+  if (exclude != nullptr)
+    for (int64_t q = 0; q < nq; ++q) any_excl |= exclude[q] >= 0;
+  if (k < 1 || k > ix->n - (any_excl ? 1 : 0)) return fail(FMGP_EINVAL, "query_knn: k out of range");
+  if (nq <= 0) return FMGP_OK;
+  FMGP_CUDA(cudaSetDevice(ix->device));
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dQ, dD;
+  DevBuf<int32_t> dI, dE;
+  FMGP_CUDA(dQ.alloc(static_cast<size_t>(nq) * ix->d, st.s));
+  FMGP_CUDA(dI.alloc(static_cast<size_t>(nq) * k, st.s));
+  FMGP_CUDA(dD.alloc(static_cast<size_t>(nq) * k, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dQ.p, Q, sizeof(double) * nq * ix->d, cudaMemcpyHostToDevice, st.s));
+  if (any_excl) {
+    FMGP_CUDA(dE.alloc(static_cast<size_t>(nq), st.s));
+    FMGP_CUDA(cudaMemcpyAsync(dE.p, exclude, sizeof(int32_t) * nq, cudaMemcpyHostToDevice, st.s));
+  }
+  FMGP_CUDA(fmgp::knn_exact(dQ.p, nq, ix->P, ix->n, ix->d, k, -1, dE.p, 0, dI.p, dD.p, num_sms_current(), st.s));
+  FMGP_CUDA(fmgp::sqrt_inplace_launch(dD.p, nq * k, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(idx_out, dI.p, sizeof(int32_t) * nq * k, cudaMemcpyDeviceToHost, st.s));
+  if (dist_out) FMGP_CUDA(cudaMemcpyAsync(dist_out, dD.p, sizeof(double) * nq * k, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
+int fmgp_index_nearest(const fmgp_index* ix, const double* Q, int64_t nq, int32_t* idx_out) {
+  if (ix == nullptr) return fail(FMGP_EINVAL, "null index");
+  if (nq <= 0) return FMGP_OK;
+  FMGP_CUDA(cudaSetDevice(ix->device));
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dQ;
+  DevBuf<int32_t> dI;
+  FMGP_CUDA(dQ.alloc(static_cast<size_t>(nq) * ix->d, st.s));
+  FMGP_CUDA(dI.alloc(static_cast<size_t>(nq), st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dQ.p, Q, sizeof(double) * nq * ix->d, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(fmgp::knn_exact(dQ.p, nq, ix->P, ix->n, ix->d, 1, -1, nullptr, 0, dI.p, nullptr, num_sms_current(), st.s));
+  FMGP_CUDA(cudaMemcpyAsync(idx_out, dI.p, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
+int fmgp_index_distances(const fmgp_index* ix, const double* q, const int32_t* idx, int64_t cnt, double* out) {
+  if (ix == nullptr) return fail(FMGP_EINVAL, "null index");
+  for (int64_t e = 0; e < cnt; ++e)
+    if (idx[e] < 0 || idx[e] >= ix->n) return fail(FMGP_EINVAL, "distance_to: bad query or index");
+  if (cnt <= 0) return FMGP_OK;
+  FMGP_CUDA(cudaSetDevice(ix->device));
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dq, dO;
+  DevBuf<int32_t> dI;
+  FMGP_CUDA(dq.alloc(static_cast<size_t>(ix->d), st.s));
+  FMGP_CUDA(dI.alloc(static_cast<size_t>(cnt), st.s));
+  FMGP_CUDA(dO.alloc(static_cast<size_t>(cnt), st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dq.p, q, sizeof(double) * ix->d, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dI.p, idx, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(fmgp::distances_launch(ix->P, ix->d, dq.p, dI.p, cnt, dO.p, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(out, dO.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st.s));
   FMGP_CUDA(cudaStreamSynchronize(st.s));
   return FMGP_OK;
 }

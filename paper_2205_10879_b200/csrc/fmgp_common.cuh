@@ -15,10 +15,126 @@ constexpr int kMaxK = 160;  // largest neighbourhood the fused solve stages in s
 // attempt a of linalg.cpp:13-19 (cumulative `+= jitter - previous`).
 struct KParams {
   int kind;
-  int nu_code;  // 0: nu=0.5, 1: nu=1.5, 2: nu=2.5 (Matern); unused for RBF
+  int nu_code;  // 0: nu=0.5, 1: nu=1.5, 2: nu=2.5, 3: general nu (Matern); unused for RBF
   double s2, rho, diag;
   double diag_jit[4];
+  // general nu (kernel.cpp:40-51, :72-74): x = sqrt(2 nu) d / rho and
+  // log bracket = c0 + nu log x + log K_nu(x), c0 = (1 - nu) ln 2 - lgamma(nu)
+  // (host-evaluated with the reference's own std:: calls).
+  double nu, sqrt2nu, c0;
 };
+
+// log K_nu(x) for x > 0, nu >= 0 — the quantity the reference takes from
+// GSL's gsl_sf_bessel_lnKnu_e (kernel.cpp:42). Own implementation:
+// K_mu and K_{mu+1} for mu = nu - round(nu) in [-1/2, 1/2) from Temme's
+// series (x <= 2) or Steed's continued fraction CF2 (x > 2), then the stable
+// upward recurrence K_{m+1} = 2m/x K_m + K_{m-1}, with a running log scale so
+// large nu cannot overflow. The 1/Gamma(1 +- mu) terms of Temme's series come
+// from the zeta-series of log Gamma(1+z) split into even/odd parts, which
+// keeps gam1 = (1/G(1-mu) - 1/G(1+mu)) / (2 mu) free of cancellation.
+// zeta(k), k = 2..10 (index k); larger k are summed directly.
+__constant__ double kZeta[11] = {0, 0, 1.6449340668482264, 1.2020569031595943, 1.0823232337111382,
+                                 1.0369277551433699, 1.0173430619844491, 1.0083492773819228, 1.0040773561979443,
+                                 1.0020083928260822, 1.0009945751278181};
+
+__device__ inline double ln_bessel_k(double nu, double x) {
+  const double kEps = 1e-16;
+  const double kEuler = 0.57721566490153286061;
+  const double kPi = 3.14159265358979323846;
+  const int nl = static_cast<int>(nu + 0.5);
+  const double mu = nu - nl;
+  const double mu2 = mu * mu;
+  const double xi = 1.0 / x, xi2 = 2.0 * xi;
+  double rkmu, rk1;
+  if (x < 2.0) {
+    double even = 0.0, odd_over_mu = kEuler, pw = mu;  // pw = mu^(k-1)
+    for (int k = 2; k <= 60; ++k) {
+      double z;
+      if (k <= 10) {
+        z = kZeta[k];
+      } else {
+        z = 1.0;
+        for (int j = 2; j <= 12; ++j) z += pow(static_cast<double>(j), -static_cast<double>(k));
+      }
+      pw *= (k == 2 ? 1.0 : mu);  // mu^(k-1) for k >= 2 starting at mu^1
+      const double term = z / k;
+      if (k % 2 == 0) even -= term * pw * mu;   // -zeta(k) mu^k / k
+      else odd_over_mu += term * pw;            // zeta(k) mu^(k-1) / k
+      if (fabs(term * pw) < 1e-18) break;
+    }
+    const double odd = odd_over_mu * mu;
+    const double eev = exp(even);
+    const double shc = fabs(odd) < 1e-8 ? 1.0 + odd * odd / 6.0 : sinh(odd) / odd;
+    const double gam1 = -eev * shc * odd_over_mu;     // (1/G(1-mu) - 1/G(1+mu)) / (2 mu)
+    const double gam2 = eev * cosh(odd);              // (1/G(1-mu) + 1/G(1+mu)) / 2
+    const double gampl = exp(even + odd);             // 1/G(1+mu)
+    const double gammi = exp(even - odd);             // 1/G(1-mu)
+    const double x2 = 0.5 * x;
+    const double pimu = kPi * mu;
+    const double fact = fabs(pimu) < kEps ? 1.0 : pimu / sin(pimu);
+    double d = -log(x2);
+    double e = mu * d;
+    const double fact2 = fabs(e) < kEps ? 1.0 : sinh(e) / e;
+    double ff = fact * (gam1 * cosh(e) + gam2 * fact2 * d);
+    double sum = ff;
+    e = exp(e);
+    double p = 0.5 * e / gampl;
+    double q = 0.5 / (e * gammi);
+    double c = 1.0;
+    d = x2 * x2;
+    double sum1 = p;
+    for (int i = 1; i < 1000; ++i) {
+      ff = (i * ff + p + q) / (i * static_cast<double>(i) - mu2);
+      c *= d / i;
+      p /= (i - mu);
+      q /= (i + mu);
+      const double del = c * ff;
+      sum += del;
+      sum1 += c * (p - i * ff);
+      if (fabs(del) < fabs(sum) * kEps) break;
+    }
+    rkmu = sum;
+    rk1 = sum1 * xi2;
+  } else {
+    double b = 2.0 * (1.0 + x);
+    double d = 1.0 / b;
+    double h = d, delh = d;
+    double q1 = 0.0, q2 = 1.0;
+    const double a1 = 0.25 - mu2;
+    double q = a1, c = a1, a = -a1;
+    double s = 1.0 + q * delh;
+    for (int i = 2; i < 100000; ++i) {
+      a -= 2 * (i - 1);
+      c = -a * c / i;
+      const double qnew = (q1 - b * q2) / a;
+      q1 = q2;
+      q2 = qnew;
+      q += c * qnew;
+      b += 2.0;
+      d = 1.0 / (b + a * d);
+      delh = (b * d - 1.0) * delh;
+      h += delh;
+      const double dels = q * delh;
+      s += dels;
+      if (fabs(dels / s) < kEps) break;
+    }
+    h = a1 * h;
+    rkmu = sqrt(kPi / (2.0 * x)) * exp(-x) / s;
+    rk1 = rkmu * (mu + x + 0.5 - h) * xi;
+  }
+  double logscale = 0.0;
+  for (int i = 1; i <= nl; ++i) {
+    const double t = (mu + i) * xi2 * rk1 + rkmu;
+    rkmu = rk1;
+    rk1 = t;
+    if (rk1 > 1e250) {
+      rkmu *= 1e-250;
+      rk1 *= 1e-250;
+      logscale += 575.64627324851142;  // 250 ln 10
+    }
+  }
+  return log(rkmu) + logscale;
+}
 
 // The reference's neighbour key, nn_index.cpp:73-81: s = 0; s += diff*diff in
 // ascending t, with no FMA contraction (explicit _rn intrinsics). The first
@@ -58,9 +174,12 @@ __device__ __forceinline__ double kernel_eval(double dist, const KParams& p) {
   } else if (p.nu_code == 1) {  // a = sqrt(3) d / rho; (1 + a) e^{-a}
     double a = __ddiv_rn(__dmul_rn(1.7320508075688772, dist), p.rho);
     br = __dmul_rn(__dadd_rn(1.0, a), exp(-a));
-  } else {  // a = sqrt(5) d / rho; (1 + a + a^2/3) e^{-a}
+  } else if (p.nu_code == 2) {  // a = sqrt(5) d / rho; (1 + a + a^2/3) e^{-a}
     double a = __ddiv_rn(__dmul_rn(2.2360679774997898, dist), p.rho);
     br = __dmul_rn(__dadd_rn(__dadd_rn(1.0, a), __ddiv_rn(__dmul_rn(a, a), 3.0)), exp(-a));
+  } else {  // general nu: exp(c0 + nu log x + log K_nu(x)), x = sqrt(2 nu) d / rho
+    double x = __ddiv_rn(__dmul_rn(p.sqrt2nu, dist), p.rho);
+    br = exp(__dadd_rn(__dadd_rn(p.c0, __dmul_rn(p.nu, log(x))), ln_bessel_k(p.nu, x)));
   }
   return __dmul_rn(p.s2, br);
 }

@@ -46,5 +46,35 @@ cudaError_t cov_matrix_launch(const double* A, int64_t na, const double* B, int6
 cudaError_t kernel_values_launch(const double* dist, int64_t n, const KParams& kp, double* out, cudaStream_t stream);
 cudaError_t sqrt_inplace_launch(double* v, int64_t n, cudaStream_t stream);
 cudaError_t self_rows_launch(int32_t* S, int64_t nrows, int64_t row_begin, cudaStream_t stream);
+cudaError_t distances_launch(const double* P, int d, const double* q, const int32_t* idx, int64_t cnt, double* out,
+                             cudaStream_t stream);
+
+}  // namespace fmgp
+
+namespace fmgp {
+
+// Exact kNN through a uniform cell grid (d <= 3, kk <= 128); same contract as
+// knn_bruteforce (excl_arr only with external queries).
+bool knn_grid_supported(int d, int kk);
+cudaError_t knn_grid(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
+                     const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
+                     cudaStream_t stream);
+
+// Dispatcher used by the C ABI: the grid search where it applies, else brute
+// force. FMGP_KNN=brute in the environment forces brute force (A/B checks).
+cudaError_t knn_exact(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
+                      const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
+                      cudaStream_t stream);
+
+}  // namespace fmgp
+
+namespace fmgp {
+
+// CTA-per-neighbourhood fallbacks with a global-memory workspace (any k).
+cudaError_t fused_solve_big(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
+                            int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
+                            int num_sms, cudaStream_t stream);
+cudaError_t spd_solve_big(const double* K, const double* B, int64_t batch, int k, int m, double* X, double* jit_out,
+                          unsigned long long* fail_min, int num_sms, cudaStream_t stream);
 
 }  // namespace fmgp

@@ -19,6 +19,8 @@
 //    in ascending-t order so the key is still bit-exact.
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
+#include <string>
 
 #include "fmgp_common.cuh"
 #include "fmgp_internal.h"
@@ -290,6 +292,22 @@ cudaError_t knn_bruteforce(const double* Q, int64_t nq, const double* P, int64_t
   cudaFreeAsync(wd, stream);
   cudaFreeAsync(wi, stream);
   return cudaGetLastError();
+}
+
+}  // namespace fmgp
+
+namespace fmgp {
+
+cudaError_t knn_exact(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
+                      const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
+                      cudaStream_t stream) {
+  static const bool force_brute = [] {
+    const char* e = std::getenv("FMGP_KNN");
+    return e != nullptr && std::string(e) == "brute";
+  }();
+  if (!force_brute && knn_grid_supported(d, kk))
+    return knn_grid(Q, nq, P, np, d, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
+  return knn_bruteforce(Q, nq, P, np, d, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
 }
 
 }  // namespace fmgp

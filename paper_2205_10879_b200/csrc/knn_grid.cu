@@ -1,0 +1,640 @@
+// K1-grid — exact k-nearest neighbours for low dimension (d <= 3) through a
+// uniform cell grid, bit-exact with the reference's Exact NeighborIndex
+// (proj/core/src/nn_index.cpp:254-287, :351-366).
+//
+// The reference scans all n points per query (O(n^2 d) for precompute). For
+// d <= 3 the same answer is found by examining only the points in the cells
+// around the query: cells are visited as a block of radius 1 and then in
+// rings of growing Chebyshev radius, and the search stops once every point
+// outside the visited block is provably farther than the current k-th
+// neighbour. "Provably" uses the computed key itself: the stop test compares
+// the k-th key against (lower bound - margin)^2 with a margin far above any
+// rounding in the cell assignment, so the neighbour set and order are the
+// reference's, not an approximation.
+//
+// Layout in HBM (built per call, O(n)):
+//   cell id   key(x) = ((c_z * G_y) + c_y) * G_x + c_x, c_t = floor((x_t - lo_t) / h) clamped
+//   cstart    n_cells + 1 offsets (counting sort by key)
+//   pts       n x d f64, points in cell order;  pid  n int32 original indices
+// Rows of cells along x are contiguous, so a block of radius r is (2r+1)^(d-1)
+// contiguous ranges.
+//
+// Query side: one warp per query. Candidates are evaluated 32 at a time
+// (one per lane, coalesced loads from `pts`); a ballot skips batches with no
+// candidate below the current k-th key; otherwise the batch is bitonic-sorted
+// across lanes and merged into the warp's sorted top-KP list, which lives in
+// registers (E = KP/32 entries per lane, lane-strided). Order is the
+// reference's (dist_sq, index) pair order.
+#include <cfloat>
+#include <climits>
+#include <cstdlib>
+
+#include "fmgp_common.cuh"
+#include "fmgp_internal.h"
+
+namespace fmgp {
+
+namespace {
+
+struct GridParams {
+  double lo[3];
+  double h, inv_h;
+  int G[3];
+  int d;
+  int64_t ncells;
+};
+
+// ---------------------------------------------------------------- build
+
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+  unsigned long long b = (k & 0x8000000000000000ull) ? (k & ~0x8000000000000000ull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__global__ void bbox_kernel(const double* __restrict__ X, int64_t n, int d, unsigned long long* __restrict__ mm) {
+  unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    for (int t = 0; t < d; ++t) {
+      unsigned long long k = ord_key(X[i * d + t]);
+      lo[t] = k < lo[t] ? k : lo[t];
+      hi[t] = k > hi[t] ? k : hi[t];
+    }
+  }
+  for (int t = 0; t < d; ++t) {
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long a = __shfl_xor_sync(0xffffffffu, lo[t], o);
+      unsigned long long b = __shfl_xor_sync(0xffffffffu, hi[t], o);
+      lo[t] = a < lo[t] ? a : lo[t];
+      hi[t] = b > hi[t] ? b : hi[t];
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&mm[2 * t], lo[t]);
+      atomicMax(&mm[2 * t + 1], hi[t]);
+    }
+  }
+}
+
+// Cubic cells with ~`per_cell` points on average over the bounding box;
+// degenerate (zero-extent) dimensions get one cell. Capped at max_cells.
+__global__ void grid_params_kernel(const unsigned long long* __restrict__ mm, int64_t n, int d, double per_cell,
+                                   int64_t max_cells, GridParams* __restrict__ gp) {
+  double lo[3], ext[3];
+  double vol = 1.0;
+  int live = 0;
+  for (int t = 0; t < d; ++t) {
+    lo[t] = ord_val(mm[2 * t]);
+    ext[t] = ord_val(mm[2 * t + 1]) - lo[t];
+    if (ext[t] > 0.0) {
+      vol *= ext[t];
+      ++live;
+    }
+  }
+  double cells = fmax(1.0, static_cast<double>(n) / per_cell);
+  double h = live > 0 ? pow(vol / cells, 1.0 / live) : 1.0;
+  int G[3] = {1, 1, 1};
+  for (int iter = 0; iter < 64; ++iter) {
+    double total = 1.0;
+    for (int t = 0; t < d; ++t) {
+      double g = ext[t] > 0.0 ? ceil(ext[t] / h) : 1.0;
+      g = fmin(fmax(g, 1.0), 1048576.0);
+      G[t] = static_cast<int>(g);
+      total *= g;
+    }
+    if (total <= static_cast<double>(max_cells)) break;
+    h *= 1.25;
+  }
+  GridParams p;
+  p.d = d;
+  p.h = h;
+  p.inv_h = 1.0 / h;
+  p.ncells = 1;
+  for (int t = 0; t < 3; ++t) {
+    p.lo[t] = t < d ? lo[t] : 0.0;
+    p.G[t] = t < d ? G[t] : 1;
+    p.ncells *= p.G[t];
+  }
+  *gp = p;
+}
+
+__device__ __forceinline__ int cell_coord(double x, double lo, double inv_h, int G) {
+  double f = floor(__dmul_rn(__dsub_rn(x, lo), inv_h));
+  int c = f < 0.0 ? 0 : (f >= static_cast<double>(G) ? G - 1 : static_cast<int>(f));
+  return c;
+}
+
+template <int D>
+__device__ __forceinline__ int64_t cell_key(const double* x, const GridParams& g, int c[3]) {
+#pragma unroll
+  for (int t = 0; t < 3; ++t) c[t] = t < D ? cell_coord(x[t], g.lo[t], g.inv_h, g.G[t]) : 0;
+  return (static_cast<int64_t>(c[2]) * g.G[1] + c[1]) * g.G[0] + c[0];
+}
+
+template <int D>
+__global__ void count_kernel(const double* __restrict__ X, int64_t n, const GridParams* __restrict__ gpp,
+                             int32_t* __restrict__ counts, int32_t* __restrict__ key, int32_t* __restrict__ slot) {
+  const GridParams g = *gpp;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double x[3];
+#pragma unroll
+    for (int t = 0; t < D; ++t) x[t] = X[i * D + t];
+    int c[3];
+    int64_t kk = cell_key<D>(x, g, c);
+    key[i] = static_cast<int32_t>(kk);
+    slot[i] = atomicAdd(&counts[kk], 1);
+  }
+}
+
+// Exclusive scan of counts[0..m) into start[0..m] (start[m] = total): per-block
+// scan, then a scan of block sums, then the add-back.
+constexpr int kScanBlock = 1024;
+constexpr int kScanItems = 4;  // per thread
+
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* warp_sums, int32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int32_t w = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    warp_sums[lane] = w;
+  }
+  __syncthreads();
+  int32_t before = wid > 0 ? warp_sums[wid - 1] : 0;
+  if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
+  return before + x - v;
+}
+
+__global__ void scan_local_kernel(const int32_t* __restrict__ in, int64_t m, int32_t* __restrict__ out,
+                                  int32_t* __restrict__ block_sums) {
+  __shared__ int32_t ws[32];
+  __shared__ int32_t tot;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock * kScanItems;
+  int32_t v[kScanItems];
+  int32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    int64_t i = base + static_cast<int64_t>(threadIdx.x) * kScanItems + j;
+    v[j] = i < m ? in[i] : 0;
+    s += v[j];
+  }
+  int32_t pre = block_excl_scan(s, ws, threadIdx.x == 0 ? &tot : nullptr);
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    int64_t i = base + static_cast<int64_t>(threadIdx.x) * kScanItems + j;
+    if (i < m) out[i] = pre;
+    pre += v[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+
+__global__ void scan_sums_kernel(int32_t* __restrict__ sums, int64_t nb, int32_t* __restrict__ total_out) {
+  __shared__ int32_t ws[32];
+  __shared__ int32_t carry;
+  __shared__ int32_t tot;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < nb; b0 += blockDim.x) {
+    int64_t i = b0 + threadIdx.x;
+    int32_t v = i < nb ? sums[i] : 0;
+    int32_t pre = block_excl_scan(v, ws, threadIdx.x == 0 ? &tot : nullptr);
+    __syncthreads();
+    if (i < nb) sums[i] = carry + pre;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total_out = carry;
+}
+
+__global__ void scan_add_kernel(int32_t* __restrict__ out, int64_t m, const int32_t* __restrict__ sums) {
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock * kScanItems;
+  const int32_t add = sums[blockIdx.x];
+  for (int j = 0; j < kScanItems; ++j) {
+    int64_t i = base + static_cast<int64_t>(threadIdx.x) * kScanItems + j;
+    if (i < m) out[i] += add;
+  }
+}
+
+template <int D>
+__global__ void scatter_kernel(const double* __restrict__ X, int64_t n, const int32_t* __restrict__ key,
+                               const int32_t* __restrict__ slot, const int32_t* __restrict__ start,
+                               double* __restrict__ pts, int32_t* __restrict__ pid, int32_t* __restrict__ pos_of) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t p = static_cast<int64_t>(start[key[i]]) + slot[i];
+#pragma unroll
+    for (int t = 0; t < D; ++t) pts[p * D + t] = X[i * D + t];
+    pid[p] = static_cast<int32_t>(i);
+    if (pos_of) pos_of[i] = static_cast<int32_t>(p);
+  }
+}
+
+// ---------------------------------------------------------------- warp top-k
+
+struct Cand {
+  double d;
+  int32_t i;
+};
+
+__device__ __forceinline__ bool cless(const Cand& a, const Cand& b) { return pair_less(a.d, a.i, b.d, b.i); }
+
+__device__ __forceinline__ Cand shfl_xor_c(const Cand& c, int m) {
+  return Cand{__shfl_xor_sync(0xffffffffu, c.d, m), __shfl_xor_sync(0xffffffffu, c.i, m)};
+}
+__device__ __forceinline__ Cand shfl_c(const Cand& c, int src) {
+  return Cand{__shfl_sync(0xffffffffu, c.d, src), __shfl_sync(0xffffffffu, c.i, src)};
+}
+
+// One compare-exchange stage across lanes: lanes whose `stride` bit is clear
+// keep the min when `up`, else the max.
+__device__ __forceinline__ Cand cx_stage(Cand v, int stride, bool up, int lane) {
+  Cand o = shfl_xor_c(v, stride);
+  const bool lower = (lane & stride) == 0;
+  const bool take_min = (lower == up);
+  const bool o_less = cless(o, v);
+  return (take_min == o_less) ? o : v;
+}
+
+__device__ __forceinline__ Cand bitonic_sort32(Cand v, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) v = cx_stage(v, stride, (lane & size) == 0, lane);
+  }
+  return v;
+}
+
+// Sort a bitonic 32-sequence ascending.
+__device__ __forceinline__ Cand bitonic_clean32(Cand v, int lane) {
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) v = cx_stage(v, stride, true, lane);
+  return v;
+}
+
+// Merge two ascending 32-sequences: a <- 32 smallest (ascending), b <- 32 largest (ascending).
+__device__ __forceinline__ void merge32(Cand& a, Cand& b, int lane) {
+  Cand br = shfl_c(b, 31 - lane);
+  Cand lo = cless(br, a) ? br : a;
+  Cand hi = cless(br, a) ? a : br;
+  a = bitonic_clean32(lo, lane);
+  b = bitonic_clean32(hi, lane);
+}
+
+// Keep the KP = 32*E smallest of (L u batch); L ascending over (e, lane).
+template <int E>
+__device__ __forceinline__ void merge_batch_chain(Cand (&L)[E], Cand c, int lane) {
+  c = bitonic_sort32(c, lane);
+  Cand cr = shfl_c(c, 31 - lane);
+  Cand x = cless(cr, L[E - 1]) ? cr : L[E - 1];
+  x = bitonic_clean32(x, lane);
+  // Insert the sorted segment x into the sorted chain L[0..E-2] from the top:
+  // merge(L[E-2], x) -> (L[E-2], L[E-1]), then merge(L[E-3], L[E-2]) -> ...
+#pragma unroll
+  for (int e = E - 1; e >= 1; --e) {
+    Cand a = L[e - 1];
+    Cand b = (e == E - 1) ? x : L[e];
+    merge32(a, b, lane);
+    L[e - 1] = a;
+    L[e] = b;
+  }
+  if (E == 1) L[0] = x;
+}
+
+// ---------------------------------------------------------------- query
+
+// Squared lower bound on the distance from q to any point outside the block
+// of radius r (infinite when the block covers the grid), shrunk by a margin
+// (1e-7 h) that dominates every rounding in the cell assignment (~eps * G * h)
+// and in the key itself (~5 eps relative).
+template <int D>
+__device__ __forceinline__ double outside_lb_sq(const GridParams& g, const double* q, const int c[3], int r) {
+  double lb = INFINITY;
+#pragma unroll
+  for (int t = 0; t < D; ++t) {
+    if (c[t] - r > 0) lb = fmin(lb, q[t] - (g.lo[t] + (c[t] - r) * g.h));
+    if (c[t] + r < g.G[t] - 1) lb = fmin(lb, (g.lo[t] + (c[t] + r + 1) * g.h) - q[t]);
+  }
+  if (lb == INFINITY) return INFINITY;
+  lb -= 1e-7 * g.h;
+  if (!(lb > 0.0)) return 0.0;
+  return lb * lb * (1.0 - 1e-12);
+}
+
+constexpr int kQueryThreads = 256;
+constexpr int kSlots = 64;  // ranges per chunk: 2 per lane (one cell-row per lane)
+
+// One warp per query. Query w is: sorted position qpos[w] (self mode,
+// exclusion by original index), or sorted position w when qpos == nullptr
+// and Q == nullptr, or external coordinates Q[w] (no exclusion). Output row
+// index: original index - row_offset (self modes) or qout[w] / w.
+template <int D, int E>
+__global__ void __launch_bounds__(kQueryThreads, 2)
+grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
+                  const int32_t* __restrict__ cstart, int64_t nq, const int32_t* __restrict__ qpos,
+                  const double* __restrict__ Q, const int32_t* __restrict__ qout, const int32_t* __restrict__ excl_arr,
+                  int kk, int with_self, int64_t row_offset, int32_t* __restrict__ out, double* __restrict__ out_d) {
+  __shared__ int32_t s_beg[kQueryThreads / 32][kSlots];
+  __shared__ int32_t s_pre[kQueryThreads / 32][kSlots + 1];
+  const GridParams g = *gpp;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int32_t* rb = s_beg[wib];
+  int32_t* rp = s_pre[wib];
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w = warp0; w < nq; w += nwarps) {
+    double q[D];
+    int32_t self = -1;
+    int64_t orow;
+    if (Q == nullptr) {
+      const int64_t p = qpos != nullptr ? qpos[w] : w;
+#pragma unroll
+      for (int t = 0; t < D; ++t) q[t] = pts[p * D + t];
+      self = pid[p];
+      orow = static_cast<int64_t>(self) - row_offset;
+    } else {
+#pragma unroll
+      for (int t = 0; t < D; ++t) q[t] = Q[w * D + t];
+      orow = qout != nullptr ? qout[w] : w;
+      if (excl_arr != nullptr) self = excl_arr[orow];
+    }
+    int c[3];
+    cell_key<D>(q, g, c);
+
+    Cand L[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) L[e] = Cand{INFINITY, INT_MAX};
+    Cand thr{INFINITY, INT_MAX};
+    const int tl = (kk - 1) & 31, te = (kk - 1) >> 5;
+
+    for (int r = 1;; ++r) {
+      const bool block = (r == 1);
+      const int z0 = D >= 3 ? max(0, c[2] - r) : 0, z1 = D >= 3 ? min(g.G[2] - 1, c[2] + r) : 0;
+      const int y0 = D >= 2 ? max(0, c[1] - r) : 0, y1 = D >= 2 ? min(g.G[1] - 1, c[1] + r) : 0;
+      const int xl = c[0] - r, xr = c[0] + r;
+      const int x0 = max(0, xl), x1 = min(g.G[0] - 1, xr);
+      const int ny = y1 - y0 + 1;
+      const int nrows = (z1 - z0 + 1) * ny;
+      for (int rbase = 0; rbase < nrows; rbase += 32) {
+        // each lane turns one cell-row of the ring into <= 2 contiguous ranges
+        const int ridx = rbase + lane;
+        int32_t b0 = 0, l0 = 0, b1 = 0, l1 = 0;
+        if (ridx < nrows) {
+          const int z = z0 + ridx / ny, y = y0 + ridx % ny;
+          const bool edge = block || (D >= 3 && (z == c[2] - r || z == c[2] + r)) ||
+                            (D >= 2 && (y == c[1] - r || y == c[1] + r));
+          const int64_t rowkey = (static_cast<int64_t>(z) * g.G[1] + y) * g.G[0];
+          if (edge) {
+            b0 = cstart[rowkey + x0];
+            l0 = cstart[rowkey + x1 + 1] - b0;
+          } else {
+            if (xl >= 0) {
+              b0 = cstart[rowkey + xl];
+              l0 = cstart[rowkey + xl + 1] - b0;
+            }
+            if (xr < g.G[0]) {
+              b1 = cstart[rowkey + xr];
+              l1 = cstart[rowkey + xr + 1] - b1;
+            }
+          }
+        }
+        int32_t incl = l0 + l1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int32_t excl = incl - (l0 + l1);
+        rb[2 * lane] = b0;
+        rb[2 * lane + 1] = b1;
+        rp[2 * lane] = excl;
+        rp[2 * lane + 1] = excl + l0;
+        const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 31) rp[kSlots] = total;
+        __syncwarp();
+        for (int32_t base = 0; base < total; base += 32) {
+          const int32_t want = base + lane;
+          Cand cd{INFINITY, INT_MAX};
+          if (want < total) {
+            int j = 0;  // largest slot j with rp[j] <= want (skips empty slots)
+#pragma unroll
+            for (int step = kSlots / 2; step > 0; step >>= 1)
+              if (rp[j + step] <= want) j += step;
+            const int64_t p = static_cast<int64_t>(rb[j]) + (want - rp[j]);
+            const int32_t id = pid[p];
+            double x[D];
+#pragma unroll
+            for (int t = 0; t < D; ++t) x[t] = pts[p * D + t];
+            const double s = dist_sq_fixed<D>(q, x);
+            if (id != self) cd = Cand{s, id};
+          }
+          const bool pass = cless(cd, thr);
+          if (__ballot_sync(0xffffffffu, pass) != 0) {
+            if (!pass) cd = Cand{INFINITY, INT_MAX};
+            merge_batch_chain<E>(L, cd, lane);
+            Cand t{0, 0};
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+              if (e == te) t = L[e];
+            thr = shfl_c(t, tl);
+          }
+        }
+        __syncwarp();
+      }
+      const double lb2 = outside_lb_sq<D>(g, q, c, r);
+      if (lb2 == INFINITY) break;  // the block covers every cell
+      if (thr.d < lb2) break;      // nothing outside can enter the top-kk
+    }
+    // write the row: [self,] top kk in order
+    const int width = kk + (with_self ? 1 : 0);
+    int32_t* row = out + orow * width;
+    if (with_self && lane == 0) row[0] = self;
+    const int o = with_self ? 1 : 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int t = e * 32 + lane;
+      if (t < kk) {
+        row[o + t] = L[e].i;
+        if (out_d) out_d[orow * kk + t] = L[e].d;
+      }
+    }
+  }
+}
+
+__global__ void compact_rows_kernel(const int32_t* __restrict__ pid, int64_t n, int64_t rb, int64_t re,
+                                    int32_t* __restrict__ qpos, int32_t* __restrict__ counter) {
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t id = pid[p];
+    if (id >= rb && id < re) {
+      // warp-aggregated append keeps cell order within each warp's run
+      const int32_t s = atomicAdd(counter, 1);
+      qpos[s] = static_cast<int32_t>(p);
+    }
+  }
+}
+
+unsigned grid1d(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 64) g = 148 * 64;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+// Device scratch for one counting sort of `n` points into `ncap` cells.
+struct SortBufs {
+  int32_t *counts = nullptr, *key = nullptr, *slot = nullptr, *cstart = nullptr, *bsums = nullptr;
+  int32_t* pid = nullptr;
+  double* pts = nullptr;
+  int64_t nb = 0;
+  cudaError_t alloc(int64_t n, int64_t ncap, int D, cudaStream_t s) {
+    nb = (ncap + 1 + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems);
+    cudaError_t e = cudaMallocAsync(&counts, sizeof(int32_t) * (ncap + 1), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&cstart, sizeof(int32_t) * (ncap + 2), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&bsums, sizeof(int32_t) * (nb + 1), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&key, sizeof(int32_t) * (n > 0 ? n : 1), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&slot, sizeof(int32_t) * (n > 0 ? n : 1), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&pid, sizeof(int32_t) * (n > 0 ? n : 1), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&pts, sizeof(double) * (n > 0 ? n : 1) * D, s);
+    return e;
+  }
+  void release(cudaStream_t s) {
+    for (void* p : {static_cast<void*>(counts), static_cast<void*>(cstart), static_cast<void*>(bsums),
+                    static_cast<void*>(key), static_cast<void*>(slot), static_cast<void*>(pid),
+                    static_cast<void*>(pts)})
+      if (p) cudaFreeAsync(p, s);
+  }
+};
+
+// Counting sort of P (np x D) by the cells of `gp`: pts/pid in cell order,
+// cstart = cell offsets.
+template <int D>
+void cell_sort(const double* P, int64_t np, const GridParams* gp, int64_t ncap, SortBufs& b, cudaStream_t s) {
+  cudaMemsetAsync(b.counts, 0, sizeof(int32_t) * (ncap + 1), s);
+  count_kernel<D><<<grid1d(np), 256, 0, s>>>(P, np, gp, b.counts, b.key, b.slot);
+  const int64_t m = ncap + 1;
+  scan_local_kernel<<<static_cast<unsigned>(b.nb), kScanBlock, 0, s>>>(b.counts, m, b.cstart, b.bsums);
+  scan_sums_kernel<<<1, kScanBlock, 0, s>>>(b.bsums, b.nb, b.bsums + b.nb);
+  scan_add_kernel<<<static_cast<unsigned>(b.nb), kScanBlock, 0, s>>>(b.cstart, m, b.bsums);
+  scatter_kernel<D><<<grid1d(np), 256, 0, s>>>(P, np, b.key, b.slot, b.cstart, b.pts, b.pid, nullptr);
+  note_launches(5);
+}
+
+template <int D, int E>
+void launch_query(const GridParams* gp, const double* pts, const int32_t* pid, const int32_t* cstart, int64_t nq,
+                  const int32_t* qpos, const double* Q, const int32_t* qout, const int32_t* excl_arr, int kk,
+                  int with_self, int64_t row_offset, int32_t* out, double* out_d, int num_sms, cudaStream_t s) {
+  int64_t blocks = (nq * 32 + kQueryThreads - 1) / kQueryThreads;
+  const int64_t cap = static_cast<int64_t>(num_sms) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  grid_query_kernel<D, E><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(
+      gp, pts, pid, cstart, nq, qpos, Q, qout, excl_arr, kk, with_self, row_offset, out, out_d);
+  note_launches(1);
+}
+
+template <int D>
+void launch_query_e(int E, const GridParams* gp, const double* pts, const int32_t* pid, const int32_t* cstart,
+                    int64_t nq, const int32_t* qpos, const double* Q, const int32_t* qout, const int32_t* excl_arr,
+                    int kk, int with_self, int64_t row_offset, int32_t* out, double* out_d, int num_sms,
+                    cudaStream_t s) {
+  if (E == 1)
+    launch_query<D, 1>(gp, pts, pid, cstart, nq, qpos, Q, qout, excl_arr, kk, with_self, row_offset, out, out_d,
+                          num_sms, s);
+  else if (E == 2)
+    launch_query<D, 2>(gp, pts, pid, cstart, nq, qpos, Q, qout, excl_arr, kk, with_self, row_offset, out, out_d,
+                          num_sms, s);
+  else
+    launch_query<D, 4>(gp, pts, pid, cstart, nq, qpos, Q, qout, excl_arr, kk, with_self, row_offset, out, out_d,
+                          num_sms, s);
+}
+
+template <int D>
+cudaError_t knn_grid_d(const double* Q, int64_t nq, const double* P, int64_t np, int kk, int64_t self_offset,
+                       const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
+                       cudaStream_t s) {
+  const int E = kk <= 32 ? 1 : (kk <= 64 ? 2 : 4);
+  // Points per cell: enough that the radius-1 block usually holds the kk-th neighbour.
+  const double per_cell = (D == 1) ? fmax(4.0, 0.6 * kk) : (D == 2 ? fmax(4.0, 0.5 * kk) : fmax(3.0, 0.37 * kk));
+  const int64_t ncap = np;  // cells never exceed the point count
+  GridParams* gp = nullptr;
+  unsigned long long* mm = nullptr;
+  SortBufs pb, qb;
+  int32_t *qpos = nullptr, *cnt = nullptr;
+  cudaError_t err = cudaMallocAsync(&gp, sizeof(GridParams), s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&mm, sizeof(unsigned long long) * 6, s);
+  if (err == cudaSuccess) err = pb.alloc(np, ncap, D, s);
+  if (err != cudaSuccess) return err;
+  // bounding box -> grid parameters -> counting sort of the reference points
+  cudaMemsetAsync(mm, 0, sizeof(unsigned long long) * 6, s);
+  for (int t = 0; t < D; ++t) cudaMemsetAsync(mm + 2 * t, 0xFF, sizeof(unsigned long long), s);
+  bbox_kernel<<<grid1d(np), 256, 0, s>>>(P, np, D, mm);
+  grid_params_kernel<<<1, 1, 0, s>>>(mm, np, D, per_cell, ncap, gp);
+  note_launches(2);
+  cell_sort<D>(P, np, gp, ncap, pb, s);
+
+  const bool self_mode = excl_arr == nullptr && self_offset >= 0 && Q == P + self_offset * D;
+  if (self_mode && self_offset == 0 && nq == np) {
+    // every training row is a query: walk them in cell order
+    launch_query_e<D>(E, gp, pb.pts, pb.pid, pb.cstart, nq, nullptr, nullptr, nullptr, nullptr, kk, with_self, 0,
+                      out, out_d, num_sms, s);
+  } else if (self_mode) {
+    // a row shard: its sorted positions, mostly in cell order
+    err = cudaMallocAsync(&qpos, sizeof(int32_t) * (nq > 0 ? nq : 1), s);
+    if (err == cudaSuccess) err = cudaMallocAsync(&cnt, sizeof(int32_t), s);
+    if (err != cudaSuccess) return err;
+    cudaMemsetAsync(cnt, 0, sizeof(int32_t), s);
+    compact_rows_kernel<<<grid1d(np), 256, 0, s>>>(pb.pid, np, self_offset, self_offset + nq, qpos, cnt);
+    note_launches(1);
+    launch_query_e<D>(E, gp, pb.pts, pb.pid, pb.cstart, nq, qpos, nullptr, nullptr, nullptr, kk, with_self,
+                      self_offset, out, out_d, num_sms, s);
+  } else {
+    // external queries (predict): sort them by the same cells for locality
+    err = qb.alloc(nq, ncap, D, s);
+    if (err != cudaSuccess) return err;
+    cell_sort<D>(Q, nq, gp, ncap, qb, s);
+    launch_query_e<D>(E, gp, pb.pts, pb.pid, pb.cstart, nq, nullptr, qb.pts, qb.pid, excl_arr, kk, with_self, 0,
+                      out, out_d, num_sms, s);
+  }
+  err = cudaGetLastError();
+  cudaFreeAsync(gp, s);
+  cudaFreeAsync(mm, s);
+  pb.release(s);
+  qb.release(s);
+  if (qpos) cudaFreeAsync(qpos, s);
+  if (cnt) cudaFreeAsync(cnt, s);
+  return err;
+}
+
+}  // namespace
+
+bool knn_grid_supported(int d, int kk) { return d >= 1 && d <= 3 && kk >= 1 && kk <= 128; }
+
+cudaError_t knn_grid(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
+                     const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
+                     cudaStream_t stream) {
+  if (nq <= 0) return cudaSuccess;
+  switch (d) {
+    case 1: return knn_grid_d<1>(Q, nq, P, np, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
+    case 2: return knn_grid_d<2>(Q, nq, P, np, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
+    case 3: return knn_grid_d<3>(Q, nq, P, np, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace fmgp

@@ -51,6 +51,14 @@ __global__ void self_rows_kernel(int32_t* __restrict__ S, int64_t nrows, int64_t
     S[e] = static_cast<int32_t>(row_begin + e);
 }
 
+// distance_to (nn_index.cpp:344-349): sqrt(dist_sq(q, P[idx[e]])).
+__global__ void distances_kernel(const double* __restrict__ P, int d, const double* __restrict__ q,
+                                 const int32_t* __restrict__ idx, int64_t cnt, double* __restrict__ out) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < cnt;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[e] = sqrt(dist_sq_dyn(q, P + static_cast<int64_t>(idx[e]) * d, d));
+}
+
 unsigned grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
@@ -79,6 +87,14 @@ cudaError_t kernel_values_launch(const double* dist, int64_t n, const KParams& k
 cudaError_t sqrt_inplace_launch(double* v, int64_t n, cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
   sqrt_kernel<<<grid_for(n), 256, 0, stream>>>(v, n);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t distances_launch(const double* P, int d, const double* q, const int32_t* idx, int64_t cnt, double* out,
+                             cudaStream_t stream) {
+  if (cnt == 0) return cudaSuccess;
+  distances_kernel<<<grid_for(cnt), 256, 0, stream>>>(P, d, q, idx, cnt, out);
   note_launches(1);
   return cudaGetLastError();
 }

@@ -92,12 +92,12 @@ def test_precompute_argument_errors():
     assert rc == _native.FMGP_EINVAL and _native.LIB.fmgp_last_error() == b"NeighborIndex: non-finite coordinates"
 
 
-def test_general_nu_is_rejected_not_approximated():
+def test_general_nu_is_accepted():
+    # The Bessel branch (kernel.cpp:40-51) is implemented on the device.
     from paper_2205_10879_b200 import _native
-    kp = _kp(nu=3.7)
-    assert _native.LIB.fmgp_validate_kernel(C.byref(kp)) == _native.FMGP_EINVAL
-    kp = _kp(kind=1, nu=3.7)  # RBF ignores nu (kernel.hpp:44-46)
-    assert _native.LIB.fmgp_validate_kernel(C.byref(kp)) == _native.FMGP_OK
+    for kind in (0, 1):
+        kp = _kp(kind=kind, nu=3.7)
+        assert _native.LIB.fmgp_validate_kernel(C.byref(kp)) == _native.FMGP_OK
 
 
 def test_no_cpu_fallback_without_a_gpu():
