@@ -75,6 +75,7 @@ int make_kparams(const fmgp_kernel_params* p, fmgp::KParams* kp) {
   kp->c0 = (1.0 - p->nu) * 0.69314718055994530942 - std::lgamma(p->nu);
   kp->s2 = p->sigma * p->sigma;
   kp->rho = p->rho;
+  kp->inv_rho = 1.0 / p->rho;
   kp->diag = kp->s2 * (1.0 + p->tau * p->tau);
   static const double jit[4] = {0.0, 1e-10, 1e-8, 1e-6};
   kp->diag_jit[0] = kp->diag;

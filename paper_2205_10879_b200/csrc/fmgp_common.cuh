@@ -22,6 +22,7 @@ struct KParams {
   // log bracket = c0 + nu log x + log K_nu(x), c0 = (1 - nu) ln 2 - lgamma(nu)
   // (host-evaluated with the reference's own std:: calls).
   double nu, sqrt2nu, c0;
+  double inv_rho;  // 1 / rho, for the kernel-matrix build (kernel_eval_fast)
 };
 
 // log K_nu(x) for x > 0, nu >= 0 — the quantity the reference takes from
@@ -182,6 +183,30 @@ __device__ __forceinline__ double kernel_eval(double dist, const KParams& p) {
     br = exp(__dadd_rn(__dadd_rn(p.c0, __dmul_rn(p.nu, log(x))), ln_bessel_k(p.nu, x)));
   }
   return __dmul_rn(p.s2, br);
+}
+
+// kernel_value for the neighbourhood matrices of the fused solve: the same
+// formulas with 1/rho multiplied instead of divided and contraction allowed.
+// The matrix entries differ from kernel_eval by at most a few ulps, far inside
+// the coefficient tolerance; predictions use the exact-order kernel_eval.
+__device__ __forceinline__ double kernel_eval_fast(double dist, const KParams& p) {
+  if (dist == 0.0) return p.diag;
+  double br;
+  if (p.kind == 1) {
+    const double u = dist * p.inv_rho;
+    br = exp(-0.5 * u * u);
+  } else if (p.nu_code == 0) {
+    br = exp(-dist * p.inv_rho);
+  } else if (p.nu_code == 1) {
+    const double a = 1.7320508075688772 * dist * p.inv_rho;
+    br = (1.0 + a) * exp(-a);
+  } else if (p.nu_code == 2) {
+    const double a = 2.2360679774997898 * dist * p.inv_rho;
+    br = fma(a, a * (1.0 / 3.0), 1.0 + a) * exp(-a);
+  } else {
+    return kernel_eval(dist, p);
+  }
+  return p.s2 * br;
 }
 
 // (dist, idx) lexicographic order of std::pair<double,int> (nn_index.cpp:275-281, :363).

@@ -8,10 +8,12 @@
 //   C.row(i) = solution                proj/core/src/fast_predict.cpp:104-106
 //
 // Shared memory per warp (doubles unless noted):
-//   A   k(k+1)/2: the lower triangle, packed column-major: column p holds rows
-//       p..k-1 contiguously at offset p*k - p(p-1)/2, so a warp reading one
-//       column (lanes = rows) is conflict-free and a pivot-row element is a
-//       broadcast.
+//   A   the lower triangle, packed ROW-major with every row padded to an even
+//       length: row i holds L[i][0..i] at ro(i) = i(i+1)/2 + ceil(i/2), so
+//       rows start 16-byte aligned and two consecutive entries are one
+//       128-bit load. Left-looking Cholesky, the forward solve and the
+//       backward solve all walk rows.
+//   dinv k: 1 / L_jj.
 //   xs  k x dchunk: neighbour coordinates, dchunk dims at a time (coalesced
 //       row gathers from X).
 //   B   k x m right-hand sides -> solution;  s  k int32 neighbour indices.
@@ -19,12 +21,12 @@
 // strict lower triangle, then replaced by kernel values; the diagonal is
 // sigma^2 (1 + tau^2) plus the jitter rung. A failed factorisation rebuilds K
 // with the next rung of {0, 1e-10, 1e-8, 1e-6} (linalg.cpp:13-19), so no copy
-// of K is kept (retries are rare), which halves the footprint and doubles the
-// warps per SM.
+// of K is kept (retries are rare).
 //
-// Cholesky is left-looking by columns: lane l owns rows j + l + 32c
-// (c < R = ceil(k/32)) of the current column and accumulates
-// a_ij - sum_p L_ip L_jp in registers with two interleaved partial sums.
+// Column j of the factor: lane l owns rows i = j + l + 32c (c < R, only the
+// warp-uniformly live c are executed) and accumulates
+// a_ij - sum_p L_ip L_jp two p at a time from 128-bit loads (the pivot row
+// L_j. is a broadcast).
 #include <cfloat>
 
 #include "fmgp_common.cuh"
@@ -36,88 +38,88 @@ namespace {
 
 __constant__ double kJitters[4] = {0.0, 1e-10, 1e-8, 1e-6};
 
-__host__ __device__ __forceinline__ int coff(int p, int k) { return p * k - ((p * (p - 1)) >> 1); }
+// Start of row i in the padded row-major packed triangle.
+__host__ __device__ __forceinline__ int ro(int i) { return ((i * (i + 1)) >> 1) + ((i + 1) >> 1); }
 
-// The diagonal after jitter attempt `a`: the reference adds (jitter - previous)
-// to the same matrix on every retry (linalg.cpp:14-18).
 __device__ __forceinline__ double jittered(double v, int a) {
   for (int t = 1; t <= a; ++t) v = __dadd_rn(v, __dsub_rn(kJitters[t], kJitters[t - 1]));
   return v;
 }
 
-// In-place lower Cholesky of the packed matrix; false at the first pivot <= 0
-// (Eigen LLT semantics; NaN fails too).
+// In-place lower Cholesky; false at the first pivot <= 0 (Eigen LLT
+// semantics, NaN fails too). dinv[j] = 1 / L_jj.
 template <int R>
-__device__ bool warp_cholesky(double* A, int k, int lane) {
+__device__ bool warp_cholesky(double* A, double* dinv, int k, int lane) {
   for (int j = 0; j < k; ++j) {
-    const int oj = coff(j, k);
+    const int live = (k - j + 31) >> 5;  // warp-uniform number of live row slots
+    const double* Lj = A + ro(j);
     double acc0[R], acc1[R];
+    const double* Li[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) {
-      const int i = j + lane + 32 * c;
-      acc0[c] = i < k ? A[oj + i - j] : 0.0;
       acc1[c] = 0.0;
+      acc0[c] = 0.0;
+      Li[c] = A;
+      if (c < live) {
+        const int i = min(j + lane + 32 * c, k - 1);  // clamp: lanes past k recompute row k-1
+        Li[c] = A + ro(i);
+        acc0[c] = Li[c][j];
+      }
     }
     int p = 0;
     for (; p + 1 < j; p += 2) {
-      const int op0 = coff(p, k), op1 = op0 + (k - p);  // coff(p + 1)
-      const double l0 = A[op0 + j - p];
-      const double l1 = A[op1 + j - p - 1];
+      const double2 lj = *reinterpret_cast<const double2*>(Lj + p);
 #pragma unroll
       for (int c = 0; c < R; ++c) {
-        const int i = j + lane + 32 * c;
-        if (i < k) {
-          acc0[c] = fma(-A[op0 + i - p], l0, acc0[c]);
-          acc1[c] = fma(-A[op1 + i - p - 1], l1, acc1[c]);
+        if (c < live) {
+          const double2 li = *reinterpret_cast<const double2*>(Li[c] + p);
+          acc0[c] = fma(-li.x, lj.x, acc0[c]);
+          acc1[c] = fma(-li.y, lj.y, acc1[c]);
         }
       }
     }
     if (p < j) {
-      const int op = coff(p, k);
-      const double l0 = A[op + j - p];
+      const double ljp = Lj[p];
 #pragma unroll
-      for (int c = 0; c < R; ++c) {
-        const int i = j + lane + 32 * c;
-        if (i < k) acc0[c] = fma(-A[op + i - p], l0, acc0[c]);
-      }
+      for (int c = 0; c < R; ++c)
+        if (c < live) acc0[c] = fma(-Li[c][p], ljp, acc0[c]);
     }
-#pragma unroll
-    for (int c = 0; c < R; ++c) acc0[c] += acc1[c];
-    const double piv = __shfl_sync(0xffffffffu, acc0[0], 0);  // row j = lane 0, c = 0
+    const double piv = __shfl_sync(0xffffffffu, acc0[0] + acc1[0], 0);  // row j: lane 0, c = 0
     if (!(piv > 0.0)) return false;
     const double ljj = sqrt(piv);
+    const double inv = 1.0 / ljj;
     __syncwarp();
 #pragma unroll
     for (int c = 0; c < R; ++c) {
       const int i = j + lane + 32 * c;
-      if (i < k) A[oj + i - j] = (c == 0 && lane == 0) ? ljj : acc0[c] / ljj;
+      if (c < live && i < k) A[ro(i) + j] = (i == j) ? ljj : (acc0[c] + acc1[c]) * inv;
     }
+    if (lane == 0) dinv[j] = inv;
     __syncwarp();
   }
   return true;
 }
 
-// L y = b then L^T x = y for each of the m columns of B (k x m).
-__device__ void warp_llt_solve(const double* A, double* B, int k, int m, int lane) {
+// L y = b (row dot products), then L^T x = y (right-looking over rows), for
+// each of the m columns of B (k x m).
+__device__ void warp_llt_solve(const double* A, const double* dinv, double* B, int k, int m, int lane) {
   for (int c = 0; c < m; ++c) {
-    // forward, right-looking: y_j = b_j / L_jj; b_i -= L_ij y_j (column j contiguous)
     for (int j = 0; j < k; ++j) {
-      const int oj = coff(j, k);
-      const double yj = B[j * m + c] / A[oj];
+      const double* Lj = A + ro(j);
+      double s = 0.0;
+      for (int p = lane; p < j; p += kWarp) s = fma(Lj[p], B[p * m + c], s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      const double yj = (B[j * m + c] - s) * dinv[j];
       __syncwarp();
-      for (int i = j + 1 + lane; i < k; i += kWarp) B[i * m + c] = fma(-A[oj + i - j], yj, B[i * m + c]);
       if (lane == 0) B[j * m + c] = yj;
       __syncwarp();
     }
-    // backward: x_j = (y_j - sum_{i>j} L_ij x_i) / L_jj, a warp dot product per j
     for (int j = k - 1; j >= 0; --j) {
-      const int oj = coff(j, k);
-      double s = 0.0;
-      for (int i = j + 1 + lane; i < k; i += kWarp) s = fma(A[oj + i - j], B[i * m + c], s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      const double xj = (B[j * m + c] - s) / A[oj];
+      const double* Lj = A + ro(j);
+      const double xj = B[j * m + c] * dinv[j];
       __syncwarp();
+      for (int i = lane; i < j; i += kWarp) B[i * m + c] = fma(-Lj[i], xj, B[i * m + c]);
       if (lane == 0) B[j * m + c] = xj;
       __syncwarp();
     }
@@ -126,30 +128,42 @@ __device__ void warp_llt_solve(const double* A, double* B, int k, int m, int lan
 
 struct WarpSmem {
   double* A;
+  double* dinv;
   double* xs;
   double* B;
   int32_t* sr;
 };
 
 __host__ __device__ __forceinline__ size_t per_warp_doubles(int k, int dchunk, int m) {
-  return static_cast<size_t>(k) * (k + 1) / 2 + static_cast<size_t>(k) * dchunk + static_cast<size_t>(k) * m +
-         (k + 1) / 2 + 1;
+  const size_t n = static_cast<size_t>(ro(k)) + k + static_cast<size_t>(k) * dchunk + static_cast<size_t>(k) * m +
+                   (k + 1) / 2 + 2;
+  return (n + 1) & ~static_cast<size_t>(1);  // even: every warp's A stays 16-byte aligned
 }
 
 __device__ __forceinline__ WarpSmem carve(double* smem, int warp, int k, int dchunk, int m) {
   WarpSmem w;
-  w.A = smem + warp * per_warp_doubles(k, dchunk, m);
-  w.xs = w.A + static_cast<size_t>(k) * (k + 1) / 2;
+  w.A = smem + warp * per_warp_doubles(k, dchunk, m);  // per_warp_doubles is even -> 16B aligned
+  w.dinv = w.A + ro(k);
+  w.xs = w.dinv + k;
   w.B = w.xs + static_cast<size_t>(k) * dchunk;
   w.sr = reinterpret_cast<int32_t*>(w.B + static_cast<size_t>(k) * m);
   return w;
 }
 
-// K(S_i) (cov_matrix_self, kernel.cpp:106-119) into the packed triangle with
-// the diagonal at jitter rung `attempt`. Coordinates are gathered from X in
-// dchunk-wide slices (the whole point when d <= dchunk).
+// (i, p) of strict-lower pair number e in row-major order (p < i).
+__device__ __forceinline__ void pair_of(int e, int& i, int& p) {
+  i = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(e))) * 0.5f);
+  while ((i * (i - 1)) / 2 > e) --i;
+  while ((i * (i + 1)) / 2 <= e) ++i;
+  p = e - (i * (i - 1)) / 2;
+}
+
+// K(S_i) (cov_matrix_self, kernel.cpp:106-119) with the diagonal at jitter
+// rung `attempt`. Coordinates are gathered from X in dchunk-wide slices (the
+// whole point when d <= dchunk); the k(k-1)/2 pairs are spread over all lanes.
 __device__ void build_kernel_matrix(const double* __restrict__ X, int d, const int32_t* sr, int k, int dchunk,
                                     const KParams& kp, int attempt, double* A, double* xs, int lane) {
+  const int npairs = (k * (k - 1)) / 2;
   for (int c0 = 0; c0 < d; c0 += dchunk) {
     const int dc = min(dchunk, d - c0);
     for (int e = lane; e < k * dc; e += kWarp) {
@@ -157,26 +171,28 @@ __device__ void build_kernel_matrix(const double* __restrict__ X, int d, const i
       xs[t * dc + c] = X[static_cast<int64_t>(sr[t]) * d + c0 + c];
     }
     __syncwarp();
-    for (int p = 0; p < k - 1; ++p) {
-      const int op = coff(p, k);
+    const bool last = c0 + dc >= d;
+    int i, p;
+    pair_of(lane, i, p);
+    for (int e = lane; e < npairs; e += kWarp) {
+      const double* xa = xs + i * dc;
       const double* xb = xs + p * dc;
-      for (int i = p + 1 + lane; i < k; i += kWarp) {
-        double acc = c0 == 0 ? 0.0 : A[op + i - p];
-        const double* xa = xs + i * dc;
-        for (int c = 0; c < dc; ++c) {
-          const double diff = __dsub_rn(xa[c], xb[c]);
-          acc = __dadd_rn(acc, __dmul_rn(diff, diff));
-        }
-        A[op + i - p] = acc;
+      double acc = c0 == 0 ? 0.0 : A[ro(i) + p];
+      for (int c = 0; c < dc; ++c) {
+        const double diff = __dsub_rn(xa[c], xb[c]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+      }
+      A[ro(i) + p] = last ? kernel_eval_fast(sqrt(acc), kp) : acc;
+      p += kWarp;  // advance to pair e + 32
+      while (p >= i) {
+        p -= i;
+        ++i;
       }
     }
     __syncwarp();
   }
   const double dg = jittered(kp.diag, attempt);
-  for (int p = 0; p < k; ++p) {
-    const int op = coff(p, k);
-    for (int i = p + lane; i < k; i += kWarp) A[op + i - p] = i == p ? dg : kernel_eval(sqrt(A[op + i - p]), kp);
-  }
+  for (int i = lane; i < k; i += kWarp) A[ro(i) + i] = dg;
   __syncwarp();
 }
 
@@ -198,7 +214,7 @@ solve_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, 
     int used = -1;
     for (int attempt = 0; attempt < 4; ++attempt) {
       build_kernel_matrix(X, d, w.sr, k, dchunk, kp, attempt, w.A, w.xs, lane);
-      if (warp_cholesky<R>(w.A, k, lane)) {
+      if (warp_cholesky<R>(w.A, w.dinv, k, lane)) {
         used = attempt;
         break;
       }
@@ -217,7 +233,7 @@ solve_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, 
       w.B[e] = Y[static_cast<int64_t>(w.sr[t]) * m + c];
     }
     __syncwarp();
-    warp_llt_solve(w.A, w.B, k, m, lane);
+    warp_llt_solve(w.A, w.dinv, w.B, k, m, lane);
     for (int e = lane; e < k * m; e += kWarp) C[r * k * m + e] = w.B[e];
     __syncwarp();
   }
@@ -239,14 +255,12 @@ spd_kernel(const double* __restrict__ K, const double* __restrict__ Bin, int64_t
     const double* Kr = K + r * k * k;
     int used = -1;
     for (int attempt = 0; attempt < 4; ++attempt) {
-      for (int p = 0; p < k; ++p) {
-        const int op = coff(p, k);
-        for (int i = p + lane; i < k; i += kWarp)
-          w.A[op + i - p] = i == p ? jittered(Kr[static_cast<int64_t>(p) * k + p], attempt)
-                                   : Kr[static_cast<int64_t>(i) * k + p];
-      }
+      for (int i = 0; i < k; ++i)
+        for (int p = lane; p <= i; p += kWarp)
+          w.A[ro(i) + p] = i == p ? jittered(Kr[static_cast<int64_t>(i) * k + i], attempt)
+                                  : Kr[static_cast<int64_t>(i) * k + p];
       __syncwarp();
-      if (warp_cholesky<R>(w.A, k, lane)) {
+      if (warp_cholesky<R>(w.A, w.dinv, k, lane)) {
         used = attempt;
         break;
       }
@@ -259,7 +273,7 @@ spd_kernel(const double* __restrict__ K, const double* __restrict__ Bin, int64_t
     if (jit_out && lane == 0) jit_out[r] = kJitters[used];
     for (int e = lane; e < k * m; e += kWarp) w.B[e] = Bin[r * k * m + e];
     __syncwarp();
-    warp_llt_solve(w.A, w.B, k, m, lane);
+    warp_llt_solve(w.A, w.dinv, w.B, k, m, lane);
     for (int e = lane; e < k * m; e += kWarp) Xout[r * k * m + e] = w.B[e];
     __syncwarp();
   }
