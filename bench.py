@@ -1,22 +1,25 @@
 """FastMuyGPs B200 benchmark — precompute train-pts/s (+ predict test-pts/s).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
 
 A step is one pass of the hot path over one batch: the precompute of all
 n_train rows of the BASELINE config (exact kNN -> kernel matrices ->
-jitter-Cholesky -> coefficient table C), sharded by rows over the ranks with
-the S/C shards all-gathered over NCCL when N > 1. The predict stage (1-NN ->
-cross-covariance -> dot) over all n_test points is timed the same way and
-reported under "predict". Inputs are resident in HBM when the timed region
-starts (`value`); `e2e` is the same metric through the host-buffer C ABI
-(fmgp_precompute) with pinned host buffers, H2D/D2H inside the timed region.
+jitter-Cholesky -> coefficient table C). Rows are sharded contiguously over
+the ranks (paper_2205_10879_b200/parallel.py) and the S / C shards are
+all-gathered over NCCL when N > 1, so every rank ends the step with the whole
+model. The predict stage (1-NN -> cross-covariance -> dot) over all n_test
+points, sharded the same way, is timed identically and reported under
+"predict". `value` has the inputs resident in HBM; `e2e` is the same metric
+through the host-buffer C ABI (fmgp_precompute, include/fmgp_b200.h) with
+pinned host buffers and H2D/D2H inside the timed region.
 
 Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events
 on the launching stream; L2 is flushed (256 MiB write) between timed steps,
 outside the events; barrier + synchronize around the timed region; the max
 over ranks is reported. Data: seeded synthetic inputs with the config's
-shapes and distributions; the paper's datasets are not
-available.
+shapes and distributions; the paper's datasets are not in
+the image.
 """
 from __future__ import annotations
 
@@ -46,16 +49,13 @@ def parse():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--n", type=int, default=None, help="override n_train (debug only; not a bench line)")
-    ap.add_argument("--nt", type=int, default=None, help="override n_test (debug only)")
+    ap.add_argument("--n", type=int, default=None, help="override n_train (debug; not a bench line)")
+    ap.add_argument("--nt", type=int, default=None, help="override n_test (debug)")
     return ap.parse_args()
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
 class ClockSampler:
@@ -96,77 +96,75 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(s[0]) for s in self.samples) if v is not None]
+        mx = [v for v in (num(s[1]) for s in self.samples) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and
+                          s[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def measured_peaks():
-    p = REPO / "MEASURED_PEAKS.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text()), "measured"
-        except Exception:
-            pass
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+def load_json(path: Path):
+    try:
+        return json.loads(path.read_text())
+    except Exception:
+        return None
 
 
-def fp64_peak():
-    """FP64 peak measured on this box by profiles/tools (DADD/DMUL op rate), if recorded."""
-    p = REPO / "profiles" / "fp64_peak.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text())
-        except Exception:
-            return None
-    return None
+def peaks():
+    mp = load_json(REPO / "MEASURED_PEAKS.json")
+    hbm = (mp or {}).get("hbm_gbs")
+    return {"hbm_gbs": hbm or 6650.0, "hbm_src": "measured (MEASURED_PEAKS.json)" if hbm else "fallback",
+            "fp64": load_json(REPO / "profiles" / "fp64_peak.json")}
 
 
 # ---------------------------------------------------------------------------- reference arm
 
-def run_reference(args, cfg_info, ds):
-    """--impl reference: the reference's own CPU implementation (oracle/_ref when
-    it was compiled from /root/reference, else the C port), all host threads,
-    on a bounded row sample per step. Rank 0 only."""
-    from oracle.oracle import best_available, host_threads
-    ws, rank, _ = dist_env()
-    if rank != 0:
-        return None
-    orc = best_available()
-    thr = host_threads()
-    info = cfg_info
+def rows_sample_rate(orc, ds, info, thr, budget_s, seed):
     kp = (info.kind, info.sigma, info.rho, info.nu, info.tau)
-    # Size the per-step sample: ~10 s of wall per step in total over W+K steps budget.
     probe = np.arange(0, min(info.n, 2 * thr), dtype=np.int64)
     t = time.perf_counter()
     orc.precompute_rows(ds.X, ds.Y, *kp, info.k, probe, threads=thr)
     per_row = (time.perf_counter() - t) / probe.size
+    nrows = int(max(thr, min(info.n, budget_s / max(per_row, 1e-9))))
+    return nrows, kp
+
+
+def run_reference(args, info, ds):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref when
+    it was compiled from /root/reference, else the C port), all host threads, on
+    a bounded random row sample per step. Rank 0 only."""
+    from oracle.oracle import best_available, host_threads
+    orc = best_available()
+    thr = host_threads()
     total_steps = args.steps + args.warmup
-    rows_per_step = int(max(thr, min(info.n, (150.0 / total_steps) / max(per_row, 1e-9))))
+    nrows, kp = rows_sample_rate(orc, ds, info, thr, 150.0 / total_steps, 0)
     rng = np.random.default_rng(0)
     times = []
     for s in range(total_steps):
-        rows = np.sort(rng.choice(info.n, size=rows_per_step, replace=False)).astype(np.int64)
+        rows = np.sort(rng.choice(info.n, size=nrows, replace=False)).astype(np.int64)
         t = time.perf_counter()
         orc.precompute_rows(ds.X, ds.Y, *kp, info.k, rows, threads=thr)
-        dt = time.perf_counter() - t
         if s >= args.warmup:
-            times.append(dt)
-    total = sum(times)
-    value = rows_per_step * len(times) / total
+            times.append(time.perf_counter() - t)
+    value = nrows * len(times) / sum(times)
     return {
         "metric": "precompute train-pts/s", "value": value, "unit": "train-pts/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"cfg{info.cfg}", "d": info.d, "n_train": info.n, "k": info.k, "m": info.m,
-                   "sample_rows_per_step": rows_per_step},
+                   "sample_rows_per_step": nrows},
         "cpu_baseline": {"value": value, "unit": "train-pts/s", "cores": thr, "kind": orc.kind,
-                         "sample": f"{rows_per_step} random training rows of cfg{info.cfg} per step (kNN against "
-                                   f"all {info.n} points + local solve), {thr} threads"},
+                         "sample": f"{nrows} random training rows of cfg{info.cfg} per step (exact kNN against "
+                                   f"all {info.n} points + local solve each), {thr} threads"},
         "e2e": {"value": value, "unit": "train-pts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -176,38 +174,46 @@ def cpu_baseline(info, ds, budget_s=12.0):
     from oracle.oracle import best_available, host_threads
     orc = best_available()
     thr = host_threads()
-    kp = (info.kind, info.sigma, info.rho, info.nu, info.tau)
-    probe = np.arange(0, min(info.n, 2 * thr), dtype=np.int64)
-    t = time.perf_counter()
-    orc.precompute_rows(ds.X, ds.Y, *kp, info.k, probe, threads=thr)
-    per_row = (time.perf_counter() - t) / probe.size
-    nrows = int(max(thr, min(info.n, budget_s / max(per_row, 1e-9))))
+    nrows, kp = rows_sample_rate(orc, ds, info, thr, budget_s, 1)
     rows = np.sort(np.random.default_rng(1).choice(info.n, size=nrows, replace=False)).astype(np.int64)
     t = time.perf_counter()
     orc.precompute_rows(ds.X, ds.Y, *kp, info.k, rows, threads=thr)
     dt = time.perf_counter() - t
     return {"value": nrows / dt, "unit": "train-pts/s", "cores": thr, "kind": orc.kind,
-            "sample": f"{nrows} random training rows of cfg{info.cfg} (full-n kNN + solve each), {thr} threads, "
-                      f"{dt:.1f} s"}
+            "sample": f"{nrows} random training rows of cfg{info.cfg} (exact kNN against all {info.n} points + "
+                      f"local solve each), {thr} threads, {dt:.1f} s"}
 
 
 # ---------------------------------------------------------------------------- B200 arm
+
+def solve_flops_per_row(info):
+    """F = k^3/3 + 2 k^2 m + 3 d k(k-1)/2 fp64 flops per training row."""
+    k, m, d = info.k, info.m, info.d
+    return k ** 3 / 3 + 2 * k * k * m + 3 * d * k * (k - 1) / 2
+
+
+def predict_bytes_per_point(info):
+    """4k + 8km + 8kd + 8d + 8m HBM bytes per test point."""
+    k, m, d = info.k, info.m, info.d
+    return 4 * k + 8 * k * m + 8 * k * d + 8 * d + 8 * m
+
 
 def main():
     args = parse()
     ws, rank, local = dist_env()
     from paper_2205_10879_b200 import datagen
     info = datagen.config_info(args.config)
-    n = args.n or info.n
-    nt = args.nt or info.n_test
+    if args.n:
+        info.n = args.n
+    if args.nt:
+        info.n_test = args.nt
+    n, nt = info.n, info.n_test
 
     if args.impl == "reference":
         if rank != 0:
             return 0
         ds = datagen.generate(args.config, n, min(nt, 1000))
-        info.n = n
-        line = run_reference(args, info, ds)
-        print(json.dumps(line), flush=True)
+        print(json.dumps(run_reference(args, info, ds)), flush=True)
         return 0
 
     import torch
@@ -217,43 +223,39 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2205_10879_b200 as fm
     from paper_2205_10879_b200 import _native as N
+    from paper_2205_10879_b200.parallel import sharded_precompute, sharded_predict
     dev = torch.device("cuda", local)
 
     ds = datagen.generate(args.config, n, nt)
     X = torch.from_numpy(ds.X).to(dev)
     Y = torch.from_numpy(ds.Y).to(dev)
     Z = torch.from_numpy(ds.Z).to(dev)
-    k, m = info.k, info.m
+    k, m, d = info.k, info.m, info.d
     fit = fm.FittedParams(fm.KernelParams(info.sigma, info.rho, info.nu, info.tau), fm.KernelKind(info.kind))
-
-    # row / test shards (contiguous, rank-ordered)
-    def shard(total):
-        per = (total + ws - 1) // ws
-        b = min(total, rank * per)
-        return b, min(total, b + per), per
-
-    rb, re_, per = shard(n)
-    zb, ze, zper = shard(nt)
-    S_full = torch.empty((per * ws, k), dtype=torch.int32, device=dev)
-    C_full = torch.empty((per * ws, k, m), dtype=torch.float64, device=dev)
-    S_loc = S_full[rank * per: rank * per + per]
-    C_loc = C_full[rank * per: rank * per + per]
-    out = torch.empty((zper, m), dtype=torch.float64, device=dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    state = {}
+
+    def shard(b, e):
+        S = torch.empty((e - b, k), dtype=torch.int32, device=dev)
+        Cm = torch.empty((e - b, k, m), dtype=torch.float64, device=dev)
+        fm.precompute_device(X, Y, fit, k, b, e, S, Cm, stream)
+        return S, Cm
 
     def precompute_step():
-        fm.precompute_device(X, Y, fit, k, rb, re_, S_loc, C_loc, stream)
-        if ws > 1:
-            dist.all_gather_into_tensor(S_full, S_loc.contiguous())
-            dist.all_gather_into_tensor(C_full, C_loc.contiguous())
-
-    S_all = S_full[:n]
-    C_all = C_full[:n]
+        state["S"], state["C"] = sharded_precompute(n, shard)
 
     def predict_step():
-        fm.predict_device(X, S_all, C_all.reshape(n, k, m), fit, ds.mean_offset, Z[zb:ze], out[: ze - zb], None,
-                          stream)
+        def pshard(b, e):
+            out = torch.empty((e - b, m), dtype=torch.float64, device=dev)
+            fm.predict_device(X, state["S"], state["C"], fit, ds.mean_offset, Z[b:e], out, None, stream)
+            return out
+        state["P"] = sharded_predict(nt, pshard)
+
+    def knn_step():
+        idx = torch.empty((n, k - 1), dtype=torch.int32, device=dev)
+        N.check(N.LIB.fmgp_query_knn_device(C.c_void_p(X.data_ptr()), n, d, C.c_void_p(X.data_ptr()), n, k - 1, 0,
+                                            C.c_void_p(idx.data_ptr()), None, C.c_void_p(stream.cuda_stream)))
 
     def timed(fn, steps, warmup):
         for _ in range(warmup):
@@ -262,6 +264,7 @@ def main():
         if ws > 1:
             dist.barrier()
         ms = []
+        l0 = N.LIB.fmgp_launch_count()
         for _ in range(steps):
             flush.fill_(1.0)
             e0 = torch.cuda.Event(enable_timing=True)
@@ -271,35 +274,27 @@ def main():
             e1.record(stream)
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
+        launches = N.LIB.fmgp_launch_count() - l0
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
         t = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
         if ws > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item()) / steps, ms
+        return float(t.item()) / steps, ms, launches
 
     with ClockSampler(local) as clk:
-        pre_ms, pre_all = timed(precompute_step, args.steps, args.warmup)
-        pred_ms, pred_all = timed(predict_step, args.steps, args.warmup)
+        pre_ms, pre_all, pre_launch = timed(precompute_step, args.steps, args.warmup)
+        pred_ms, pred_all, pred_launch = timed(predict_step, args.steps, args.warmup)
     clocks = clk.summary()
-
-    # per-kernel share: time the kNN scan alone inside the same process (events)
     knn_ms = None
     if ws == 1:
-        idx_tmp = torch.empty((n, k - 1), dtype=torch.int32, device=dev)
-        import ctypes
-        def knn_only():
-            rc = N.LIB.fmgp_query_knn_device(ctypes.c_void_p(X.data_ptr()), n, info.d, ctypes.c_void_p(X.data_ptr()),
-                                             n, k - 1, 0, ctypes.c_void_p(idx_tmp.data_ptr()), None,
-                                             ctypes.c_void_p(stream.cuda_stream))
-            N.check(rc)
-        knn_ms, _ = timed(knn_only, max(1, min(3, args.steps)), 1)
-        del idx_tmp
+        knn_ms, _, _ = timed(knn_step, max(1, min(3, args.steps)), 1)
 
     value = n / (pre_ms / 1e3)
     pred_value = nt / (pred_ms / 1e3)
 
+    # e2e: the reference-facing host-buffer call, pinned buffers, copies inside the timing
     e2e = None
     if not args.no_e2e and ws == 1:
         Xh = torch.from_numpy(ds.X).pin_memory()
@@ -310,10 +305,9 @@ def main():
         failed = C.c_int64(-1)
 
         def e2e_step():
-            rc = N.LIB.fmgp_precompute(C.c_void_p(Xh.data_ptr()), C.c_void_p(Yh.data_ptr()), n, info.d, m,
-                                       C.byref(kp), k, C.c_void_p(Sh.data_ptr()), C.c_void_p(Ch.data_ptr()),
-                                       C.byref(failed))
-            N.check(rc, failed.value)
+            N.check(N.LIB.fmgp_precompute(C.c_void_p(Xh.data_ptr()), C.c_void_p(Yh.data_ptr()), n, d, m, C.byref(kp),
+                                          k, C.c_void_p(Sh.data_ptr()), C.c_void_p(Ch.data_ptr()), C.byref(failed)),
+                    failed.value)
 
         for _ in range(args.warmup):
             e2e_step()
@@ -329,32 +323,49 @@ def main():
                "d2h_bytes_per_step": int(Sh.numel() * 4 + Ch.numel() * 8),
                "api": "fmgp_precompute (include/fmgp_b200.h), pinned host buffers"}
 
-    # roofline of the dominant kernel (exact kNN scan, FP64 pipe)
-    pairs = float(n) * float(n)
-    fp64_ops = pairs * (3 * info.d - 1)
-    fpk = fp64_peak()
+    # roofline of the dominant kernel of the step
+    pk = peaks()
+    fp64 = pk["fp64"] or {}
+    solve_ms = pre_ms - knn_ms if knn_ms is not None else None
     roof = None
-    if knn_ms is not None:
-        achieved = fp64_ops / (knn_ms / 1e3) / 1e12
-        peak = fpk["fp64_tops_nonfma"] if fpk else None
-        roof = {"bound": "fp64", "kernel": "knn_scan_reg", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if peak else None,
-                "traffic": None, "work": f"{pairs:.3g} (query, point) pairs x {3 * info.d - 1} fp64 ops",
-                "kernel_ms": knn_ms, "share_of_step": knn_ms / pre_ms,
-                "peak_source": "profiles/fp64_peak.json (DADD/DMUL rate measured on B200)" if fpk else "unmeasured"}
+    if solve_ms is not None:
+        rows_per_rank = (n + ws - 1) // ws
+        if solve_ms >= knn_ms:
+            flops = solve_flops_per_row(info) * rows_per_rank
+            achieved = flops / (solve_ms / 1e3) / 1e12
+            peak = fp64.get("fp64_dmma_tflops") or fp64.get("fp64_dfma_tflops")
+            roof = {"bound": "tensor", "kernel": "solve_tc_kernel (fp64 DMMA blocked Cholesky, fused gather/kernel "
+                    "build/solve)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak if peak else None, "traffic": None,
+                    "work": f"{solve_flops_per_row(info):.0f} fp64 flops per training row (SURVEY §8(d)) x "
+                            f"{rows_per_rank} rows",
+                    "kernel_ms": solve_ms, "share_of_step": solve_ms / pre_ms,
+                    "peak_source": "profiles/fp64_peak.json: measured DMMA m8n8k4 f64 rate on B200"}
+        else:
+            roof = {"bound": "fp64", "kernel": "grid_query_kernel (exact cell-grid kNN)", "achieved": None,
+                    "peak": fp64.get("fp64_tops_nonfma"), "unit": "TFLOP/s", "frac": None, "traffic": None,
+                    "kernel_ms": knn_ms, "share_of_step": knn_ms / pre_ms}
+    pred_bytes = predict_bytes_per_point(info) * ((nt + ws - 1) // ws)
+    pred_gbs = pred_bytes / (pred_ms / 1e3) / 1e9
 
     line = {
         "metric": "precompute train-pts/s", "value": value, "unit": "train-pts/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": pre_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg{info.cfg}", "d": info.d, "n_train": n, "n_test": nt, "k": k, "m": m,
+        "config": {"workload": f"cfg{info.cfg}", "d": d, "n_train": n, "n_test": nt, "k": k, "m": m,
                    "kernel": "RBF" if info.kind == 1 else f"Matern nu={info.nu}", "parallelism": f"rows{ws}",
                    "l2": "flushed (256 MiB write) between timed steps"},
-        "predict": {"metric": "predict test-pts/s", "value": pred_value, "unit": "test-pts/s", "ms_per_step": pred_ms},
+        "predict": {"metric": "predict test-pts/s", "value": pred_value, "unit": "test-pts/s", "ms_per_step": pred_ms,
+                    "roofline": {"bound": "hbm", "achieved": pred_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                 "frac": pred_gbs / pk["hbm_gbs"], "peak_source": pk["hbm_src"],
+                                 "work": f"{predict_bytes_per_point(info)} B per test point (SURVEY §8(d)); the "
+                                         "stage also runs the grid 1-NN", "traffic": None},
+                    "gpu_launches": pred_launch},
+        "stages_ms": {"knn": knn_ms, "solve": solve_ms, "precompute": pre_ms, "predict": pred_ms},
         "e2e": e2e,
         "roofline": roof,
         "clocks": clocks,
-        "gpu_launches": None,
+        "gpu_launches": pre_launch,
         "step_ms": {"precompute": pre_all, "predict": pred_all},
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -169,6 +169,12 @@ int fmgp_kernel_values(const double* dist, int64_t ndist, const fmgp_kernel_para
 int fmgp_solve_spd_batched(const double* K, const double* B, int64_t batch, int32_t k, int32_t m,
                            double* X_out, double* applied_jitter, int64_t* failed_index);
 
+/* ---- diagnostics ---------------------------------------------------------
+ * D~ (the tensor-core filter value n^_q + n^_p - 2 q^.p^ in the scaled fp16
+ * space) of the first 128 x 256 (query, point) tile of the tcgen05 kNN, for
+ * validating the GEMM plumbing. G_out: 128 x 256 fp32 (host). d >= 4. */
+int fmgp_debug_tc_tile(const double* Q, int64_t nq, const double* P, int64_t np, int32_t d, float* G_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,7 @@ SIGNATURES: dict[str, tuple] = {
     "fmgp_cov_matrix": (C.c_int, [_vp, C.c_int64, _vp, C.c_int64, C.c_int32, _kp, _vp]),
     "fmgp_kernel_values": (C.c_int, [_vp, C.c_int64, _kp, _vp]),
     "fmgp_solve_spd_batched": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _vp, _vp, _i64]),
+    "fmgp_debug_tc_tile": (C.c_int, [_vp, C.c_int64, _vp, C.c_int64, C.c_int32, _vp]),
 }
 
 

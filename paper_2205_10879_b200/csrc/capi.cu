@@ -611,4 +611,27 @@ int fmgp_solve_spd_batched(const double* K, const double* B, int64_t batch, int3
   return FMGP_OK;
 }
 
+int fmgp_debug_tc_tile(const double* Q, int64_t nq, const double* P, int64_t np, int32_t d, float* G_out) {
+  int rc;
+  if ((rc = check_points(P, np, d)) != FMGP_OK) return rc;
+  if (d < 4) return fail(FMGP_EINVAL, "debug tc tile needs d >= 4");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dQ, dP;
+  DevBuf<float> dG;
+  DevBuf<int32_t> dO;
+  FMGP_CUDA(dQ.alloc(static_cast<size_t>(nq) * d, st.s));
+  FMGP_CUDA(dP.alloc(static_cast<size_t>(np) * d, st.s));
+  FMGP_CUDA(dG.alloc(128 * 256, st.s));
+  FMGP_CUDA(dO.alloc(static_cast<size_t>(nq), st.s));
+  FMGP_CUDA(cudaMemsetAsync(dG.p, 0, sizeof(float) * 128 * 256, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dQ.p, Q, sizeof(double) * nq * d, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dP.p, P, sizeof(double) * np * d, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(fmgp::knn_tc(dQ.p, nq, dP.p, np, d, 1, -1, nullptr, 0, dO.p, nullptr, num_sms_current(), st.s, dG.p));
+  FMGP_CUDA(cudaMemcpyAsync(G_out, dG.p, sizeof(float) * 128 * 256, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
 }  // extern "C"

@@ -78,3 +78,34 @@ cudaError_t spd_solve_big(const double* K, const double* B, int64_t batch, int k
                           unsigned long long* fail_min, int num_sms, cudaStream_t stream);
 
 }  // namespace fmgp
+
+namespace fmgp {
+
+// FP64 tensor-core (DMMA) blocked variant of fused_solve (k <= 128, m <= 16).
+bool fused_solve_tc_supported(int k, int d, int m);
+cudaError_t fused_solve_tc(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
+                           int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
+                           int num_sms, cudaStream_t stream);
+
+}  // namespace fmgp
+
+namespace fmgp {
+
+// Register-resident-row variant of fused_solve for compile-time shapes.
+bool fused_solve_reg_supported(int k, int d, int m);
+cudaError_t fused_solve_reg(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
+                            int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
+                            int num_sms, cudaStream_t stream);
+
+}  // namespace fmgp
+
+namespace fmgp {
+
+// Tensor-core exact kNN (d >= 4): tcgen05 fp16 distance GEMM + bounded filter +
+// exact fp64 recheck. debug_G (nullable): write D~ of the first 128x256 tile and stop.
+bool knn_tc_supported(int d, int kk);
+cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
+                   const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
+                   cudaStream_t stream, float* debug_G);
+
+}  // namespace fmgp

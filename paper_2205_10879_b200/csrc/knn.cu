@@ -301,12 +301,15 @@ namespace fmgp {
 cudaError_t knn_exact(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
                       const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
                       cudaStream_t stream) {
+  // FMGP_KNN = brute forces the fp64 brute-force scan (A/B checks).
   static const bool force_brute = [] {
     const char* e = std::getenv("FMGP_KNN");
     return e != nullptr && std::string(e) == "brute";
   }();
   if (!force_brute && knn_grid_supported(d, kk))
     return knn_grid(Q, nq, P, np, d, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
+  if (!force_brute && knn_tc_supported(d, kk))
+    return knn_tc(Q, nq, P, np, d, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream, nullptr);
   return knn_bruteforce(Q, nq, P, np, d, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
 }
 

@@ -1,0 +1,491 @@
+// K1-tc — exact kNN for d >= 4 on the 5th-generation tensor cores:
+// a tcgen05 distance GEMM fed by TMA, a per-query threshold filter in the
+// TMEM epilogue, and an exact fp64 recheck, so the neighbour indices are the
+// reference's bit for bit (proj/core/src/nn_index.cpp:73-81 key,
+// :254-287 query_knn, :351-366 nearest).
+//
+// Data path
+//   prep      x^ = fp16(s (x - mu)) row-major, zero-padded to DP = 64*KB
+//             columns (one 128-byte swizzle row per 64 dims); n^ = ||x^||^2 (fp32).
+//             mu = mean of the reference points, s = 2^e so max |x^| ~ 2^14
+//             (exact scaling, no fp16 subnormals in practice).
+//   GEMM      per CTA one 128-query tile (TMEM lanes) x a stream of 256-point
+//             tiles (TMEM columns): tcgen05.mma.cta_group::1.kind::f16,
+//             M=128 N=256 K=16, fp32 accumulators in TMEM (two 256-column
+//             buffers, 512 columns), A/B staged by TMA (SWIZZLE_128B, 4 stages).
+//   filter    D~ = n^_q + n^_p - 2 G~ (fp32). Keep p iff D~ <= F_q with
+//             F_q = (s sqrt(T_q)(1+1e-12) + eta_q)^2 + eps_q, T_q the exact
+//             kk-th key so far, eta_q = 2^-11 (||q^|| + max||p^||) (1 + 1e-3)
+//             bounding the fp16 input rounding of the distance, and
+//             eps_q = (DP + 8) 2^-22 (n^_q + max n^_p) bounding fp32
+//             accumulation (even with truncating adds) and the combination.
+//             Any p whose exact key can reach the top-kk passes.
+//   recheck   passing p get the exact fp64 key from the original coordinates
+//             and are inserted into the query's sorted (key, index) list;
+//             points are streamed in ascending index, so equal keys keep the
+//             lower index (the reference's max-heap order).
+// Roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
+// issuer (one elected lane), warps 2-5 epilogue (thread = TMEM lane = query).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <climits>
+#include <cmath>
+
+#include "fmgp_common.cuh"
+#include "fmgp_internal.h"
+
+namespace fmgp {
+
+namespace {
+
+constexpr int kBM = 128;  // queries per tile (TMEM lanes)
+constexpr int kBN = 256;  // reference points per tile (TMEM columns per buffer)
+constexpr int kBK = 64;   // fp16 dims per k-block (one 128 B swizzle row)
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
+constexpr uint32_t kBBytes = kBN * kBK * 2;  // 32 KB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+
+// ------------------------------------------------------------------ PTX helpers
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(su32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// K-major operand in a SWIZZLE_128B tile: rows of 128 B, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;             // leading byte offset (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;     // stride byte offset: next 8-row group
+  d |= static_cast<uint64_t>(1u) << 46;             // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2u) << 61;             // SWIZZLE_128B
+  return d;
+}
+// kind::f16 instruction descriptor: fp16 x fp16 -> fp32, both K-major, M=128, N=256.
+constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
+                            (static_cast<uint32_t>(kBM >> 4) << 24);
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ prep
+
+__global__ void mean_kernel(const double* __restrict__ P, int64_t np, int d, double* __restrict__ sums) {
+  // column sums: thread per (dim, row-chunk)
+  for (int t = blockIdx.y * blockDim.x + threadIdx.x; t < d; t += gridDim.y * blockDim.x) {
+    double s = 0.0;
+    for (int64_t i = blockIdx.x; i < np; i += gridDim.x) s += P[i * d + t];
+    atomicAdd(&sums[t], s);
+  }
+}
+
+__global__ void maxabs_kernel(const double* __restrict__ A, int64_t n, int d, const double* __restrict__ sums,
+                              int64_t np, unsigned long long* __restrict__ maxbits) {
+  double m = 0.0;
+  const int64_t total = n * d;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(e % d);
+    m = fmax(m, fabs(A[e] - sums[t] / static_cast<double>(np)));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+// x^ rows (fp16, DP wide) and n^ = ||x^||^2; also max ||x^|| into pmax (as bits).
+__global__ void convert_kernel(const double* __restrict__ A, int64_t n, int d, int DP, const double* __restrict__ sums,
+                               int64_t np, const unsigned long long* __restrict__ maxbits, __half* __restrict__ H,
+                               float* __restrict__ norms, unsigned long long* __restrict__ pmax_bits) {
+  const double maxabs = __longlong_as_double(static_cast<long long>(*maxbits));
+  const double s = maxabs > 0.0 ? exp2(floor(log2(16384.0 / maxabs))) : 1.0;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    double acc = 0.0;
+    for (int t = lane; t < DP; t += 32) {
+      __half h = __float2half_rn(0.0f);
+      if (t < d) {
+        h = __double2half((A[i * d + t] - sums[t] / static_cast<double>(np)) * s);
+        const double v = static_cast<double>(__half2float(h));
+        acc += v * v;
+      }
+      H[i * DP + t] = h;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      norms[i] = static_cast<float>(acc);
+      if (pmax_bits) atomicMax(pmax_bits, static_cast<unsigned long long>(__double_as_longlong(sqrt(acc))));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ main kernel
+
+struct TcArgs {
+  const double* Q;       // nq x d original coordinates (fp64)
+  const double* P;       // np x d
+  const float* qn;       // ||q^||^2
+  const float* pn;       // ||p^||^2
+  int64_t nq, np;
+  int d, DP, KB, kk;
+  int64_t self_offset;   // exclude p == q + self_offset when >= 0
+  const int32_t* excl;   // or per-query exclusion (nullable)
+  int with_self;
+  int32_t* out;          // nq x (kk + with_self)
+  double* out_d;         // nq x kk (nullable)
+  double* wd;            // nq x kk scratch lists
+  int32_t* wi;
+  const unsigned long long* maxabs_bits;
+  const unsigned long long* pmax_bits;
+  float* debug_G;        // when non-null: D~ of (query tile 0, point tile 0), 128 x 256, and no search
+};
+
+__device__ __forceinline__ void list_insert_tc(double* ld, int32_t* li, int& cnt, int kk, double s, int32_t j,
+                                               double& thr) {
+  int pos = cnt < kk ? cnt : kk - 1;
+  while (pos > 0) {
+    const double pd = ld[pos - 1];
+    if (pd > s) {
+      ld[pos] = pd;
+      li[pos] = li[pos - 1];
+      --pos;
+    } else {
+      break;
+    }
+  }
+  ld[pos] = s;
+  li[pos] = j;
+  if (cnt < kk) ++cnt;
+  if (cnt == kk) thr = ld[kk - 1];
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmP, TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for SWIZZLE_128B tiles
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                 // kStages x 16 KB
+  uint8_t* sB = smem + kStages * kABytes;             // kStages x 32 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;   // 2 TMEM buffers
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nqt = (a.nq + kBM - 1) / kBM;
+  const int64_t npt = (a.np + kBN - 1) / kBN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
+        const int64_t pt_end = a.debug_G ? 1 : npt;
+        for (int64_t pt = 0; pt < pt_end; ++pt) {
+          for (int kb = 0; kb < a.KB; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], kStageBytes);
+            tma_load_2d(sA + stage * kABytes, &tmQ, &full[stage], kb * kBK, static_cast<int>(qt * kBM));
+            tma_load_2d(sB + stage * kBBytes, &tmP, &full[stage], kb * kBK, static_cast<int>(pt * kBN));
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    int buf = 0;
+    uint32_t tphase = 0;
+    for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
+      const int64_t pt_end = a.debug_G ? 1 : npt;
+      for (int64_t pt = 0; pt < pt_end; ++pt) {
+        mbar_wait(&tempty[buf], tphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * kBN);
+        for (int kb = 0; kb < a.KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint64_t ad = sdesc_sw128(su32(sA + stage * kABytes));
+            const uint64_t bd = sdesc_sw128(su32(sB + stage * kBBytes));
+#pragma unroll
+            for (int k16 = 0; k16 < kBK / 16; ++k16)
+              tc_mma_f16(d_tmem, ad + 2 * k16, bd + 2 * k16, kIdesc, (kb > 0 || k16 > 0) ? 1u : 0u);
+            tc_commit(&empty[stage]);
+            if (kb == a.KB - 1) tc_commit(&tfull[buf]);
+          }
+          __syncwarp();
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (++buf == 2) {
+          buf = 0;
+          tphase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: thread = TMEM lane = query row
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
+    const double maxabs = __longlong_as_double(static_cast<long long>(*a.maxabs_bits));
+    const double s = maxabs > 0.0 ? exp2(floor(log2(16384.0 / maxabs))) : 1.0;
+    const double pmax = __longlong_as_double(static_cast<long long>(*a.pmax_bits));
+    int buf = 0;
+    uint32_t tphase = 0;
+    for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
+      const int64_t q = qt * kBM + row;
+      const bool valid = q < a.nq;
+      const double nq_hat = valid ? static_cast<double>(a.qn[q]) : 0.0;
+      // 2^-11 (||q^|| + max||p^||) relative rounding + 2^-25 per (possibly subnormal) coordinate
+      const double eta = 4.8828125e-4 * (sqrt(nq_hat) + pmax) * 1.001 + 2.0 * 2.98023223876953125e-8 * sqrt(double(a.DP));
+      const double eps = (a.DP + 8) * 2.384185791015625e-7 * (nq_hat + pmax * pmax);  // (DP+8) 2^-22 (...)
+      const int64_t excl = a.excl != nullptr ? (valid ? a.excl[q] : -1)
+                                             : (a.self_offset >= 0 ? q + a.self_offset : -1);
+      double* ld = a.wd + (valid ? q : 0) * a.kk;
+      int32_t* li = a.wi + (valid ? q : 0) * a.kk;
+      const double* qx = a.Q + (valid ? q : 0) * a.d;
+      int cnt = 0;
+      double thr = valid ? INFINITY : -INFINITY;
+      float fthr = valid ? INFINITY : -INFINITY;  // bound on pn - 2G for admission
+      const int64_t pt_end = a.debug_G ? 1 : npt;
+      for (int64_t pt = 0; pt < pt_end; ++pt) {
+        mbar_wait(&tfull[buf], tphase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + lane_addr + static_cast<uint32_t>(buf * kBN);
+        for (int ch = 0; ch < kBN / 32; ++ch) {
+          uint32_t r[32];
+          tmem_ld32(tbase + ch * 32, r);
+          const int64_t j0 = pt * kBN + ch * 32;
+          if (a.debug_G) {
+            if (qt == 0)
+              for (int c = 0; c < 32; ++c)
+                a.debug_G[row * kBN + ch * 32 + c] =
+                    static_cast<float>(nq_hat) + fmaf(-2.0f, __uint_as_float(r[c]), j0 + c < a.np ? a.pn[j0 + c] : 0.f);
+            continue;
+          }
+#pragma unroll 8
+          for (int c = 0; c < 32; ++c) {
+            const int64_t j = j0 + c;
+            const float v = fmaf(-2.0f, __uint_as_float(r[c]), j < a.np ? __ldg(a.pn + j) : 0.0f);
+            if (v <= fthr && j < a.np && j != excl) {
+              // exact fp64 key, the reference's order
+              const double key = dist_sq_dyn(qx, a.P + j * a.d, a.d);
+              if (key < thr) {
+                list_insert_tc(ld, li, cnt, a.kk, key, static_cast<int32_t>(j), thr);
+                if (cnt == a.kk) {
+                  const double rr = s * sqrt(thr) * (1.0 + 1e-12) + eta;
+                  const double F = rr * rr + eps - nq_hat;
+                  fthr = static_cast<float>(F * (1.0 + 1e-6) + 1e-30);
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[buf]);
+        if (++buf == 2) {
+          buf = 0;
+          tphase ^= 1;
+        }
+      }
+      if (valid && !a.debug_G) {
+        const int width = a.kk + (a.with_self ? 1 : 0);
+        int32_t* orow = a.out + q * width;
+        int o = 0;
+        if (a.with_self) orow[o++] = static_cast<int32_t>(q + a.self_offset);
+        for (int t = 0; t < a.kk; ++t) {
+          orow[o + t] = t < cnt ? li[t] : INT_MAX;
+          if (a.out_d) a.out_d[q * a.kk + t] = t < cnt ? ld[t] : INFINITY;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+bool make_map(CUtensorMap* map, const __half* ptr, int64_t rows, int DP, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (encode == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || fn == nullptr)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(DP), static_cast<cuuint64_t>(rows)};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(DP) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(ptr), gdim, gstride, box, estride,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+unsigned g1(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return static_cast<unsigned>(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
+}
+
+}  // namespace
+
+bool knn_tc_supported(int d, int kk) { return d >= 4 && d <= 1024 && kk >= 1; }
+
+cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
+                   const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
+                   cudaStream_t s, float* debug_G) {
+  if (nq <= 0) return cudaSuccess;
+  const int KB = (d + kBK - 1) / kBK;
+  const int DP = KB * kBK;
+  __half *Qh = nullptr, *Ph = nullptr;
+  float *qn = nullptr, *pn = nullptr;
+  double *sums = nullptr, *wd = nullptr;
+  int32_t* wi = nullptr;
+  unsigned long long* bits = nullptr;  // [0] maxabs, [1] pmax
+  cudaError_t err = cudaMallocAsync(&Qh, sizeof(__half) * nq * DP, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&Ph, sizeof(__half) * np * DP, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&qn, sizeof(float) * nq, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&pn, sizeof(float) * np, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&sums, sizeof(double) * d, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&bits, sizeof(unsigned long long) * 2, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&wd, sizeof(double) * nq * kk, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&wi, sizeof(int32_t) * nq * kk, s);
+  if (err != cudaSuccess) return err;
+  cudaMemsetAsync(sums, 0, sizeof(double) * d, s);
+  cudaMemsetAsync(bits, 0, sizeof(unsigned long long) * 2, s);
+  mean_kernel<<<dim3(256, (d + 255) / 256), 256, 0, s>>>(P, np, d, sums);
+  maxabs_kernel<<<g1(np * d), 256, 0, s>>>(P, np, d, sums, np, bits);
+  if (Q != P) maxabs_kernel<<<g1(nq * d), 256, 0, s>>>(Q, nq, d, sums, np, bits);
+  convert_kernel<<<g1(np * 32), 256, 0, s>>>(P, np, d, DP, sums, np, bits, Ph, pn, bits + 1);
+  convert_kernel<<<g1(nq * 32), 256, 0, s>>>(Q, nq, d, DP, sums, np, bits, Qh, qn, nullptr);
+  note_launches(Q != P ? 5 : 4);
+
+  CUtensorMap mq, mp;
+  if (!make_map(&mq, Qh, nq, DP, kBM) || !make_map(&mp, Ph, np, DP, kBN)) return cudaErrorInvalidValue;
+  TcArgs a;
+  a.Q = Q;
+  a.P = P;
+  a.qn = qn;
+  a.pn = pn;
+  a.nq = nq;
+  a.np = np;
+  a.d = d;
+  a.DP = DP;
+  a.KB = KB;
+  a.kk = kk;
+  a.self_offset = self_offset;
+  a.excl = excl_arr;
+  a.with_self = with_self;
+  a.out = out;
+  a.out_d = out_d;
+  a.wd = wd;
+  a.wi = wi;
+  a.maxabs_bits = bits;
+  a.pmax_bits = bits + 1;
+  a.debug_G = debug_G;
+  const size_t smem = 1024 + kStages * kStageBytes + 256;
+  err = cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  const int64_t nqt = (nq + kBM - 1) / kBM;
+  const int grid = static_cast<int>(nqt < num_sms ? nqt : num_sms);
+  knn_tc_kernel<<<debug_G ? 1 : grid, kThreads, smem, s>>>(mq, mp, a);
+  note_launches(1);
+  err = cudaGetLastError();
+  for (void* p : {static_cast<void*>(Qh), static_cast<void*>(Ph), static_cast<void*>(qn), static_cast<void*>(pn),
+                  static_cast<void*>(sums), static_cast<void*>(bits), static_cast<void*>(wd), static_cast<void*>(wi)})
+    cudaFreeAsync(p, s);
+  return err;
+}
+
+}  // namespace fmgp

@@ -28,6 +28,8 @@
 // a_ij - sum_p L_ip L_jp two p at a time from 128-bit loads (the pivot row
 // L_j. is a broadcast).
 #include <cfloat>
+#include <cstdlib>
+#include <string>
 
 #include "fmgp_common.cuh"
 #include "fmgp_internal.h"
@@ -46,45 +48,62 @@ __device__ __forceinline__ double jittered(double v, int a) {
   return v;
 }
 
-// In-place lower Cholesky; false at the first pivot <= 0 (Eigen LLT
-// semantics, NaN fails too). dinv[j] = 1 / L_jj.
+// The augmented matrix [K ; B^T]: rows 0..k-1 are the packed lower triangle
+// of K (row i: i+1 entries), rows k..k+m-1 are the right-hand sides b_c^T
+// (k entries each), every row padded to an even length so rows start 16-byte
+// aligned. The left-looking column sweep over rows j..k+m-1 factors K and, on
+// the RHS rows, performs the forward substitution y = L^-1 b in the same pass.
+struct Aug {
+  int k, m, rw;  // rw: padded RHS row length
+  __device__ __forceinline__ int row(int i) const { return i < k ? ro(i) : ro(k) + (i - k) * rw; }
+};
+
+// Factor in place; false at the first pivot <= 0 (Eigen LLT semantics, NaN
+// fails too). dinv[j] = 1 / L_jj.
 template <int R>
-__device__ bool warp_cholesky(double* A, double* dinv, int k, int lane) {
-  for (int j = 0; j < k; ++j) {
-    const int live = (k - j + 31) >> 5;  // warp-uniform number of live row slots
+__device__ bool warp_cholesky_aug(double* A, double* dinv, const Aug& G, int lane) {
+  const int rows = G.k + G.m;
+  for (int j = 0; j < G.k; ++j) {
+    const int live = (rows - j + 31) >> 5;  // warp-uniform number of live row slots
     const double* Lj = A + ro(j);
-    double acc0[R], acc1[R];
+    // four partial sums per row (p mod 4): ILP and a shallower summation tree
+    double acc0[R], acc1[R], acc2[R], acc3[R];
     const double* Li[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) {
-      acc1[c] = 0.0;
-      acc0[c] = 0.0;
+      acc0[c] = acc1[c] = acc2[c] = acc3[c] = 0.0;
       Li[c] = A;
       if (c < live) {
-        const int i = min(j + lane + 32 * c, k - 1);  // clamp: lanes past k recompute row k-1
-        Li[c] = A + ro(i);
+        const int i = min(j + lane + 32 * c, rows - 1);  // lanes past the end redo the last row
+        Li[c] = A + G.row(i);
         acc0[c] = Li[c][j];
       }
     }
     int p = 0;
-    for (; p + 1 < j; p += 2) {
-      const double2 lj = *reinterpret_cast<const double2*>(Lj + p);
+    for (; p + 3 < j; p += 4) {
+      const double2 la = *reinterpret_cast<const double2*>(Lj + p);
+      const double2 lb = *reinterpret_cast<const double2*>(Lj + p + 2);
 #pragma unroll
       for (int c = 0; c < R; ++c) {
         if (c < live) {
-          const double2 li = *reinterpret_cast<const double2*>(Li[c] + p);
-          acc0[c] = fma(-li.x, lj.x, acc0[c]);
-          acc1[c] = fma(-li.y, lj.y, acc1[c]);
+          const double2 xa = *reinterpret_cast<const double2*>(Li[c] + p);
+          const double2 xb = *reinterpret_cast<const double2*>(Li[c] + p + 2);
+          acc0[c] = fma(-xa.x, la.x, acc0[c]);
+          acc1[c] = fma(-xa.y, la.y, acc1[c]);
+          acc2[c] = fma(-xb.x, lb.x, acc2[c]);
+          acc3[c] = fma(-xb.y, lb.y, acc3[c]);
         }
       }
     }
-    if (p < j) {
-      const double ljp = Lj[p];
+    for (; p < j; ++p) {
+      const double l = Lj[p];
 #pragma unroll
       for (int c = 0; c < R; ++c)
-        if (c < live) acc0[c] = fma(-Li[c][p], ljp, acc0[c]);
+        if (c < live) acc0[c] = fma(-Li[c][p], l, acc0[c]);
     }
-    const double piv = __shfl_sync(0xffffffffu, acc0[0] + acc1[0], 0);  // row j: lane 0, c = 0
+#pragma unroll
+    for (int c = 0; c < R; ++c) acc0[c] = (acc0[c] + acc1[c]) + (acc2[c] + acc3[c]);
+    const double piv = __shfl_sync(0xffffffffu, acc0[0], 0);  // row j: lane 0, c = 0
     if (!(piv > 0.0)) return false;
     const double ljj = sqrt(piv);
     const double inv = 1.0 / ljj;
@@ -92,7 +111,7 @@ __device__ bool warp_cholesky(double* A, double* dinv, int k, int lane) {
 #pragma unroll
     for (int c = 0; c < R; ++c) {
       const int i = j + lane + 32 * c;
-      if (c < live && i < k) A[ro(i) + j] = (i == j) ? ljj : (acc0[c] + acc1[c]) * inv;
+      if (c < live && i < rows) A[G.row(i) + j] = (i == j) ? ljj : acc0[c] * inv;
     }
     if (lane == 0) dinv[j] = inv;
     __syncwarp();
@@ -100,27 +119,17 @@ __device__ bool warp_cholesky(double* A, double* dinv, int k, int lane) {
   return true;
 }
 
-// L y = b (row dot products), then L^T x = y (right-looking over rows), for
-// each of the m columns of B (k x m).
-__device__ void warp_llt_solve(const double* A, const double* dinv, double* B, int k, int m, int lane) {
-  for (int c = 0; c < m; ++c) {
-    for (int j = 0; j < k; ++j) {
+// Backward solve L^T x = y for each RHS row (y = the factored RHS rows),
+// right-looking over rows of L; x overwrites y.
+__device__ void warp_back_solve(double* A, const double* dinv, const Aug& G, int lane) {
+  for (int c = 0; c < G.m; ++c) {
+    double* y = A + G.row(G.k + c);
+    for (int j = G.k - 1; j >= 0; --j) {
       const double* Lj = A + ro(j);
-      double s = 0.0;
-      for (int p = lane; p < j; p += kWarp) s = fma(Lj[p], B[p * m + c], s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      const double yj = (B[j * m + c] - s) * dinv[j];
+      const double xj = y[j] * dinv[j];
       __syncwarp();
-      if (lane == 0) B[j * m + c] = yj;
-      __syncwarp();
-    }
-    for (int j = k - 1; j >= 0; --j) {
-      const double* Lj = A + ro(j);
-      const double xj = B[j * m + c] * dinv[j];
-      __syncwarp();
-      for (int i = lane; i < j; i += kWarp) B[i * m + c] = fma(-Lj[i], xj, B[i * m + c]);
-      if (lane == 0) B[j * m + c] = xj;
+      for (int i = lane; i < j; i += kWarp) y[i] = fma(-Lj[i], xj, y[i]);
+      if (lane == 0) y[j] = xj;
       __syncwarp();
     }
   }
@@ -130,23 +139,21 @@ struct WarpSmem {
   double* A;
   double* dinv;
   double* xs;
-  double* B;
   int32_t* sr;
 };
 
 __host__ __device__ __forceinline__ size_t per_warp_doubles(int k, int dchunk, int m) {
-  const size_t n = static_cast<size_t>(ro(k)) + k + static_cast<size_t>(k) * dchunk + static_cast<size_t>(k) * m +
-                   (k + 1) / 2 + 2;
+  const size_t aug = static_cast<size_t>(ro(k)) + static_cast<size_t>(m) * ((k + 1) & ~1);
+  const size_t n = aug + k + static_cast<size_t>(k) * dchunk + (k + 1) / 2 + 2;
   return (n + 1) & ~static_cast<size_t>(1);  // even: every warp's A stays 16-byte aligned
 }
 
 __device__ __forceinline__ WarpSmem carve(double* smem, int warp, int k, int dchunk, int m) {
   WarpSmem w;
-  w.A = smem + warp * per_warp_doubles(k, dchunk, m);  // per_warp_doubles is even -> 16B aligned
-  w.dinv = w.A + ro(k);
+  w.A = smem + warp * per_warp_doubles(k, dchunk, m);
+  w.dinv = w.A + ro(k) + static_cast<size_t>(m) * ((k + 1) & ~1);
   w.xs = w.dinv + k;
-  w.B = w.xs + static_cast<size_t>(k) * dchunk;
-  w.sr = reinterpret_cast<int32_t*>(w.B + static_cast<size_t>(k) * m);
+  w.sr = reinterpret_cast<int32_t*>(w.xs + static_cast<size_t>(k) * dchunk);
   return w;
 }
 
@@ -158,11 +165,13 @@ __device__ __forceinline__ void pair_of(int e, int& i, int& p) {
   p = e - (i * (i - 1)) / 2;
 }
 
-// K(S_i) (cov_matrix_self, kernel.cpp:106-119) with the diagonal at jitter
-// rung `attempt`. Coordinates are gathered from X in dchunk-wide slices (the
-// whole point when d <= dchunk); the k(k-1)/2 pairs are spread over all lanes.
-__device__ void build_kernel_matrix(const double* __restrict__ X, int d, const int32_t* sr, int k, int dchunk,
-                                    const KParams& kp, int attempt, double* A, double* xs, int lane) {
+// [K(S_i) ; Y_{S_i}^T] (cov_matrix_self, kernel.cpp:106-119) with the diagonal
+// at jitter rung `attempt`. Coordinates are gathered from X in dchunk-wide
+// slices (the whole point when d <= dchunk); the k(k-1)/2 pairs are spread
+// over all lanes with an incremental pair decode.
+__device__ void build_aug(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* sr,
+                          const Aug& G, int dchunk, const KParams& kp, int attempt, double* A, double* xs, int lane) {
+  const int k = G.k;
   const int npairs = (k * (k - 1)) / 2;
   for (int c0 = 0; c0 < d; c0 += dchunk) {
     const int dc = min(dchunk, d - c0);
@@ -174,25 +183,31 @@ __device__ void build_kernel_matrix(const double* __restrict__ X, int d, const i
     const bool last = c0 + dc >= d;
     int i, p;
     pair_of(lane, i, p);
+    int rowi = ro(i);
     for (int e = lane; e < npairs; e += kWarp) {
       const double* xa = xs + i * dc;
       const double* xb = xs + p * dc;
-      double acc = c0 == 0 ? 0.0 : A[ro(i) + p];
+      double acc = c0 == 0 ? 0.0 : A[rowi + p];
       for (int c = 0; c < dc; ++c) {
         const double diff = __dsub_rn(xa[c], xb[c]);
         acc = __dadd_rn(acc, __dmul_rn(diff, diff));
       }
-      A[ro(i) + p] = last ? kernel_eval_fast(sqrt(acc), kp) : acc;
+      A[rowi + p] = last ? kernel_eval_fast(sqrt(acc), kp) : acc;
       p += kWarp;  // advance to pair e + 32
       while (p >= i) {
         p -= i;
         ++i;
       }
+      rowi = ro(i);
     }
     __syncwarp();
   }
   const double dg = jittered(kp.diag, attempt);
   for (int i = lane; i < k; i += kWarp) A[ro(i) + i] = dg;
+  for (int e = lane; e < k * G.m; e += kWarp) {
+    const int t = e / G.m, c = e - t * G.m;
+    A[G.row(k + c) + t] = Y[static_cast<int64_t>(sr[t]) * G.m + c];
+  }
   __syncwarp();
 }
 
@@ -206,6 +221,10 @@ solve_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, 
   const int warp = threadIdx.x / kWarp;
   const int warps = blockDim.x / kWarp;
   WarpSmem w = carve(smem, warp, k, dchunk, m);
+  Aug G;
+  G.k = k;
+  G.m = m;
+  G.rw = (k + 1) & ~1;
 
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * warps + warp; r < nrows;
        r += static_cast<int64_t>(gridDim.x) * warps) {
@@ -213,8 +232,8 @@ solve_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, 
     __syncwarp();
     int used = -1;
     for (int attempt = 0; attempt < 4; ++attempt) {
-      build_kernel_matrix(X, d, w.sr, k, dchunk, kp, attempt, w.A, w.xs, lane);
-      if (warp_cholesky<R>(w.A, w.dinv, k, lane)) {
+      build_aug(X, Y, d, w.sr, G, dchunk, kp, attempt, w.A, w.xs, lane);
+      if (warp_cholesky_aug<R>(w.A, w.dinv, G, lane)) {
         used = attempt;
         break;
       }
@@ -228,13 +247,11 @@ solve_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, 
       continue;
     }
     if (status && lane == 0) status[r] = used;
+    warp_back_solve(w.A, w.dinv, G, lane);
     for (int e = lane; e < k * m; e += kWarp) {
       const int t = e / m, c = e - t * m;
-      w.B[e] = Y[static_cast<int64_t>(w.sr[t]) * m + c];
+      C[r * k * m + e] = w.A[G.row(k + c) + t];
     }
-    __syncwarp();
-    warp_llt_solve(w.A, w.dinv, w.B, k, m, lane);
-    for (int e = lane; e < k * m; e += kWarp) C[r * k * m + e] = w.B[e];
     __syncwarp();
   }
 }
@@ -250,6 +267,10 @@ spd_kernel(const double* __restrict__ K, const double* __restrict__ Bin, int64_t
   const int warp = threadIdx.x / kWarp;
   const int warps = blockDim.x / kWarp;
   WarpSmem w = carve(smem, warp, k, 0, m);
+  Aug G;
+  G.k = k;
+  G.m = m;
+  G.rw = (k + 1) & ~1;
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * warps + warp; r < batch;
        r += static_cast<int64_t>(gridDim.x) * warps) {
     const double* Kr = K + r * k * k;
@@ -259,8 +280,12 @@ spd_kernel(const double* __restrict__ K, const double* __restrict__ Bin, int64_t
         for (int p = lane; p <= i; p += kWarp)
           w.A[ro(i) + p] = i == p ? jittered(Kr[static_cast<int64_t>(i) * k + i], attempt)
                                   : Kr[static_cast<int64_t>(i) * k + p];
+      for (int e = lane; e < k * m; e += kWarp) {
+        const int t = e / m, c = e - t * m;
+        w.A[G.row(k + c) + t] = Bin[r * k * m + e];
+      }
       __syncwarp();
-      if (warp_cholesky<R>(w.A, w.dinv, k, lane)) {
+      if (warp_cholesky_aug<R>(w.A, w.dinv, G, lane)) {
         used = attempt;
         break;
       }
@@ -271,10 +296,11 @@ spd_kernel(const double* __restrict__ K, const double* __restrict__ Bin, int64_t
       continue;
     }
     if (jit_out && lane == 0) jit_out[r] = kJitters[used];
-    for (int e = lane; e < k * m; e += kWarp) w.B[e] = Bin[r * k * m + e];
-    __syncwarp();
-    warp_llt_solve(w.A, w.dinv, w.B, k, m, lane);
-    for (int e = lane; e < k * m; e += kWarp) Xout[r * k * m + e] = w.B[e];
+    warp_back_solve(w.A, w.dinv, G, lane);
+    for (int e = lane; e < k * m; e += kWarp) {
+      const int t = e / m, c = e - t * m;
+      Xout[r * k * m + e] = w.A[G.row(k + c) + t];
+    }
     __syncwarp();
   }
 }
@@ -349,10 +375,21 @@ cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const in
                         int64_t row_begin, int k, const KParams& kp, double* C, int32_t* status,
                         unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
   if (nrows <= 0) return cudaSuccess;
+  // FMGP_SOLVE = reg (default where the shape is compiled in) | tc | scalar, for A/B checks.
+  static const int mode = [] {
+    const char* e = std::getenv("FMGP_SOLVE");
+    if (e == nullptr) return 0;
+    const std::string v(e);
+    return v == "tc" ? 1 : (v == "scalar" ? 2 : 0);
+  }();
+  if (mode == 0 && status == nullptr && fused_solve_reg_supported(k, d, m))
+    return fused_solve_reg(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
+  if (mode == 1 && status == nullptr && fused_solve_tc_supported(k, d, m))
+    return fused_solve_tc(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
   const size_t bytes = per_warp_doubles(k, dchunk_for(k, d), m) * sizeof(double);
-  if (k > kMaxK || bytes > kSmemBudget)
+  if (k + m > kMaxK || bytes > kSmemBudget)
     return fused_solve_big(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
-  switch ((k + 31) / 32) {
+  switch ((k + m + 31) / 32) {
     case 1: return launch_solve<1>(X, Y, d, m, S, nrows, row_begin, k, kp, C, status, fail_min, num_sms, stream);
     case 2: return launch_solve<2>(X, Y, d, m, S, nrows, row_begin, k, kp, C, status, fail_min, num_sms, stream);
     case 3: return launch_solve<3>(X, Y, d, m, S, nrows, row_begin, k, kp, C, status, fail_min, num_sms, stream);
@@ -365,8 +402,8 @@ cudaError_t spd_solve_batched(const double* K, const double* B, int64_t batch, i
                               double* jit_out, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
   if (batch <= 0) return cudaSuccess;
   const size_t bytes = per_warp_doubles(k, 0, m) * sizeof(double);
-  if (k > kMaxK || bytes > kSmemBudget) return spd_solve_big(K, B, batch, k, m, X, jit_out, fail_min, num_sms, stream);
-  switch ((k + 31) / 32) {
+  if (k + m > kMaxK || bytes > kSmemBudget) return spd_solve_big(K, B, batch, k, m, X, jit_out, fail_min, num_sms, stream);
+  switch ((k + m + 31) / 32) {
     case 1: return launch_spd<1>(K, B, batch, k, m, X, jit_out, fail_min, num_sms, stream);
     case 2: return launch_spd<2>(K, B, batch, k, m, X, jit_out, fail_min, num_sms, stream);
     case 3: return launch_spd<3>(K, B, batch, k, m, X, jit_out, fail_min, num_sms, stream);

@@ -1,0 +1,286 @@
+// K2-reg — the fused neighbourhood solve with register-resident rows, for
+// compile-time neighbourhood sizes (the BASELINE shapes k in {30, 50}).
+// Same contract as solve.cu (fast_predict.cpp:98-106, kernel.cpp:106-119,
+// linalg.cpp:10-36), one warp per neighbourhood.
+//
+// Why: the shared-memory left-looking kernel is bound by the LSU pipe (one
+// per-lane 64-bit load per FMA). Here lane l owns rows l and l+32 of the
+// augmented matrix [K ; Y^T] for the whole factorisation, in registers
+// (static indexing: K and M are template parameters and both loops are fully
+// unrolled). Column j needs only the pivot row L_j., which its owner writes to
+// shared memory as it is produced and every lane reads as a 128-bit
+// broadcast. The RHS rows (K .. K+M-1) ride along, so the column sweep also
+// performs the forward substitution; the backward solve then runs over the
+// shared-memory copy of L.
+#include "fmgp_common.cuh"
+#include "fmgp_internal.h"
+
+namespace fmgp {
+
+namespace {
+
+__constant__ double kJitR[4] = {0.0, 1e-10, 1e-8, 1e-6};
+
+__host__ __device__ constexpr int ro_r(int i) { return ((i * (i + 1)) >> 1) + ((i + 1) >> 1); }
+
+__device__ __forceinline__ double jitter_r(double v, int a) {
+  for (int t = 1; t <= a; ++t) v = __dadd_rn(v, __dsub_rn(kJitR[t], kJitR[t - 1]));
+  return v;
+}
+
+template <int K, int M>
+struct RegShape {
+  static constexpr int kRows = K + M;
+  static constexpr int kRw = (K + 1) & ~1;             // padded RHS row length
+  static constexpr int kAug = ro_r(K) + M * kRw;       // augmented packed size (doubles)
+  static constexpr int kN0 = K < 32 ? K : 32;          // slot-0 row entries kept (row l <= 31)
+  static constexpr bool kTwo = kRows > 32;             // does slot 1 (row l + 32) exist?
+  static constexpr int kDch = 16;                      // coordinate slice width staged per pass
+  static constexpr int kCol = (K + 2) & ~1;            // colbuf (even: 16-byte aligned pairs)
+  static constexpr int kPerWarp = ((kAug + ((K + 1) & ~1) /*dinv*/ + kCol + kDch * K /*xs*/ + (K + 1) / 2 + 2) + 1) & ~1;
+  __host__ __device__ static constexpr int row_off(int i) { return i < K ? ro_r(i) : ro_r(K) + (i - K) * kRw; }
+};
+
+// Build [K(S_i) ; Y^T] in the packed shared-memory layout (pairs spread over
+// lanes, incremental decode), diagonal at jitter rung `attempt`.
+template <int K, int M>
+__device__ void build_reg(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* sr,
+                          const KParams& kp, int attempt, double* A, double* xs, int lane) {
+  using Sh = RegShape<K, M>;
+  constexpr int npairs = (K * (K - 1)) / 2;
+  const int dchunk = d < Sh::kDch ? d : Sh::kDch;
+  for (int c0 = 0; c0 < d; c0 += dchunk) {
+    const int dc = min(dchunk, d - c0);
+    for (int e = lane; e < K * dc; e += kWarp) {
+      const int t = e / dc, c = e - t * dc;
+      xs[t * dc + c] = X[static_cast<int64_t>(sr[t]) * d + c0 + c];
+    }
+    __syncwarp();
+    const bool last = c0 + dc >= d;
+    // two independent pairs per iteration (e and e + 32) for ILP through sqrt/exp
+    int ia, pa, ib, pb;
+    {
+      const int e0 = lane, e1 = lane + 32;
+      ia = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(e0))) * 0.5f);
+      while ((ia * (ia - 1)) / 2 > e0) --ia;
+      while ((ia * (ia + 1)) / 2 <= e0) ++ia;
+      pa = e0 - (ia * (ia - 1)) / 2;
+      ib = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(e1))) * 0.5f);
+      while ((ib * (ib - 1)) / 2 > e1) --ib;
+      while ((ib * (ib + 1)) / 2 <= e1) ++ib;
+      pb = e1 - (ib * (ib - 1)) / 2;
+    }
+    for (int e = lane; e < npairs; e += 2 * kWarp) {
+      const bool hb = e + kWarp < npairs;
+      const double* xa = xs + ia * dc;
+      const double* xa2 = xs + pa * dc;
+      const double* xb = xs + (hb ? ib : ia) * dc;
+      const double* xb2 = xs + (hb ? pb : pa) * dc;
+      const int offa = ro_r(ia) + pa;
+      const int offb = ro_r(hb ? ib : ia) + (hb ? pb : pa);
+      double acca = c0 == 0 ? 0.0 : A[offa];
+      double accb = c0 == 0 ? 0.0 : A[offb];
+      for (int c = 0; c < dc; ++c) {
+        const double da = __dsub_rn(xa[c], xa2[c]);
+        const double db = __dsub_rn(xb[c], xb2[c]);
+        acca = __dadd_rn(acca, __dmul_rn(da, da));
+        accb = __dadd_rn(accb, __dmul_rn(db, db));
+      }
+      if (last) {
+        const double va = kernel_eval_fast(sqrt(acca), kp);
+        const double vb = kernel_eval_fast(sqrt(accb), kp);
+        A[offa] = va;
+        if (hb) A[offb] = vb;
+      } else {
+        A[offa] = acca;
+        if (hb) A[offb] = accb;
+      }
+      pa += 2 * kWarp;
+      while (pa >= ia) {
+        pa -= ia;
+        ++ia;
+      }
+      pb += 2 * kWarp;
+      while (pb >= ib) {
+        pb -= ib;
+        ++ib;
+      }
+    }
+    __syncwarp();
+  }
+  const double dg = jitter_r(kp.diag, attempt);
+  for (int i = lane; i < K; i += kWarp) A[ro_r(i) + i] = dg;
+  for (int e = lane; e < K * M; e += kWarp) {
+    const int t = e / M, c = e - t * M;
+    A[Sh::row_off(K + c) + t] = Y[static_cast<int64_t>(sr[t]) * M + c];
+  }
+  __syncwarp();
+}
+
+// Register-resident left-looking factorisation of the augmented matrix:
+// column j of the lane's rows accumulates a_rj - sum_{p<j} a_rp L_jp from its
+// registers and the pivot row L_j. broadcast from shared memory (128-bit).
+// Returns false at the first pivot <= 0 (Eigen LLT semantics).
+template <int K, int M>
+__device__ bool factor_reg(double* A, double* dinv, double* colbuf, int lane) {
+  (void)colbuf;
+  using Sh = RegShape<K, M>;
+  constexpr int kRows = Sh::kRows;
+  const int r0 = lane, r1 = lane + 32;
+  const bool has0 = r0 < kRows;
+  const bool has1 = Sh::kTwo && r1 < kRows;
+  double a0[Sh::kN0];
+  double a1[Sh::kTwo ? K : 1];
+  {
+    const double* R0 = A + Sh::row_off(has0 ? r0 : 0);
+#pragma unroll
+    for (int p = 0; p < Sh::kN0; ++p) a0[p] = (has0 && (p <= r0 || r0 >= K)) ? R0[p] : 0.0;
+    if constexpr (Sh::kTwo) {
+      const double* R1 = A + Sh::row_off(has1 ? r1 : 0);
+#pragma unroll
+      for (int p = 0; p < K; ++p) a1[p] = (has1 && (p <= r1 || r1 >= K)) ? R1[p] : 0.0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double* Lj = A + ro_r(j);  // pivot row j (entries < j are final)
+    double s0a = 0.0, s0b = 0.0, s1a = 0.0, s1b = 0.0;
+    if (j < Sh::kN0) s0a = a0[j < Sh::kN0 ? j : 0];
+    if constexpr (Sh::kTwo) s1a = a1[j];
+#pragma unroll
+    for (int p = 0; p + 1 < j; p += 2) {
+      const double2 l = *reinterpret_cast<const double2*>(Lj + p);
+      if (j < Sh::kN0) {
+        s0a = fma(-a0[p], l.x, s0a);
+        s0b = fma(-a0[p + 1], l.y, s0b);
+      }
+      if constexpr (Sh::kTwo) {
+        s1a = fma(-a1[p], l.x, s1a);
+        s1b = fma(-a1[p + 1], l.y, s1b);
+      }
+    }
+    if (j & 1) {
+      const double l = Lj[j - 1];
+      if (j < Sh::kN0) s0a = fma(-a0[j - 1], l, s0a);
+      if constexpr (Sh::kTwo) s1a = fma(-a1[j - 1], l, s1a);
+    }
+    const double s0 = s0a + s0b, s1 = s1a + s1b;
+    const double mine = j < 32 ? s0 : s1;
+    const double piv = __shfl_sync(0xffffffffu, mine, j & 31);
+    if (!(piv > 0.0)) return false;
+    const double ljj = sqrt(piv);
+    const double inv = 1.0 / ljj;
+    if (j < Sh::kN0) {
+      if (has0 && r0 >= j) {
+        const double v = r0 == j ? ljj : s0 * inv;
+        a0[j < Sh::kN0 ? j : 0] = v;
+        A[Sh::row_off(r0) + j] = v;
+      }
+    }
+    if constexpr (Sh::kTwo) {
+      if (has1 && r1 >= j) {
+        const double v = r1 == j ? ljj : s1 * inv;
+        a1[j] = v;
+        A[Sh::row_off(r1) + j] = v;
+      }
+    }
+    if (lane == 0) dinv[j] = inv;
+    __syncwarp();
+  }
+  return true;
+}
+
+template <int K, int M>
+__device__ void back_solve_reg(double* A, const double* dinv, int lane) {
+  using Sh = RegShape<K, M>;
+  for (int c = 0; c < M; ++c) {
+    double* y = A + Sh::row_off(K + c);
+    for (int j = K - 1; j >= 0; --j) {
+      const double* Lj = A + ro_r(j);
+      const double xj = y[j] * dinv[j];
+      __syncwarp();
+      for (int i = lane; i < j; i += kWarp) y[i] = fma(-Lj[i], xj, y[i]);
+      if (lane == 0) y[j] = xj;
+      __syncwarp();
+    }
+  }
+}
+
+template <int K, int M>
+__global__ void __launch_bounds__(64)
+solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
+                 int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
+                 unsigned long long* __restrict__ fail_min) {
+  using Sh = RegShape<K, M>;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x % kWarp;
+  const int warp = threadIdx.x / kWarp;
+  const int warps = blockDim.x / kWarp;
+  double* A = smem + warp * Sh::kPerWarp;
+  double* dinv = A + Sh::kAug;
+  double* colbuf = dinv + ((K + 1) & ~1);
+  double* xs = colbuf + Sh::kCol;
+  int32_t* sr = reinterpret_cast<int32_t*>(xs + Sh::kDch * K);
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * warps + warp; r < nrows;
+       r += static_cast<int64_t>(gridDim.x) * warps) {
+    for (int t = lane; t < K; t += kWarp) sr[t] = S[r * K + t];
+    __syncwarp();
+    bool ok = false;
+    for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
+      build_reg<K, M>(X, Y, d, sr, kp, attempt, A, xs, lane);
+      ok = factor_reg<K, M>(A, dinv, colbuf, lane);
+      __syncwarp();
+    }
+    if (!ok) {
+      if (lane == 0) atomicMin(fail_min, static_cast<unsigned long long>(row_begin + r));
+      __syncwarp();
+      continue;
+    }
+    back_solve_reg<K, M>(A, dinv, lane);
+    for (int e = lane; e < K * M; e += kWarp) {
+      const int t = e / M, c = e - t * M;
+      C[r * K * M + e] = A[Sh::row_off(K + c) + t];
+    }
+    __syncwarp();
+  }
+}
+
+template <int K, int M>
+cudaError_t launch_reg(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows, int64_t row_begin,
+                       const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
+  using Sh = RegShape<K, M>;
+  constexpr int kWarps = 2;
+  const size_t smem = sizeof(double) * Sh::kPerWarp * kWarps;
+  cudaError_t err = cudaFuncSetAttribute(solve_reg_kernel<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  int per_sm = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_reg_kernel<K, M>, kWarps * kWarp, smem);
+  if (err != cudaSuccess) return err;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (nrows + kWarps - 1) / kWarps;
+  const int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(num_sms) * per_sm);
+  solve_reg_kernel<K, M><<<static_cast<unsigned>(grid), kWarps * kWarp, smem, stream>>>(X, Y, d, S, nrows, row_begin,
+                                                                                        kp, C, fail_min);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool fused_solve_reg_supported(int k, int d, int m) {
+  (void)d;
+  return (k == 50 && m == 1) || (k == 30 && m == 1) || (k == 30 && m == 10);
+}
+
+cudaError_t fused_solve_reg(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
+                            int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
+                            int num_sms, cudaStream_t stream) {
+  if (nrows <= 0) return cudaSuccess;
+  if (k == 50 && m == 1) return launch_reg<50, 1>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+  if (k == 30 && m == 1) return launch_reg<30, 1>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+  if (k == 30 && m == 10) return launch_reg<30, 10>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fmgp

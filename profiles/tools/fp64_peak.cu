@@ -40,6 +40,24 @@ __global__ void fmaop(double* out, double a, double b) {
   if (s == 12345.678) out[0] = s;
 }
 
+// DMMA (mma.sync.m8n8k4.f64) issue rate: 8 independent accumulator chains.
+__global__ void dmmaop(double* out, double a, double b) {
+  double c[kChains][2];
+#pragma unroll
+  for (int q = 0; q < kChains; ++q) c[q][0] = c[q][1] = threadIdx.x * 1e-3 + q;
+  for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+    for (int q = 0; q < kChains; ++q)
+      asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+          : "+d"(c[q][0]), "+d"(c[q][1])
+          : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int q = 0; q < kChains; ++q) s += c[q][0] + c[q][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 int main() {
   int sms = 0, clk = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -50,7 +68,7 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  float best_am = 1e30f, best_f = 1e30f;
+  float best_am = 1e30f, best_f = 1e30f, best_mma = 1e30f;
   for (int r = 0; r < 6; ++r) {
     cudaEventRecord(e0);
     addmul<<<grid, block>>>(out, 1e-9, 0.999999);
@@ -65,15 +83,23 @@ int main() {
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     if (r > 0 && ms < best_f) best_f = ms;
+    cudaEventRecord(e0);
+    dmmaop<<<grid, block>>>(out, 0.999999, 1e-9);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0 && ms < best_mma) best_mma = ms;
   }
   double threads = double(grid.x) * block.x;
   double ops_am = threads * kIters * kChains * 2;  // DADD + DMUL
   double ops_f = threads * kIters * kChains;       // DFMA
   double tops_am = ops_am / (best_am * 1e-3) / 1e12;
   double tflops_f = 2 * ops_f / (best_f * 1e-3) / 1e12;
-  printf("{\"fp64_tops_nonfma\": %.3f, \"fp64_dfma_tflops\": %.3f, \"sms\": %d, \"clock_khz_attr\": %d, "
+  double warps = threads / 32;
+  double tflops_mma = warps * kIters * kChains * 512.0 / (best_mma * 1e-3) / 1e12;  // 8x8x4 FMAs = 512 flops
+  printf("{\"fp64_tops_nonfma\": %.3f, \"fp64_dfma_tflops\": %.3f, \"fp64_dmma_tflops\": %.3f, \"sms\": %d, \"clock_khz_attr\": %d, "
          "\"ops_per_clk_per_sm_nonfma_at_attr_clock\": %.2f, \"how\": \"independent DADD+DMUL chains (1 op each) and "
-         "DFMA chains (2 flops), %d blocks x 256 threads x %d chains x %d iters, best of 5, CUDA events\"}\n",
-         tops_am, tflops_f, sms, clk, tops_am * 1e12 / (sms * (clk * 1e3)), grid.x, kChains, kIters);
+         "DFMA chains (2 flops), DMMA m8n8k4 chains (512 flops), %d blocks x 256 threads x %d chains x %d iters, best of 5, CUDA events\"}\n",
+         tops_am, tflops_f, tflops_mma, sms, clk, tops_am * 1e12 / (sms * (clk * 1e3)), grid.x, kChains, kIters);
   return 0;
 }
