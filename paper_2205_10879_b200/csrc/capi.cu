@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -161,6 +162,14 @@ int predict_device_impl(const double* X, const int32_t* S, const double* C, int6
                         int64_t nz, double* out, int32_t* nn_out, cudaStream_t stream) {
   if (nz <= 0) return FMGP_OK;
   const int sms = num_sms_current();
+  static const bool force_brute = [] {
+    const char* e = std::getenv("FMGP_KNN");
+    return e != nullptr && std::string(e) == "brute";
+  }();
+  if (!force_brute && d <= 3) {
+    FMGP_CUDA(fmgp::predict_grid(X, n, d, S, C, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, sms, stream));
+    return FMGP_OK;
+  }
   DevBuf<int32_t> nn_tmp;
   int32_t* nn = nn_out;
   if (nn == nullptr) {

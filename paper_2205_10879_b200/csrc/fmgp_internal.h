@@ -109,3 +109,12 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
                    cudaStream_t stream, float* debug_G);
 
 }  // namespace fmgp
+
+namespace fmgp {
+
+// Fused grid 1-NN + gather-kernel-dot predict for d <= 3.
+cudaError_t predict_grid(const double* X, int64_t n, int d, const int32_t* S, const double* Cf, int k, int m,
+                         const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz, double* out,
+                         int32_t* nn_out, int num_sms, cudaStream_t stream);
+
+}  // namespace fmgp

@@ -476,6 +476,126 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
   }
 }
 
+// Fused predict for d <= 3 (fast_predict_one, fast_predict.cpp:132-144): one
+// warp per test point finds the nearest training point with the same ring
+// search (an argmin over (key, index) instead of a top-k list), then
+// evaluates the k cross-covariances and the dot with C_j in the reference's
+// sequential order, without writing the 1-NN index out in between.
+template <int D>
+__global__ void __launch_bounds__(kQueryThreads)
+grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
+                    const int32_t* __restrict__ cstart, int64_t nq, const double* __restrict__ Qs,
+                    const int32_t* __restrict__ qout, const double* __restrict__ X, const int32_t* __restrict__ S,
+                    const double* __restrict__ Cf, int k, int m, KParams kp, const double* __restrict__ mean_offset,
+                    double* __restrict__ out, int32_t* __restrict__ nn_out) {
+  __shared__ int32_t s_beg[kQueryThreads / 32][kSlots];
+  __shared__ int32_t s_pre[kQueryThreads / 32][kSlots + 1];
+  const GridParams g = *gpp;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int32_t* rb = s_beg[wib];
+  int32_t* rp = s_pre[wib];
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w = warp0; w < nq; w += nwarps) {
+    double q[D];
+#pragma unroll
+    for (int t = 0; t < D; ++t) q[t] = Qs[w * D + t];
+    const int64_t orow = qout[w];
+    int c[3];
+    cell_key<D>(q, g, c);
+    Cand best{INFINITY, INT_MAX};
+    for (int r = 1;; ++r) {
+      const bool block = (r == 1);
+      const int z0 = D >= 3 ? max(0, c[2] - r) : 0, z1 = D >= 3 ? min(g.G[2] - 1, c[2] + r) : 0;
+      const int y0 = D >= 2 ? max(0, c[1] - r) : 0, y1 = D >= 2 ? min(g.G[1] - 1, c[1] + r) : 0;
+      const int xl = c[0] - r, xr = c[0] + r;
+      const int x0 = max(0, xl), x1 = min(g.G[0] - 1, xr);
+      const int ny = y1 - y0 + 1;
+      const int nrows = (z1 - z0 + 1) * ny;
+      for (int rbase = 0; rbase < nrows; rbase += 32) {
+        const int ridx = rbase + lane;
+        int32_t b0 = 0, l0 = 0, b1 = 0, l1 = 0;
+        if (ridx < nrows) {
+          const int z = z0 + ridx / ny, y = y0 + ridx % ny;
+          const bool edge = block || (D >= 3 && (z == c[2] - r || z == c[2] + r)) ||
+                            (D >= 2 && (y == c[1] - r || y == c[1] + r));
+          const int64_t rowkey = (static_cast<int64_t>(z) * g.G[1] + y) * g.G[0];
+          if (edge) {
+            b0 = cstart[rowkey + x0];
+            l0 = cstart[rowkey + x1 + 1] - b0;
+          } else {
+            if (xl >= 0) {
+              b0 = cstart[rowkey + xl];
+              l0 = cstart[rowkey + xl + 1] - b0;
+            }
+            if (xr < g.G[0]) {
+              b1 = cstart[rowkey + xr];
+              l1 = cstart[rowkey + xr + 1] - b1;
+            }
+          }
+        }
+        int32_t incl = l0 + l1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int32_t excl = incl - (l0 + l1);
+        rb[2 * lane] = b0;
+        rb[2 * lane + 1] = b1;
+        rp[2 * lane] = excl;
+        rp[2 * lane + 1] = excl + l0;
+        const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 31) rp[kSlots] = total;
+        __syncwarp();
+        for (int32_t base = 0; base < total; base += 32) {
+          const int32_t want = base + lane;
+          if (want < total) {
+            int j = 0;
+#pragma unroll
+            for (int step = kSlots / 2; step > 0; step >>= 1)
+              if (rp[j + step] <= want) j += step;
+            const int64_t p = static_cast<int64_t>(rb[j]) + (want - rp[j]);
+            double x[D];
+#pragma unroll
+            for (int t = 0; t < D; ++t) x[t] = pts[p * D + t];
+            const Cand cd{dist_sq_fixed<D>(q, x), pid[p]};
+            if (cless(cd, best)) best = cd;
+          }
+        }
+        __syncwarp();
+      }
+      // warp argmin over (key, index)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const Cand other = shfl_xor_c(best, o);
+        if (cless(other, best)) best = other;
+      }
+      const double lb2 = outside_lb_sq<D>(g, q, c, r);
+      if (lb2 == INFINITY) break;
+      if (best.d < lb2) break;
+    }
+    const int64_t j = best.i;
+    if (nn_out != nullptr && lane == 0) nn_out[orow] = static_cast<int32_t>(j);
+    for (int cc = 0; cc < m; ++cc) {
+      double acc = 0.0;
+      for (int t0 = 0; t0 < k; t0 += kWarp) {
+        const int t = t0 + lane;
+        double prod = 0.0;
+        if (t < k) {
+          const int64_t nb = S[j * k + t];
+          const double dist = sqrt(dist_sq_fixed<D>(q, X + nb * D));
+          prod = __dmul_rn(kernel_eval(dist, kp), Cf[(j * k + t) * m + cc]);
+        }
+        const int cnt = min(kWarp, k - t0);
+        for (int s2 = 0; s2 < cnt; ++s2) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, prod, s2));
+      }
+      if (lane == 0) out[orow * m + cc] = __dadd_rn(acc, mean_offset[cc]);
+    }
+  }
+}
+
 __global__ void compact_rows_kernel(const int32_t* __restrict__ pid, int64_t n, int64_t rb, int64_t re,
                                     int32_t* __restrict__ qpos, int32_t* __restrict__ counter) {
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
@@ -621,7 +741,55 @@ cudaError_t knn_grid_d(const double* Q, int64_t nq, const double* P, int64_t np,
   return err;
 }
 
+template <int D>
+cudaError_t predict_grid_d(const double* X, int64_t n, const int32_t* S, const double* Cf, int k, int m,
+                           const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz, double* out,
+                           int32_t* nn_out, int num_sms, cudaStream_t s) {
+  const double per_cell = (D == 1) ? 4.0 : (D == 2 ? 4.0 : 3.0);  // ~1 neighbour wanted: small cells
+  const int64_t ncap = n;
+  GridParams* gp = nullptr;
+  unsigned long long* mm = nullptr;
+  SortBufs pb, qb;
+  cudaError_t err = cudaMallocAsync(&gp, sizeof(GridParams), s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&mm, sizeof(unsigned long long) * 6, s);
+  if (err == cudaSuccess) err = pb.alloc(n, ncap, D, s);
+  if (err == cudaSuccess) err = qb.alloc(nz, ncap, D, s);
+  if (err != cudaSuccess) return err;
+  cudaMemsetAsync(mm, 0, sizeof(unsigned long long) * 6, s);
+  for (int t = 0; t < D; ++t) cudaMemsetAsync(mm + 2 * t, 0xFF, sizeof(unsigned long long), s);
+  bbox_kernel<<<grid1d(n), 256, 0, s>>>(X, n, D, mm);
+  grid_params_kernel<<<1, 1, 0, s>>>(mm, n, D, per_cell, ncap, gp);
+  note_launches(2);
+  cell_sort<D>(X, n, gp, ncap, pb, s);
+  cell_sort<D>(Z, nz, gp, ncap, qb, s);
+  int64_t blocks = (nz * 32 + kQueryThreads - 1) / kQueryThreads;
+  const int64_t cap = static_cast<int64_t>(num_sms) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  grid_predict_kernel<D><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(
+      gp, pb.pts, pb.pid, pb.cstart, nz, qb.pts, qb.pid, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out);
+  note_launches(1);
+  err = cudaGetLastError();
+  cudaFreeAsync(gp, s);
+  cudaFreeAsync(mm, s);
+  pb.release(s);
+  qb.release(s);
+  return err;
+}
+
 }  // namespace
+
+cudaError_t predict_grid(const double* X, int64_t n, int d, const int32_t* S, const double* Cf, int k, int m,
+                         const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz, double* out,
+                         int32_t* nn_out, int num_sms, cudaStream_t stream) {
+  if (nz <= 0) return cudaSuccess;
+  switch (d) {
+    case 1: return predict_grid_d<1>(X, n, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
+    case 2: return predict_grid_d<2>(X, n, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
+    case 3: return predict_grid_d<3>(X, n, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 bool knn_grid_supported(int d, int kk) { return d >= 1 && d <= 3 && kk >= 1 && kk <= 128; }
 

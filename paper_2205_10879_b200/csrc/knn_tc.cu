@@ -13,17 +13,20 @@
 //             tiles (TMEM columns): tcgen05.mma.cta_group::1.kind::f16,
 //             M=128 N=256 K=16, fp32 accumulators in TMEM (two 256-column
 //             buffers, 512 columns), A/B staged by TMA (SWIZZLE_128B, 4 stages).
-//   filter    D~ = n^_q + n^_p - 2 G~ (fp32). Keep p iff D~ <= F_q with
-//             F_q = (s sqrt(T_q)(1+1e-12) + eta_q)^2 + eps_q, T_q the exact
-//             kk-th key so far, eta_q = 2^-11 (||q^|| + max||p^||) (1 + 1e-3)
-//             bounding the fp16 input rounding of the distance, and
-//             eps_q = (DP + 8) 2^-22 (n^_q + max n^_p) bounding fp32
-//             accumulation (even with truncating adds) and the combination.
-//             Any p whose exact key can reach the top-kk passes.
-//   recheck   passing p get the exact fp64 key from the original coordinates
-//             and are inserted into the query's sorted (key, index) list;
-//             points are streamed in ascending index, so equal keys keep the
-//             lower index (the reference's max-heap order).
+//   filter    D~ = n^_q + n^_p - 2 G~ (fp32) approximates s^2 D (D = exact key):
+//             |D~ - s^2 D| <= E(D) = 2 eta s sqrt(D) + eta^2 + eps with
+//             eta_q = 2^-11 (||q^|| + max||p^||)(1+1e-3) + 2^-24 sqrt(DP) (fp16 input
+//             rounding, subnormals included) and eps_q = (DP+8) 2^-22 (n^_q + max n^_p)
+//             (fp32 accumulation even with truncating adds, and the combination).
+//   epilogue  per query a shared-memory list, sorted by D~, that keeps every point
+//             with D~ <= W = T~ + 2 E(T~) (T~ = kk-th smallest D~ in the list): any
+//             point of the exact top-kk satisfies this at every moment, so it is
+//             never dropped. No fp64 work during the scan.
+//   recheck   at the end of a query tile each list entry (kk + a few) gets its
+//             exact fp64 key from the original coordinates; the exact top-kk by
+//             (key, index) is selected — the reference's order. A list that
+//             would overflow its capacity flags the query, which is then redone
+//             by the exact fp64 brute-force kernel.
 // Roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
 // issuer (one elected lane), warps 2-5 epilogue (thread = TMEM lane = query).
 #include <cuda.h>
@@ -42,12 +45,14 @@ namespace fmgp {
 namespace {
 
 constexpr int kBM = 128;  // queries per tile (TMEM lanes)
-constexpr int kBN = 256;  // reference points per tile (TMEM columns per buffer)
+constexpr int kBN = 128;  // reference points per tile (TMEM columns per buffer)
 constexpr int kBK = 64;   // fp16 dims per k-block (one 128 B swizzle row)
-constexpr int kStages = 4;
+constexpr int kStages = 2;
+constexpr int kCapMax = 128;  // candidate-list capacity per query (kk <= kCapMax - 29)
 constexpr int kThreads = 192;
+constexpr int kScrStride = 36;  // floats per lane scratch row (16 B aligned, spreads banks)
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
-constexpr uint32_t kBBytes = kBN * kBK * 2;  // 32 KB
+constexpr uint32_t kBBytes = kBN * kBK * 2;  // 16 KB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -105,7 +110,7 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   d |= static_cast<uint64_t>(2u) << 61;             // SWIZZLE_128B
   return d;
 }
-// kind::f16 instruction descriptor: fp16 x fp16 -> fp32, both K-major, M=128, N=256.
+// kind::f16 instruction descriptor: fp16 x fp16 -> fp32, both K-major, M=128, N=kBN.
 constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
                             (static_cast<uint32_t>(kBM >> 4) << 24);
 
@@ -181,48 +186,40 @@ struct TcArgs {
   const float* qn;       // ||q^||^2
   const float* pn;       // ||p^||^2
   int64_t nq, np;
-  int d, DP, KB, kk;
+  int d, DP, KB, kk, cap;
   int64_t self_offset;   // exclude p == q + self_offset when >= 0
   const int32_t* excl;   // or per-query exclusion (nullable)
   int with_self;
   int32_t* out;          // nq x (kk + with_self)
   double* out_d;         // nq x kk (nullable)
-  double* wd;            // nq x kk scratch lists
+  double* wd;            // nq x kk exact selection scratch
   int32_t* wi;
+  int32_t* overflow;     // [0] = count, [1..] = query ids whose list overflowed
   const unsigned long long* maxabs_bits;
   const unsigned long long* pmax_bits;
-  float* debug_G;        // when non-null: D~ of (query tile 0, point tile 0), 128 x 256, and no search
+  float* debug_G;        // when non-null: D~ of (query tile 0, point tile 0) and no search
 };
 
-__device__ __forceinline__ void list_insert_tc(double* ld, int32_t* li, int& cnt, int kk, double s, int32_t j,
-                                               double& thr) {
-  int pos = cnt < kk ? cnt : kk - 1;
-  while (pos > 0) {
-    const double pd = ld[pos - 1];
-    if (pd > s) {
-      ld[pos] = pd;
-      li[pos] = li[pos - 1];
-      --pos;
-    } else {
-      break;
-    }
-  }
-  ld[pos] = s;
-  li[pos] = j;
-  if (cnt < kk) ++cnt;
-  if (cnt == kk) thr = ld[kk - 1];
+// Admission window W = T + 2 E(T), E(T) = 2 eta (sqrt(T) + 2 eta) + eta^2 + eps (scaled units).
+__device__ __forceinline__ float window_of(float T, double eta, double eps) {
+  const double t = static_cast<double>(T);
+  const double E = 2.0 * eta * (sqrt(t) + 2.0 * eta) + eta * eta + eps;
+  return static_cast<float>((t + 2.0 * E) * 1.0001 + 1e-30);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmP, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte alignment for SWIZZLE_128B tiles
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                 // kStages x 16 KB
-  uint8_t* sB = smem + kStages * kABytes;             // kStages x 32 KB
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+  uint8_t* sB = smem + kStages * kABytes;             // kStages x 16 KB
+  float* lk = reinterpret_cast<float*>(sB + kStages * kBBytes);  // [cap][128] candidate D~ (column = query)
+  int32_t* li = reinterpret_cast<int32_t*>(lk + a.cap * kBM);   // [cap][128] candidate index
+  float* pn_stage = reinterpret_cast<float*>(li + a.cap * kBM);      // [4 warps][kBN]
+  float* scratch = pn_stage + 4 * kBN;                                // [4 warps][32 lanes][kScrStride]
+  uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 4 * 32 * kScrStride);
   uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;   // 2 TMEM buffers
+  uint64_t* tfull = empty + kStages;  // 2 TMEM buffers
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -243,7 +240,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(2 * kBN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -309,61 +307,168 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       }
     }
   } else {
-    // ---------------- epilogue: thread = TMEM lane = query row
+    // ---------------- epilogue: thread = TMEM lane = query row of the tile
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
-    const double maxabs = __longlong_as_double(static_cast<long long>(*a.maxabs_bits));
-    const double s = maxabs > 0.0 ? exp2(floor(log2(16384.0 / maxabs))) : 1.0;
     const double pmax = __longlong_as_double(static_cast<long long>(*a.pmax_bits));
+    float* pns = pn_stage + (warp - 2) * kBN;          // this warp's copy of the tile's point norms
+    float* scr = scratch + ((warp - 2) * 32 + lane) * kScrStride;  // this lane's hot-chunk values
+    float* mk = lk + row;    // this query's column of the candidate list (stride kBM)
+    int32_t* mi = li + row;
     int buf = 0;
     uint32_t tphase = 0;
     for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
       const int64_t q = qt * kBM + row;
       const bool valid = q < a.nq;
       const double nq_hat = valid ? static_cast<double>(a.qn[q]) : 0.0;
-      // 2^-11 (||q^|| + max||p^||) relative rounding + 2^-25 per (possibly subnormal) coordinate
-      const double eta = 4.8828125e-4 * (sqrt(nq_hat) + pmax) * 1.001 + 2.0 * 2.98023223876953125e-8 * sqrt(double(a.DP));
-      const double eps = (a.DP + 8) * 2.384185791015625e-7 * (nq_hat + pmax * pmax);  // (DP+8) 2^-22 (...)
+      const float nqf = static_cast<float>(nq_hat);
+      const double eta = 4.8828125e-4 * (sqrt(nq_hat) + pmax) * 1.001 + 5.9604644775390625e-8 * sqrt(double(a.DP));
+      const double eps = (a.DP + 8) * 2.384185791015625e-7 * (nq_hat + pmax * pmax);
       const int64_t excl = a.excl != nullptr ? (valid ? a.excl[q] : -1)
                                              : (a.self_offset >= 0 ? q + a.self_offset : -1);
-      double* ld = a.wd + (valid ? q : 0) * a.kk;
-      int32_t* li = a.wi + (valid ? q : 0) * a.kk;
-      const double* qx = a.Q + (valid ? q : 0) * a.d;
-      int cnt = 0;
-      double thr = valid ? INFINITY : -INFINITY;
-      float fthr = valid ? INFINITY : -INFINITY;  // bound on pn - 2G for admission
+      // Candidate state (shared memory, column `row`, stride kBM):
+      //   heap[0..hn)   max-heap by D~ of the kk smallest so far (root = T~)
+      //   wb[0..wn)     window buffer: points with T~ < D~ <= W = T~ + 2E(T~)
+      // Every point of the exact top-kk is in heap u wb at all times.
+      float* hk = mk;
+      int32_t* hi = mi;
+      float* wk = mk + a.kk * kBM;
+      int32_t* wi_ = mi + a.kk * kBM;
+      const int wcap = a.cap - a.kk;
+      int hn = 0, wn = 0;
+      bool over = false;
+      float win = valid ? INFINITY : -INFINITY;  // admission bound on D~ - n^_q
+      float root = INFINITY;
       const int64_t pt_end = a.debug_G ? 1 : npt;
       for (int64_t pt = 0; pt < pt_end; ++pt) {
         mbar_wait(&tfull[buf], tphase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + lane_addr + static_cast<uint32_t>(buf * kBN);
+        // point norms of this tile, staged in this warp's smem slice and read back as
+        // float4 broadcasts; points past np get NaN (never admitted, ignored by fminf)
+        __syncwarp();
+#pragma unroll
+        for (int ch = 0; ch < kBN / 32; ++ch) {
+          const int64_t j = pt * kBN + ch * 32 + lane;
+          pns[ch * 32 + lane] = j < a.np ? __ldg(a.pn + j) : __int_as_float(0x7fffffff);
+        }
+        __syncwarp();
+#pragma unroll
         for (int ch = 0; ch < kBN / 32; ++ch) {
           uint32_t r[32];
+          __syncwarp();  // tcgen05.ld is warp-collective; the admission loop diverges
           tmem_ld32(tbase + ch * 32, r);
           const int64_t j0 = pt * kBN + ch * 32;
           if (a.debug_G) {
             if (qt == 0)
               for (int c = 0; c < 32; ++c)
-                a.debug_G[row * kBN + ch * 32 + c] =
-                    static_cast<float>(nq_hat) + fmaf(-2.0f, __uint_as_float(r[c]), j0 + c < a.np ? a.pn[j0 + c] : 0.f);
+                a.debug_G[row * 256 + ch * 32 + c] =
+                    j0 + c < a.np ? nqf + fmaf(-2.0f, __uint_as_float(r[c]), pns[ch * 32 + c]) : 0.0f;
             continue;
           }
-#pragma unroll 8
-          for (int c = 0; c < 32; ++c) {
+          // v_c = D~ - n^_q; a chunk with nothing under the window (for any lane) is skipped
+          float m0 = INFINITY, m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 p4 = *reinterpret_cast<const float4*>(pns + ch * 32 + 4 * c4);
+            const float v0 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 0]), p4.x);
+            const float v1 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 1]), p4.y);
+            const float v2 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 2]), p4.z);
+            const float v3 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 3]), p4.w);
+            r[4 * c4 + 0] = __float_as_uint(v0);
+            r[4 * c4 + 1] = __float_as_uint(v1);
+            r[4 * c4 + 2] = __float_as_uint(v2);
+            r[4 * c4 + 3] = __float_as_uint(v3);
+            m0 = fminf(m0, v0);
+            m1 = fminf(m1, v1);
+            m2 = fminf(m2, v2);
+            m3 = fminf(m3, v3);
+          }
+          const float vmin = fminf(fminf(m0, m1), fminf(m2, m3));
+          if (!__any_sync(0xffffffffu, vmin <= win)) continue;
+          // hot chunk: per-lane bit mask of admissible columns; values parked in this
+          // lane's scratch row so the admission loop visits only the set bits
+          uint32_t mask = 0;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) mask |= (__uint_as_float(r[c]) <= win ? 1u : 0u) << c;
+          if (mask == 0) continue;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4)
+            *reinterpret_cast<uint4*>(scr + 4 * c4) = make_uint4(r[4 * c4], r[4 * c4 + 1], r[4 * c4 + 2], r[4 * c4 + 3]);
+          while (mask != 0) {
+            const int c = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float v = scr[c];
             const int64_t j = j0 + c;
-            const float v = fmaf(-2.0f, __uint_as_float(r[c]), j < a.np ? __ldg(a.pn + j) : 0.0f);
-            if (v <= fthr && j < a.np && j != excl) {
-              // exact fp64 key, the reference's order
-              const double key = dist_sq_dyn(qx, a.P + j * a.d, a.d);
-              if (key < thr) {
-                list_insert_tc(ld, li, cnt, a.kk, key, static_cast<int32_t>(j), thr);
-                if (cnt == a.kk) {
-                  const double rr = s * sqrt(thr) * (1.0 + 1e-12) + eta;
-                  const double F = rr * rr + eps - nq_hat;
-                  fthr = static_cast<float>(F * (1.0 + 1e-6) + 1e-30);
-                }
+            if (!(v <= win) || j == excl) continue;
+            if (hn < a.kk) {  // fill the heap (sift up)
+              int pos = hn++;
+              while (pos > 0) {
+                const int par = (pos - 1) >> 1;
+                const float pk = hk[par * kBM];
+                if (pk >= v) break;
+                hk[pos * kBM] = pk;
+                hi[pos * kBM] = hi[par * kBM];
+                pos = par;
               }
+              hk[pos * kBM] = v;
+              hi[pos * kBM] = static_cast<int32_t>(j);
+              if (hn == a.kk) {
+                root = hk[0];
+                win = window_of(root + nqf, eta, eps) - nqf;
+              }
+              continue;
+            }
+            float vk = v;  // the value that goes to the window buffer
+            int32_t vi = static_cast<int32_t>(j);
+            if (v < root) {  // replace the root, sift down; the old root moves to the buffer
+              vk = root;
+              vi = hi[0];
+              int pos = 0;
+              for (;;) {
+                const int l = 2 * pos + 1;
+                if (l >= a.kk) break;
+                int ch2 = l;
+                float ck = hk[l * kBM];
+                if (l + 1 < a.kk) {
+                  const float rk = hk[(l + 1) * kBM];
+                  if (rk > ck) {
+                    ck = rk;
+                    ch2 = l + 1;
+                  }
+                }
+                if (ck <= v) break;
+                hk[pos * kBM] = ck;
+                hi[pos * kBM] = hi[ch2 * kBM];
+                pos = ch2;
+              }
+              hk[pos * kBM] = v;
+              hi[pos * kBM] = static_cast<int32_t>(j);
+              root = hk[0];
+              win = window_of(root + nqf, eta, eps) - nqf;
+            }
+            if (vk <= win) {
+              if (wn == wcap) {  // compact: drop entries that left the window
+                int o = 0;
+                for (int t = 0; t < wn; ++t) {
+                  const float tk = wk[t * kBM];
+                  if (tk <= win) {
+                    wk[o * kBM] = tk;
+                    wi_[o * kBM] = wi_[t * kBM];
+                    ++o;
+                  }
+                }
+                wn = o;
+              }
+              if (wn == wcap) {
+                over = true;  // the query is redone exactly
+                win = -INFINITY;
+                continue;
+              }
+              wk[wn * kBM] = vk;
+              wi_[wn * kBM] = vi;
+              ++wn;
             }
           }
         }
@@ -374,15 +479,51 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           tphase ^= 1;
         }
       }
-      if (valid && !a.debug_G) {
-        const int width = a.kk + (a.with_self ? 1 : 0);
-        int32_t* orow = a.out + q * width;
-        int o = 0;
-        if (a.with_self) orow[o++] = static_cast<int32_t>(q + a.self_offset);
-        for (int t = 0; t < a.kk; ++t) {
-          orow[o + t] = t < cnt ? li[t] : INT_MAX;
-          if (a.out_d) a.out_d[q * a.kk + t] = t < cnt ? ld[t] : INFINITY;
+      // candidates = heap u buffer (the exact top-kk is inside)
+      int cnt = hn;
+      for (int t = 0; t < wn; ++t) {
+        mk[cnt * kBM] = wk[t * kBM];
+        mi[cnt * kBM] = wi_[t * kBM];
+        ++cnt;
+      }
+      if (!valid || a.debug_G) continue;
+      if (over) {
+        const int32_t slot = atomicAdd(a.overflow, 1);
+        a.overflow[1 + slot] = static_cast<int32_t>(q);
+        continue;
+      }
+      // exact recheck of the window and selection of the top-kk by (key, index)
+      double* wd = a.wd + q * a.kk;
+      int32_t* wi = a.wi + q * a.kk;
+      const double* qx = a.Q + q * a.d;
+      int m = 0;
+      double thr = INFINITY;
+      int32_t thr_i = INT_MAX;
+      for (int t = 0; t < cnt; ++t) {
+        const int32_t j = mi[t * kBM];
+        const double key = dist_sq_dyn(qx, a.P + static_cast<int64_t>(j) * a.d, a.d);
+        if (m == a.kk && !pair_less(key, j, thr, thr_i)) continue;
+        int pos = m < a.kk ? m : a.kk - 1;
+        while (pos > 0 && pair_less(key, j, wd[pos - 1], wi[pos - 1])) {
+          wd[pos] = wd[pos - 1];
+          wi[pos] = wi[pos - 1];
+          --pos;
         }
+        wd[pos] = key;
+        wi[pos] = j;
+        if (m < a.kk) ++m;
+        if (m == a.kk) {
+          thr = wd[a.kk - 1];
+          thr_i = wi[a.kk - 1];
+        }
+      }
+      const int width = a.kk + (a.with_self ? 1 : 0);
+      int32_t* orow = a.out + q * width;
+      int o = 0;
+      if (a.with_self) orow[o++] = static_cast<int32_t>(q + a.self_offset);
+      for (int t = 0; t < a.kk; ++t) {
+        orow[o + t] = t < m ? wi[t] : INT_MAX;
+        if (a.out_d) a.out_d[q * a.kk + t] = t < m ? wd[t] : INFINITY;
       }
     }
   }
@@ -390,7 +531,36 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kBN));
+  }
+}
+
+// Redo the overflowed queries exactly (brute force): gather their rows, run
+// the fp64 scan with per-query exclusion, scatter the rows back.
+__global__ void gather_rows_kernel(const double* __restrict__ Q, int d, const int32_t* __restrict__ ids, int cnt,
+                                   int64_t self_offset, const int32_t* __restrict__ excl_in, double* __restrict__ Qg,
+                                   int32_t* __restrict__ excl_out) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < static_cast<int64_t>(cnt) * d;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / d), t = static_cast<int>(e % d);
+    const int64_t q = ids[r];
+    Qg[e] = Q[q * d + t];
+    if (t == 0)
+      excl_out[r] = excl_in != nullptr ? excl_in[q] : (self_offset >= 0 ? static_cast<int32_t>(q + self_offset) : -1);
+  }
+}
+
+__global__ void scatter_rows_kernel(const int32_t* __restrict__ rows, const double* __restrict__ rows_d,
+                                    const int32_t* __restrict__ ids, int cnt, int kk, int with_self,
+                                    int64_t self_offset, int32_t* __restrict__ out, double* __restrict__ out_d) {
+  const int width = kk + (with_self ? 1 : 0);
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < static_cast<int64_t>(cnt) * kk;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / kk), t = static_cast<int>(e % kk);
+    const int64_t q = ids[r];
+    if (with_self && t == 0) out[q * width] = static_cast<int32_t>(q + self_offset);
+    out[q * width + (with_self ? 1 : 0) + t] = rows[e];
+    if (out_d) out_d[q * kk + t] = rows_d[e];
   }
 }
 
@@ -420,7 +590,7 @@ unsigned g1(int64_t n) {
 
 }  // namespace
 
-bool knn_tc_supported(int d, int kk) { return d >= 4 && d <= 1024 && kk >= 1; }
+bool knn_tc_supported(int d, int kk) { return d >= 4 && d <= 1024 && kk >= 1 && kk <= kCapMax - 29; }
 
 cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
                    const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
@@ -428,10 +598,11 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   if (nq <= 0) return cudaSuccess;
   const int KB = (d + kBK - 1) / kBK;
   const int DP = KB * kBK;
+  const int cap = std::min(kCapMax, ((kk + 29 + 3) / 4) * 4);
   __half *Qh = nullptr, *Ph = nullptr;
   float *qn = nullptr, *pn = nullptr;
   double *sums = nullptr, *wd = nullptr;
-  int32_t* wi = nullptr;
+  int32_t *wi = nullptr, *ovf = nullptr;
   unsigned long long* bits = nullptr;  // [0] maxabs, [1] pmax
   cudaError_t err = cudaMallocAsync(&Qh, sizeof(__half) * nq * DP, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&Ph, sizeof(__half) * np * DP, s);
@@ -441,9 +612,11 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   if (err == cudaSuccess) err = cudaMallocAsync(&bits, sizeof(unsigned long long) * 2, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&wd, sizeof(double) * nq * kk, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&wi, sizeof(int32_t) * nq * kk, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&ovf, sizeof(int32_t) * (nq + 1), s);
   if (err != cudaSuccess) return err;
   cudaMemsetAsync(sums, 0, sizeof(double) * d, s);
   cudaMemsetAsync(bits, 0, sizeof(unsigned long long) * 2, s);
+  cudaMemsetAsync(ovf, 0, sizeof(int32_t), s);
   mean_kernel<<<dim3(256, (d + 255) / 256), 256, 0, s>>>(P, np, d, sums);
   maxabs_kernel<<<g1(np * d), 256, 0, s>>>(P, np, d, sums, np, bits);
   if (Q != P) maxabs_kernel<<<g1(nq * d), 256, 0, s>>>(Q, nq, d, sums, np, bits);
@@ -464,6 +637,7 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.DP = DP;
   a.KB = KB;
   a.kk = kk;
+  a.cap = cap;
   a.self_offset = self_offset;
   a.excl = excl_arr;
   a.with_self = with_self;
@@ -471,10 +645,12 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.out_d = out_d;
   a.wd = wd;
   a.wi = wi;
+  a.overflow = ovf;
   a.maxabs_bits = bits;
   a.pmax_bits = bits + 1;
   a.debug_G = debug_G;
-  const size_t smem = 1024 + kStages * kStageBytes + 256;
+  const size_t smem = 1024 + kStages * kStageBytes + static_cast<size_t>(cap) * kBM * 8 +
+                      sizeof(float) * 4 * (kBN + 32 * kScrStride) + 256;
   err = cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   const int64_t nqt = (nq + kBM - 1) / kBM;
@@ -482,8 +658,33 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   knn_tc_kernel<<<debug_G ? 1 : grid, kThreads, smem, s>>>(mq, mp, a);
   note_launches(1);
   err = cudaGetLastError();
+  if (err == cudaSuccess && debug_G == nullptr) {
+    // exact fallback for the (rare) queries whose candidate window overflowed
+    int32_t novf = 0;
+    err = cudaMemcpyAsync(&novf, ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+    if (err == cudaSuccess && novf > 0) {
+      double *Qg = nullptr, *rd = nullptr;
+      int32_t *eg = nullptr, *rows = nullptr;
+      err = cudaMallocAsync(&Qg, sizeof(double) * novf * d, s);
+      if (err == cudaSuccess) err = cudaMallocAsync(&eg, sizeof(int32_t) * novf, s);
+      if (err == cudaSuccess) err = cudaMallocAsync(&rows, sizeof(int32_t) * novf * kk, s);
+      if (err == cudaSuccess) err = cudaMallocAsync(&rd, sizeof(double) * novf * kk, s);
+      if (err == cudaSuccess) {
+        gather_rows_kernel<<<g1(static_cast<int64_t>(novf) * d), 256, 0, s>>>(Q, d, ovf + 1, novf, self_offset,
+                                                                              excl_arr, Qg, eg);
+        err = knn_bruteforce(Qg, novf, P, np, d, kk, -1, eg, 0, rows, rd, num_sms, s);
+        scatter_rows_kernel<<<g1(static_cast<int64_t>(novf) * kk), 256, 0, s>>>(rows, rd, ovf + 1, novf, kk,
+                                                                                with_self, self_offset, out, out_d);
+        note_launches(2);
+      }
+      for (void* p : {static_cast<void*>(Qg), static_cast<void*>(eg), static_cast<void*>(rows), static_cast<void*>(rd)})
+        if (p) cudaFreeAsync(p, s);
+    }
+  }
   for (void* p : {static_cast<void*>(Qh), static_cast<void*>(Ph), static_cast<void*>(qn), static_cast<void*>(pn),
-                  static_cast<void*>(sums), static_cast<void*>(bits), static_cast<void*>(wd), static_cast<void*>(wi)})
+                  static_cast<void*>(sums), static_cast<void*>(bits), static_cast<void*>(wd), static_cast<void*>(wi),
+                  static_cast<void*>(ovf)})
     cudaFreeAsync(p, s);
   return err;
 }

@@ -45,6 +45,20 @@ def test_precompute_and_predict_match_oracle(fm, port, cfg, n, nt):
     assert mean_rel_err(pred, out_o.reshape(pred.shape)).max() <= MEAN_TOL
     nn = model.index.nearest_batch(ds.Z)
     assert np.array_equal(nn, nn_o)
+    # the fused predict path's own 1-NN (fmgp_predict nn_out) is the reference's too
+    import ctypes as C
+    from paper_2205_10879_b200 import _native as N
+    k_, m_ = model.S.shape[1], info.m
+    out2 = np.empty((ds.Z.shape[0], m_))
+    nn2 = np.empty(ds.Z.shape[0], dtype=np.int32)
+    kp = model.params.c(model.kind)
+    mo = np.ascontiguousarray(np.broadcast_to(np.asarray(ds.mean_offset, dtype=np.float64), (m_,)))
+    Cc = np.ascontiguousarray(model.C.reshape(n, k_, m_))
+    N.check(N.LIB.fmgp_predict(ds.X.ctypes.data, model.S.ctypes.data, Cc.ctypes.data, n, info.d, k_, m_,
+                               C.byref(kp), mo.ctypes.data, ds.Z.ctypes.data, ds.Z.shape[0], out2.ctypes.data,
+                               nn2.ctypes.data))
+    assert np.array_equal(nn2, nn_o)
+    assert mean_rel_err(out2, out_o).max() <= MEAN_TOL
 
 
 def test_ties_resolve_by_ascending_index(fm):
