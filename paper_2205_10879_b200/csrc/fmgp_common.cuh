@@ -185,6 +185,36 @@ __device__ __forceinline__ double kernel_eval(double dist, const KParams& p) {
   return __dmul_rn(p.s2, br);
 }
 
+// exp(-a) for a >= 0 (the only sign the kernels need): Cody-Waite reduction
+// r = n ln2 - a, |r| <= ln2/2, degree-13 Taylor polynomial (truncation
+// < 5e-18 relative), then 2^-n built directly in the exponent field. Result
+// within ~1 ulp of exp(-a); a >= 708 (exp < 3.3e-308) returns 0; NaN passes.
+__constant__ double kExpTaylor[14] = {1.0,
+                                      1.0,
+                                      0.5,
+                                      1.6666666666666666e-01,
+                                      4.1666666666666664e-02,
+                                      8.3333333333333332e-03,
+                                      1.3888888888888889e-03,
+                                      1.9841269841269841e-04,
+                                      2.4801587301587302e-05,
+                                      2.7557319223985893e-06,
+                                      2.7557319223985888e-07,
+                                      2.5052108385441720e-08,
+                                      2.0876756987868100e-09,
+                                      1.6059043836821613e-10};
+__device__ __forceinline__ double exp_neg(double a) {
+  if (!(a < 708.0)) return a == a ? 0.0 : a;
+  const double n = rint(a * 1.4426950408889634);
+  double r = fma(n, 6.93147180369123816490e-01, -a);
+  r = fma(n, 1.90821492927058770002e-10, r);
+  double q = kExpTaylor[13];
+#pragma unroll
+  for (int i = 12; i >= 0; --i) q = fma(q, r, kExpTaylor[i]);
+  const int e = 1023 - static_cast<int>(n);  // n in [0, 1022]
+  return q * __hiloint2double(e << 20, 0);
+}
+
 // kernel_value for the neighbourhood matrices of the fused solve: the same
 // formulas with 1/rho multiplied instead of divided and contraction allowed.
 // The matrix entries differ from kernel_eval by at most a few ulps, far inside
@@ -194,15 +224,15 @@ __device__ __forceinline__ double kernel_eval_fast(double dist, const KParams& p
   double br;
   if (p.kind == 1) {
     const double u = dist * p.inv_rho;
-    br = exp(-0.5 * u * u);
+    br = exp_neg(0.5 * u * u);
   } else if (p.nu_code == 0) {
-    br = exp(-dist * p.inv_rho);
+    br = exp_neg(dist * p.inv_rho);
   } else if (p.nu_code == 1) {
     const double a = 1.7320508075688772 * dist * p.inv_rho;
-    br = (1.0 + a) * exp(-a);
+    br = (1.0 + a) * exp_neg(a);
   } else if (p.nu_code == 2) {
     const double a = 2.2360679774997898 * dist * p.inv_rho;
-    br = fma(a, a * (1.0 / 3.0), 1.0 + a) * exp(-a);
+    br = fma(a, a * (1.0 / 3.0), 1.0 + a) * exp_neg(a);
   } else {
     return kernel_eval(dist, p);
   }

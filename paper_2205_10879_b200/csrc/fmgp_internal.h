@@ -91,6 +91,12 @@ cudaError_t fused_solve_tc(const double* X, const double* Y, int d, int m, const
 
 namespace fmgp {
 
+// CTA-per-neighbourhood variant of fused_solve for large compile-time k.
+bool fused_solve_cta_supported(int k, int d, int m);
+cudaError_t fused_solve_cta(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
+                            int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
+                            int num_sms, cudaStream_t stream);
+
 // Register-resident-row variant of fused_solve for compile-time shapes.
 bool fused_solve_reg_supported(int k, int d, int m);
 cudaError_t fused_solve_reg(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,

@@ -37,6 +37,9 @@
 #include <climits>
 #include <cmath>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "fmgp_common.cuh"
 #include "fmgp_internal.h"
 
@@ -79,6 +82,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// Back-off variant for the producer-side roles (TMA, MMA): when the epilogue
+// is the bottleneck their spin would otherwise take its issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(su32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+    __nanosleep(128);
+  }
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -114,7 +133,7 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
                             (static_cast<uint32_t>(kBM >> 4) << 24);
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
       "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
@@ -123,8 +142,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------------ prep
 
@@ -192,8 +211,8 @@ struct TcArgs {
   int with_self;
   int32_t* out;          // nq x (kk + with_self)
   double* out_d;         // nq x kk (nullable)
-  double* wd;            // nq x kk exact selection scratch
-  int32_t* wi;
+  int32_t* cand;         // [cap][nq] candidate ids, column-major (coalesced stores)
+  int32_t* ccount;       // [nq] candidates per query, -1 = overflowed
   int32_t* overflow;     // [0] = count, [1..] = query ids whose list overflowed
   const unsigned long long* maxabs_bits;
   const unsigned long long* pmax_bits;
@@ -258,7 +277,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         const int64_t pt_end = a.debug_G ? 1 : npt;
         for (int64_t pt = 0; pt < pt_end; ++pt) {
           for (int kb = 0; kb < a.KB; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_wait_sleep(&empty[stage], phase ^ 1);
             mbar_expect_tx(&full[stage], kStageBytes);
             tma_load_2d(sA + stage * kABytes, &tmQ, &full[stage], kb * kBK, static_cast<int>(qt * kBM));
             tma_load_2d(sB + stage * kBBytes, &tmP, &full[stage], kb * kBK, static_cast<int>(pt * kBN));
@@ -279,7 +298,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
       const int64_t pt_end = a.debug_G ? 1 : npt;
       for (int64_t pt = 0; pt < pt_end; ++pt) {
-        mbar_wait(&tempty[buf], tphase ^ 1);
+        mbar_wait_sleep(&tempty[buf], tphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * kBN);
         for (int kb = 0; kb < a.KB; ++kb) {
@@ -318,6 +337,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     int32_t* mi = li + row;
     int buf = 0;
     uint32_t tphase = 0;
+    float pnext[kBN / 32];  // norms of the next point tile
+#pragma unroll
+    for (int ch = 0; ch < kBN / 32; ++ch) {
+      const int64_t j = ch * 32 + lane;
+      pnext[ch] = j < a.np ? __ldg(a.pn + j) : __int_as_float(0x7fffffff);
+    }
     for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
       const int64_t q = qt * kBM + row;
       const bool valid = q < a.nq;
@@ -342,133 +367,147 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       float root = INFINITY;
       const int64_t pt_end = a.debug_G ? 1 : npt;
       for (int64_t pt = 0; pt < pt_end; ++pt) {
+        // point norms of this tile (prefetched into registers during the previous
+        // tile), staged in this warp's smem slice and read back as float4
+        // broadcasts; points past np are NaN (never admitted, ignored by fminf)
+        __syncwarp();
+#pragma unroll
+        for (int ch = 0; ch < kBN / 32; ++ch) pns[ch * 32 + lane] = pnext[ch];
+        __syncwarp();
+        {
+          const int64_t nxt = pt + 1 < pt_end ? pt + 1 : 0;  // next tile (or tile 0 of the next query tile)
+#pragma unroll
+          for (int ch = 0; ch < kBN / 32; ++ch) {
+            const int64_t j = nxt * kBN + ch * 32 + lane;
+            pnext[ch] = j < a.np ? __ldg(a.pn + j) : __int_as_float(0x7fffffff);
+          }
+        }
         mbar_wait(&tfull[buf], tphase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + lane_addr + static_cast<uint32_t>(buf * kBN);
-        // point norms of this tile, staged in this warp's smem slice and read back as
-        // float4 broadcasts; points past np get NaN (never admitted, ignored by fminf)
-        __syncwarp();
 #pragma unroll
-        for (int ch = 0; ch < kBN / 32; ++ch) {
-          const int64_t j = pt * kBN + ch * 32 + lane;
-          pns[ch * 32 + lane] = j < a.np ? __ldg(a.pn + j) : __int_as_float(0x7fffffff);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int ch = 0; ch < kBN / 32; ++ch) {
-          uint32_t r[32];
+        for (int h = 0; h < kBN / 64; ++h) {
+          // two 32-column chunks per TMEM round trip
+          uint32_t rr[2][32];
           __syncwarp();  // tcgen05.ld is warp-collective; the admission loop diverges
-          tmem_ld32(tbase + ch * 32, r);
-          const int64_t j0 = pt * kBN + ch * 32;
-          if (a.debug_G) {
-            if (qt == 0)
-              for (int c = 0; c < 32; ++c)
-                a.debug_G[row * 256 + ch * 32 + c] =
-                    j0 + c < a.np ? nqf + fmaf(-2.0f, __uint_as_float(r[c]), pns[ch * 32 + c]) : 0.0f;
-            continue;
-          }
-          // v_c = D~ - n^_q; a chunk with nothing under the window (for any lane) is skipped
-          float m0 = INFINITY, m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;
+          tmem_ld32_nw(tbase + h * 64, rr[0]);
+          tmem_ld32_nw(tbase + h * 64 + 32, rr[1]);
+          tmem_wait_ld();
 #pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4) {
-            const float4 p4 = *reinterpret_cast<const float4*>(pns + ch * 32 + 4 * c4);
-            const float v0 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 0]), p4.x);
-            const float v1 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 1]), p4.y);
-            const float v2 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 2]), p4.z);
-            const float v3 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 3]), p4.w);
-            r[4 * c4 + 0] = __float_as_uint(v0);
-            r[4 * c4 + 1] = __float_as_uint(v1);
-            r[4 * c4 + 2] = __float_as_uint(v2);
-            r[4 * c4 + 3] = __float_as_uint(v3);
-            m0 = fminf(m0, v0);
-            m1 = fminf(m1, v1);
-            m2 = fminf(m2, v2);
-            m3 = fminf(m3, v3);
-          }
-          const float vmin = fminf(fminf(m0, m1), fminf(m2, m3));
-          if (!__any_sync(0xffffffffu, vmin <= win)) continue;
-          // hot chunk: per-lane bit mask of admissible columns; values parked in this
-          // lane's scratch row so the admission loop visits only the set bits
-          uint32_t mask = 0;
+          for (int u = 0; u < 2; ++u) {
+            const int ch = 2 * h + u;
+            uint32_t(&r)[32] = rr[u];
+            const int64_t j0 = pt * kBN + ch * 32;
+            if (a.debug_G) {
+              if (qt == 0)
+                for (int c = 0; c < 32; ++c)
+                  a.debug_G[row * 256 + ch * 32 + c] =
+                      j0 + c < a.np ? nqf + fmaf(-2.0f, __uint_as_float(r[c]), pns[ch * 32 + c]) : 0.0f;
+              continue;
+            }
+            // v_c = D~ - n^_q; a chunk with nothing under the window (for any lane) is skipped
+            float m0 = INFINITY, m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) mask |= (__uint_as_float(r[c]) <= win ? 1u : 0u) << c;
-          if (mask == 0) continue;
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const float4 p4 = *reinterpret_cast<const float4*>(pns + ch * 32 + 4 * c4);
+              const float v0 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 0]), p4.x);
+              const float v1 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 1]), p4.y);
+              const float v2 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 2]), p4.z);
+              const float v3 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 3]), p4.w);
+              r[4 * c4 + 0] = __float_as_uint(v0);
+              r[4 * c4 + 1] = __float_as_uint(v1);
+              r[4 * c4 + 2] = __float_as_uint(v2);
+              r[4 * c4 + 3] = __float_as_uint(v3);
+              m0 = fminf(m0, v0);
+              m1 = fminf(m1, v1);
+              m2 = fminf(m2, v2);
+              m3 = fminf(m3, v3);
+            }
+            const float vmin = fminf(fminf(m0, m1), fminf(m2, m3));
+            if (!__any_sync(0xffffffffu, vmin <= win)) continue;
+            // hot chunk: per-lane bit mask of admissible columns; values parked in this
+            // lane's scratch row so the admission loop visits only the set bits
+            uint32_t mask = 0;
 #pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4)
-            *reinterpret_cast<uint4*>(scr + 4 * c4) = make_uint4(r[4 * c4], r[4 * c4 + 1], r[4 * c4 + 2], r[4 * c4 + 3]);
-          while (mask != 0) {
-            const int c = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const float v = scr[c];
-            const int64_t j = j0 + c;
-            if (!(v <= win) || j == excl) continue;
-            if (hn < a.kk) {  // fill the heap (sift up)
-              int pos = hn++;
-              while (pos > 0) {
-                const int par = (pos - 1) >> 1;
-                const float pk = hk[par * kBM];
-                if (pk >= v) break;
-                hk[pos * kBM] = pk;
-                hi[pos * kBM] = hi[par * kBM];
-                pos = par;
+            for (int c = 0; c < 32; ++c) mask |= (__uint_as_float(r[c]) <= win ? 1u : 0u) << c;
+            if (mask == 0) continue;
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4)
+              *reinterpret_cast<uint4*>(scr + 4 * c4) = make_uint4(r[4 * c4], r[4 * c4 + 1], r[4 * c4 + 2], r[4 * c4 + 3]);
+            while (mask != 0) {
+              const int c = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const float v = scr[c];
+              const int64_t j = j0 + c;
+              if (!(v <= win) || j == excl) continue;
+              if (hn < a.kk) {  // fill the heap (sift up)
+                int pos = hn++;
+                while (pos > 0) {
+                  const int par = (pos - 1) >> 1;
+                  const float pk = hk[par * kBM];
+                  if (pk >= v) break;
+                  hk[pos * kBM] = pk;
+                  hi[pos * kBM] = hi[par * kBM];
+                  pos = par;
+                }
+                hk[pos * kBM] = v;
+                hi[pos * kBM] = static_cast<int32_t>(j);
+                if (hn == a.kk) {
+                  root = hk[0];
+                  win = window_of(root + nqf, eta, eps) - nqf;
+                }
+                continue;
               }
-              hk[pos * kBM] = v;
-              hi[pos * kBM] = static_cast<int32_t>(j);
-              if (hn == a.kk) {
+              float vk = v;  // the value that goes to the window buffer
+              int32_t vi = static_cast<int32_t>(j);
+              if (v < root) {  // replace the root, sift down; the old root moves to the buffer
+                vk = root;
+                vi = hi[0];
+                int pos = 0;
+                for (;;) {
+                  const int l = 2 * pos + 1;
+                  if (l >= a.kk) break;
+                  int ch2 = l;
+                  float ck = hk[l * kBM];
+                  if (l + 1 < a.kk) {
+                    const float rk = hk[(l + 1) * kBM];
+                    if (rk > ck) {
+                      ck = rk;
+                      ch2 = l + 1;
+                    }
+                  }
+                  if (ck <= v) break;
+                  hk[pos * kBM] = ck;
+                  hi[pos * kBM] = hi[ch2 * kBM];
+                  pos = ch2;
+                }
+                hk[pos * kBM] = v;
+                hi[pos * kBM] = static_cast<int32_t>(j);
                 root = hk[0];
                 win = window_of(root + nqf, eta, eps) - nqf;
               }
-              continue;
-            }
-            float vk = v;  // the value that goes to the window buffer
-            int32_t vi = static_cast<int32_t>(j);
-            if (v < root) {  // replace the root, sift down; the old root moves to the buffer
-              vk = root;
-              vi = hi[0];
-              int pos = 0;
-              for (;;) {
-                const int l = 2 * pos + 1;
-                if (l >= a.kk) break;
-                int ch2 = l;
-                float ck = hk[l * kBM];
-                if (l + 1 < a.kk) {
-                  const float rk = hk[(l + 1) * kBM];
-                  if (rk > ck) {
-                    ck = rk;
-                    ch2 = l + 1;
+              if (vk <= win) {
+                if (wn == wcap) {  // compact: drop entries that left the window
+                  int o = 0;
+                  for (int t = 0; t < wn; ++t) {
+                    const float tk = wk[t * kBM];
+                    if (tk <= win) {
+                      wk[o * kBM] = tk;
+                      wi_[o * kBM] = wi_[t * kBM];
+                      ++o;
+                    }
                   }
+                  wn = o;
                 }
-                if (ck <= v) break;
-                hk[pos * kBM] = ck;
-                hi[pos * kBM] = hi[ch2 * kBM];
-                pos = ch2;
-              }
-              hk[pos * kBM] = v;
-              hi[pos * kBM] = static_cast<int32_t>(j);
-              root = hk[0];
-              win = window_of(root + nqf, eta, eps) - nqf;
-            }
-            if (vk <= win) {
-              if (wn == wcap) {  // compact: drop entries that left the window
-                int o = 0;
-                for (int t = 0; t < wn; ++t) {
-                  const float tk = wk[t * kBM];
-                  if (tk <= win) {
-                    wk[o * kBM] = tk;
-                    wi_[o * kBM] = wi_[t * kBM];
-                    ++o;
-                  }
+                if (wn == wcap) {
+                  over = true;  // the query is redone exactly
+                  win = -INFINITY;
+                  continue;
                 }
-                wn = o;
+                wk[wn * kBM] = vk;
+                wi_[wn * kBM] = vi;
+                ++wn;
               }
-              if (wn == wcap) {
-                over = true;  // the query is redone exactly
-                win = -INFINITY;
-                continue;
-              }
-              wk[wn * kBM] = vk;
-              wi_[wn * kBM] = vi;
-              ++wn;
             }
           }
         }
@@ -479,52 +518,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           tphase ^= 1;
         }
       }
-      // candidates = heap u buffer (the exact top-kk is inside)
-      int cnt = hn;
-      for (int t = 0; t < wn; ++t) {
-        mk[cnt * kBM] = wk[t * kBM];
-        mi[cnt * kBM] = wi_[t * kBM];
-        ++cnt;
-      }
+      // candidates = heap u buffer (the exact top-kk is inside); the exact
+      // recheck and selection run in tc_recheck_kernel
       if (!valid || a.debug_G) continue;
       if (over) {
         const int32_t slot = atomicAdd(a.overflow, 1);
         a.overflow[1 + slot] = static_cast<int32_t>(q);
+        a.ccount[q] = -1;
         continue;
       }
-      // exact recheck of the window and selection of the top-kk by (key, index)
-      double* wd = a.wd + q * a.kk;
-      int32_t* wi = a.wi + q * a.kk;
-      const double* qx = a.Q + q * a.d;
-      int m = 0;
-      double thr = INFINITY;
-      int32_t thr_i = INT_MAX;
-      for (int t = 0; t < cnt; ++t) {
-        const int32_t j = mi[t * kBM];
-        const double key = dist_sq_dyn(qx, a.P + static_cast<int64_t>(j) * a.d, a.d);
-        if (m == a.kk && !pair_less(key, j, thr, thr_i)) continue;
-        int pos = m < a.kk ? m : a.kk - 1;
-        while (pos > 0 && pair_less(key, j, wd[pos - 1], wi[pos - 1])) {
-          wd[pos] = wd[pos - 1];
-          wi[pos] = wi[pos - 1];
-          --pos;
-        }
-        wd[pos] = key;
-        wi[pos] = j;
-        if (m < a.kk) ++m;
-        if (m == a.kk) {
-          thr = wd[a.kk - 1];
-          thr_i = wi[a.kk - 1];
-        }
-      }
-      const int width = a.kk + (a.with_self ? 1 : 0);
-      int32_t* orow = a.out + q * width;
-      int o = 0;
-      if (a.with_self) orow[o++] = static_cast<int32_t>(q + a.self_offset);
-      for (int t = 0; t < a.kk; ++t) {
-        orow[o + t] = t < m ? wi[t] : INT_MAX;
-        if (a.out_d) a.out_d[q * a.kk + t] = t < m ? wd[t] : INFINITY;
-      }
+      for (int t = 0; t < hn; ++t) a.cand[t * a.nq + q] = hi[t * kBM];
+      for (int t = 0; t < wn; ++t) a.cand[(hn + t) * a.nq + q] = wi_[t * kBM];
+      a.ccount[q] = hn + wn;
     }
   }
   tc_fence_before();
@@ -532,6 +537,64 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kBN));
+  }
+}
+
+// Exact recheck, one warp per query: fp64 keys of the (<= cap <= 128)
+// candidates with the reference's sequential difference order, then each
+// candidate's rank under (key, index) by broadcasting all candidates through
+// the warp; rank < kk goes straight to its output slot.
+__global__ void __launch_bounds__(256) tc_recheck_kernel(const double* __restrict__ Q, const double* __restrict__ P,
+                                                          int d, int64_t nq, int kk, const int32_t* __restrict__ cand,
+                                                          const int32_t* __restrict__ ccount, int with_self,
+                                                          int64_t self_offset, int32_t* __restrict__ out,
+                                                          double* __restrict__ out_d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t q = w0; q < nq; q += nw) {
+    const int cnt = ccount[q];
+    if (cnt < 0) continue;  // overflowed: redone by the brute-force path
+    const double* qx = Q + q * d;
+    double key[4];
+    int32_t idx[4];
+    int rank[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int t = s * 32 + lane;
+      rank[s] = 0;
+      if (t < cnt) {
+        idx[s] = cand[static_cast<int64_t>(t) * nq + q];
+        key[s] = dist_sq_dyn(qx, P + static_cast<int64_t>(idx[s]) * d, d);
+      } else {
+        idx[s] = INT_MAX;
+        key[s] = INFINITY;
+      }
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < 4; ++s2) {
+      if (s2 * 32 >= cnt) break;
+      for (int l = 0; l < 32; ++l) {
+        const double ku = __shfl_sync(0xffffffffu, key[s2], l);
+        const int32_t iu = __shfl_sync(0xffffffffu, idx[s2], l);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) rank[s] += pair_less(ku, iu, key[s], idx[s]) ? 1 : 0;
+      }
+    }
+    const int width = kk + (with_self ? 1 : 0);
+    int32_t* orow = out + q * width + (with_self ? 1 : 0);
+    if (with_self && lane == 0) out[q * width] = static_cast<int32_t>(q + self_offset);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (s * 32 + lane < cnt && rank[s] < kk) {
+        orow[rank[s]] = idx[s];
+        if (out_d) out_d[q * kk + rank[s]] = key[s];
+      }
+    }
+    for (int t = cnt + lane; t < kk; t += 32) {  // fewer candidates than kk (np < kk)
+      orow[t] = INT_MAX;
+      if (out_d) out_d[q * kk + t] = INFINITY;
+    }
   }
 }
 
@@ -601,8 +664,8 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   const int cap = std::min(kCapMax, ((kk + 29 + 3) / 4) * 4);
   __half *Qh = nullptr, *Ph = nullptr;
   float *qn = nullptr, *pn = nullptr;
-  double *sums = nullptr, *wd = nullptr;
-  int32_t *wi = nullptr, *ovf = nullptr;
+  double* sums = nullptr;
+  int32_t *cand = nullptr, *ccount = nullptr, *ovf = nullptr;
   unsigned long long* bits = nullptr;  // [0] maxabs, [1] pmax
   cudaError_t err = cudaMallocAsync(&Qh, sizeof(__half) * nq * DP, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&Ph, sizeof(__half) * np * DP, s);
@@ -610,8 +673,8 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   if (err == cudaSuccess) err = cudaMallocAsync(&pn, sizeof(float) * np, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&sums, sizeof(double) * d, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&bits, sizeof(unsigned long long) * 2, s);
-  if (err == cudaSuccess) err = cudaMallocAsync(&wd, sizeof(double) * nq * kk, s);
-  if (err == cudaSuccess) err = cudaMallocAsync(&wi, sizeof(int32_t) * nq * kk, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&cand, sizeof(int32_t) * nq * cap, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&ccount, sizeof(int32_t) * nq, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&ovf, sizeof(int32_t) * (nq + 1), s);
   if (err != cudaSuccess) return err;
   cudaMemsetAsync(sums, 0, sizeof(double) * d, s);
@@ -643,8 +706,8 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.with_self = with_self;
   a.out = out;
   a.out_d = out_d;
-  a.wd = wd;
-  a.wi = wi;
+  a.cand = cand;
+  a.ccount = ccount;
   a.overflow = ovf;
   a.maxabs_bits = bits;
   a.pmax_bits = bits + 1;
@@ -659,10 +722,20 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   note_launches(1);
   err = cudaGetLastError();
   if (err == cudaSuccess && debug_G == nullptr) {
+    const int64_t blocks = (nq + 7) / 8;
+    tc_recheck_kernel<<<static_cast<unsigned>(blocks < num_sms * 8 ? blocks : num_sms * 8), 256, 0, s>>>(
+        Q, P, d, nq, kk, cand, ccount, with_self, self_offset, out, out_d);
+    note_launches(1);
+    err = cudaGetLastError();
+  }
+  if (err == cudaSuccess && debug_G == nullptr) {
     // exact fallback for the (rare) queries whose candidate window overflowed
     int32_t novf = 0;
     err = cudaMemcpyAsync(&novf, ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+    if (err == cudaSuccess && std::getenv("FMGP_TC_STATS") != nullptr)
+      std::fprintf(stderr, "knn_tc: nq=%lld np=%lld kk=%d cap=%d overflowed=%d\n", static_cast<long long>(nq),
+                   static_cast<long long>(np), kk, cap, novf);
     if (err == cudaSuccess && novf > 0) {
       double *Qg = nullptr, *rd = nullptr;
       int32_t *eg = nullptr, *rows = nullptr;
@@ -683,7 +756,7 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
     }
   }
   for (void* p : {static_cast<void*>(Qh), static_cast<void*>(Ph), static_cast<void*>(qn), static_cast<void*>(pn),
-                  static_cast<void*>(sums), static_cast<void*>(bits), static_cast<void*>(wd), static_cast<void*>(wi),
+                  static_cast<void*>(sums), static_cast<void*>(bits), static_cast<void*>(cand), static_cast<void*>(ccount),
                   static_cast<void*>(ovf)})
     cudaFreeAsync(p, s);
   return err;

@@ -375,7 +375,7 @@ cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const in
                         int64_t row_begin, int k, const KParams& kp, double* C, int32_t* status,
                         unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
   if (nrows <= 0) return cudaSuccess;
-  // FMGP_SOLVE = reg (default where the shape is compiled in) | tc | scalar, for A/B checks.
+  // FMGP_SOLVE = reg/cta (default where the shape is compiled in) | tc | scalar, for A/B checks.
   static const int mode = [] {
     const char* e = std::getenv("FMGP_SOLVE");
     if (e == nullptr) return 0;
@@ -384,6 +384,8 @@ cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const in
   }();
   if (mode == 0 && status == nullptr && fused_solve_reg_supported(k, d, m))
     return fused_solve_reg(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
+  if (mode == 0 && status == nullptr && fused_solve_cta_supported(k, d, m))
+    return fused_solve_cta(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
   if (mode == 1 && status == nullptr && fused_solve_tc_supported(k, d, m))
     return fused_solve_tc(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
   const size_t bytes = per_warp_doubles(k, dchunk_for(k, d), m) * sizeof(double);

@@ -1,0 +1,245 @@
+// K2-cta — the fused neighbourhood solve for large compile-time k (cfg4:
+// k = 100), one thread block per neighbourhood. Same contract as solve.cu
+// (fast_predict.cpp:98-106 gather, kernel.cpp:106-119 nugget-regularised
+// matrix, linalg.cpp:10-36 jitter-ladder LLT + solve).
+//
+// Why: the warp-per-neighbourhood kernels keep a whole k x k triangle per
+// warp; at k = 100 that is ~46 KB of shared memory per warp (4 warps per SM,
+// latency-bound). Here the CTA's R = K + M threads own one row each of the
+// augmented matrix [K ; Y^T] in registers:
+//  * build: all K neighbour coordinates are staged once in shared memory
+//    (padded rows), the strict lower triangle is spread over the CTA through a
+//    pair table, entries land in a packed row-major triangle;
+//  * factor: left-looking column sweep. For column j every row r > j forms
+//    s_r = a_rj - sum_{p<j} a_rp L_jp from its registers and the pivot row
+//    L_j. (a shared-memory 128-bit broadcast); the rows also keep a running
+//    diagonal d_r = a_rr - sum_p L_rp^2, so the owner of row j+1 has its pivot
+//    as soon as it has L_{j+1,j}: one barrier per column. The RHS rows ride
+//    along (forward substitution);
+//  * backward solve: warp 0, x in registers, x_j broadcast by shuffle.
+#include "fmgp_common.cuh"
+#include "fmgp_internal.h"
+
+namespace fmgp {
+
+namespace {
+
+__constant__ double kJitC[4] = {0.0, 1e-10, 1e-8, 1e-6};
+
+__host__ __device__ constexpr int ro_c(int i) { return ((i * (i + 1)) >> 1) + ((i + 1) >> 1); }  // 16 B aligned rows
+
+template <int K, int M>
+struct CtaShape {
+  static constexpr int kRows = K + M;
+  static constexpr int kThreads = ((kRows + 31) / 32) * 32;
+  static constexpr int kTri = ro_c(K);                        // packed triangle (doubles)
+  static constexpr int kPairs = K * (K - 1) / 2;
+  static constexpr int kXsD = 48;                             // coordinate slice staged per pass
+  static constexpr int kXsStride = kXsD + 1;                  // odd stride: spread banks
+  static constexpr int kXs = ((K * kXsStride + 1) / 2) * 2;
+  // doubles: tri | xs | invd[K] | zbuf[M*K] | misc[2]; then uint32 pairs, int32 sr
+  static constexpr int kDoubles = kTri + kXs + ((K + 1) & ~1) + ((M * K + 1) & ~1) + 2;
+  static constexpr size_t kBytes = sizeof(double) * kDoubles + sizeof(uint32_t) * kPairs + sizeof(int32_t) * K;
+};
+
+__device__ __forceinline__ double jitter_c(double v, int a) {
+  for (int t = 1; t <= a; ++t) v = __dadd_rn(v, __dsub_rn(kJitC[t], kJitC[t - 1]));
+  return v;
+}
+
+template <int K, int M>
+__global__ void __launch_bounds__(CtaShape<K, M>::kThreads, 1)
+solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
+                 int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
+                 unsigned long long* __restrict__ fail_min) {
+  using Sh = CtaShape<K, M>;
+  extern __shared__ double smem[];
+  double* tri = smem;
+  double* xs = tri + Sh::kTri;
+  double* invd = xs + Sh::kXs;
+  double* zbuf = invd + ((K + 1) & ~1);
+  double* misc = zbuf + ((M * K + 1) & ~1);  // [0] = failure flag
+  uint32_t* ptab = reinterpret_cast<uint32_t*>(misc + 2);
+  int32_t* sr = reinterpret_cast<int32_t*>(ptab + Sh::kPairs);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+
+  for (int e = tid; e < Sh::kPairs; e += Sh::kThreads) {
+    int i = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(e))) * 0.5f);
+    while ((i * (i - 1)) / 2 > e) --i;
+    while ((i * (i + 1)) / 2 <= e) ++i;
+    const int p = e - (i * (i - 1)) / 2;
+    ptab[e] = (static_cast<uint32_t>(ro_c(i) + p) << 16) | (static_cast<uint32_t>(i) << 8) | static_cast<uint32_t>(p);
+  }
+
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    __syncthreads();  // previous neighbourhood fully consumed
+    for (int t = tid; t < K; t += Sh::kThreads) sr[t] = S[r * K + t];
+    __syncthreads();
+    bool ok = false;
+    for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
+      // ---- build K(S_r) into the packed triangle (sequential-in-t distance)
+      for (int c0 = 0; c0 < d; c0 += Sh::kXsD) {
+        const int dc = min(Sh::kXsD, d - c0);
+        for (int e = tid; e < K * dc; e += Sh::kThreads) {
+          const int t = e / dc, c = e - t * dc;
+          xs[t * Sh::kXsStride + c] = X[static_cast<int64_t>(sr[t]) * d + c0 + c];
+        }
+        __syncthreads();
+        const bool last = c0 + dc >= d;
+        for (int e = tid; e < Sh::kPairs; e += Sh::kThreads) {
+          const uint32_t pt = ptab[e];
+          const double* xa = xs + ((pt >> 8) & 0xffu) * Sh::kXsStride;
+          const double* xb = xs + (pt & 0xffu) * Sh::kXsStride;
+          double acc = c0 == 0 ? 0.0 : tri[pt >> 16];
+          for (int c = 0; c < dc; ++c) {
+            const double dd = __dsub_rn(xa[c], xb[c]);
+            acc = __dadd_rn(acc, __dmul_rn(dd, dd));
+          }
+          tri[pt >> 16] = last ? kernel_eval_fast(sqrt(acc), kp) : acc;
+        }
+        __syncthreads();
+      }
+      const double dg = jitter_c(kp.diag, attempt);
+      // ---- load the owned row into registers
+      double a[K];
+      double dacc = 0.0;
+      if (tid < K) {
+        const double* row = tri + ro_c(tid);
+#pragma unroll
+        for (int p = 0; p < K; ++p) a[p] = p < tid ? row[p] : (p == tid ? dg : 0.0);
+        dacc = dg;
+      } else if (tid < Sh::kRows) {
+        const int c = tid - K;
+#pragma unroll
+        for (int p = 0; p < K; ++p) a[p] = Y[static_cast<int64_t>(sr[p]) * M + c];
+      } else {
+#pragma unroll
+        for (int p = 0; p < K; ++p) a[p] = 0.0;
+      }
+      if (tid == 0) {
+        misc[0] = 0.0;
+        if (!(dg > 0.0)) {
+          misc[0] = 1.0;
+        } else {
+          const double l00 = sqrt(dg);
+          invd[0] = 1.0 / l00;
+          tri[0] = l00;
+          a[0] = l00;
+        }
+      }
+      __syncthreads();  // row reads of the triangle done; pivot 0 published
+      if (misc[0] != 0.0) continue;
+      // ---- left-looking sweep, one barrier per column (a failed pivot only sets
+      // the flag: the rest of the sweep runs on garbage and is discarded)
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (32 * warp + 31 > j) {  // warp has rows > j (uniform branch)
+          const double* Lj = tri + ro_c(j);
+          double s0 = a[j], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int p = 0; p + 3 < j; p += 4) {
+            const double2 l0 = *reinterpret_cast<const double2*>(Lj + p);
+            const double2 l1 = *reinterpret_cast<const double2*>(Lj + p + 2);
+            s0 = fma(-a[p], l0.x, s0);
+            s1 = fma(-a[p + 1], l0.y, s1);
+            s2 = fma(-a[p + 2], l1.x, s2);
+            s3 = fma(-a[p + 3], l1.y, s3);
+          }
+#pragma unroll
+          for (int p = j & ~3; p < j; ++p) s0 = fma(-a[p], Lj[p], s0);
+          const double s = (s0 + s1) + (s2 + s3);
+          if (tid > j && tid < Sh::kRows) {
+            const double l = s * invd[j];
+            a[j] = l;
+            if (tid < K) {
+              tri[ro_c(tid) + j] = l;
+              dacc = fma(-l, l, dacc);
+              if (j + 1 < K && tid == j + 1) {  // next pivot is complete
+                if (!(dacc > 0.0)) {
+                  misc[0] = 1.0;
+                } else {
+                  const double ljj = sqrt(dacc);
+                  invd[j + 1] = 1.0 / ljj;
+                  tri[ro_c(tid) + tid] = ljj;
+                  a[j + 1] = ljj;
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      ok = misc[0] == 0.0;
+      if (ok && tid >= K && tid < Sh::kRows) {
+        const int c = tid - K;
+#pragma unroll
+        for (int p = 0; p < K; ++p) zbuf[c * K + p] = a[p];
+      }
+      __syncthreads();
+    }
+    if (!ok) {
+      if (tid == 0) atomicMin(fail_min, static_cast<unsigned long long>(row_begin + r));
+      continue;
+    }
+    // ---- backward solve L^T x = z (warp 0; x_j broadcast by shuffle)
+    if (warp == 0) {
+      constexpr int kS = (K + 31) / 32;
+      for (int c = 0; c < M; ++c) {
+        double y[kS];
+#pragma unroll
+        for (int s = 0; s < kS; ++s) y[s] = s * 32 + lane < K ? zbuf[c * K + s * 32 + lane] : 0.0;
+#pragma unroll
+        for (int j = K - 1; j >= 0; --j) {
+          const double xj = __shfl_sync(0xffffffffu, y[j >> 5], j & 31) * invd[j];
+          const double* Lj = tri + ro_c(j);
+          if (lane == (j & 31)) y[j >> 5] = xj;
+#pragma unroll
+          for (int s = 0; s <= (j >> 5); ++s) {
+            if (s * 32 + lane < j) y[s] = fma(-Lj[s * 32 + lane], xj, y[s]);
+          }
+        }
+        double* Crow = C + r * K * M;
+#pragma unroll
+        for (int s = 0; s < kS; ++s)
+          if (s * 32 + lane < K) Crow[(s * 32 + lane) * M + c] = y[s];
+      }
+    }
+  }
+}
+
+template <int K, int M>
+cudaError_t launch_cta(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows, int64_t row_begin,
+                       const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
+  using Sh = CtaShape<K, M>;
+  cudaError_t err = cudaFuncSetAttribute(solve_cta_kernel<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Sh::kBytes));
+  if (err != cudaSuccess) return err;
+  int per_sm = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_cta_kernel<K, M>, Sh::kThreads, Sh::kBytes);
+  if (err != cudaSuccess) return err;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t grid = std::min<int64_t>(nrows, static_cast<int64_t>(num_sms) * per_sm);
+  solve_cta_kernel<K, M><<<static_cast<unsigned>(grid), Sh::kThreads, Sh::kBytes, stream>>>(X, Y, d, S, nrows,
+                                                                                            row_begin, kp, C, fail_min);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool fused_solve_cta_supported(int k, int d, int m) {
+  (void)d;
+  return k == 100 && m == 1;
+}
+
+cudaError_t fused_solve_cta(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
+                            int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
+                            int num_sms, cudaStream_t stream) {
+  if (nrows <= 0) return cudaSuccess;
+  if (k == 100 && m == 1) return launch_cta<100, 1>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fmgp

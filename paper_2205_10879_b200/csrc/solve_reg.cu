@@ -38,11 +38,60 @@ struct RegShape {
   static constexpr int kDch = 16;                      // coordinate slice width staged per pass
   static constexpr int kCol = (K + 2) & ~1;            // colbuf (even: 16-byte aligned pairs)
   static constexpr int kPerWarp = ((kAug + ((K + 1) & ~1) /*dinv*/ + kCol + kDch * K /*xs*/ + (K + 1) / 2 + 2) + 1) & ~1;
+  static constexpr int kTabDoubles = ((K * (K - 1) / 2 + 3) / 4) * 2;  // pair table (uint32), 16 B granules
   __host__ __device__ static constexpr int row_off(int i) { return i < K ? ro_r(i) : ro_r(K) + (i - K) * kRw; }
 };
 
 // Build [K(S_i) ; Y^T] in the packed shared-memory layout (pairs spread over
 // lanes, incremental decode), diagonal at jitter rung `attempt`.
+// Pair table shared by the CTA's warps: entry e of the strict lower triangle
+// (row-major order) = (packed offset << 16) | (row << 8) | col.
+template <int K>
+__device__ void fill_pair_table(uint32_t* ptab) {
+  constexpr int npairs = (K * (K - 1)) / 2;
+  for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
+    int i = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(e))) * 0.5f);
+    while ((i * (i - 1)) / 2 > e) --i;
+    while ((i * (i + 1)) / 2 <= e) ++i;
+    const int p = e - (i * (i - 1)) / 2;
+    ptab[e] = (static_cast<uint32_t>(ro_r(i) + p) << 16) | (static_cast<uint32_t>(i) << 8) | static_cast<uint32_t>(p);
+  }
+}
+
+// Small-d build (d = D known at compile time): all K coordinates staged once,
+// one pair per lane per step from the pair table, no index decode.
+template <int K, int M, int D>
+__device__ void build_small(const double* __restrict__ X, const double* __restrict__ Y, const int32_t* sr,
+                            const KParams& kp, int attempt, double* A, double* xs, const uint32_t* ptab, int lane) {
+  using Sh = RegShape<K, M>;
+  constexpr int npairs = (K * (K - 1)) / 2;
+  for (int e = lane; e < K * D; e += kWarp) {
+    const int t = e / D, c = e - t * D;
+    xs[e] = X[static_cast<int64_t>(sr[t]) * D + c];
+  }
+  __syncwarp();
+#pragma unroll 2
+  for (int e = lane; e < npairs; e += kWarp) {
+    const uint32_t t = ptab[e];
+    const double* xa = xs + ((t >> 8) & 0xffu) * D;
+    const double* xb = xs + (t & 0xffu) * D;
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double dd = __dsub_rn(xa[c], xb[c]);
+      acc = __dadd_rn(acc, __dmul_rn(dd, dd));
+    }
+    A[t >> 16] = kernel_eval_fast(sqrt(acc), kp);
+  }
+  const double dg = jitter_r(kp.diag, attempt);
+  for (int i = lane; i < K; i += kWarp) A[ro_r(i) + i] = dg;
+  for (int e = lane; e < K * M; e += kWarp) {
+    const int t = e / M, c = e - t * M;
+    A[Sh::row_off(K + c) + t] = Y[static_cast<int64_t>(sr[t]) * M + c];
+  }
+  __syncwarp();
+}
+
 template <int K, int M>
 __device__ void build_reg(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* sr,
                           const KParams& kp, int attempt, double* A, double* xs, int lane) {
@@ -190,23 +239,39 @@ __device__ bool factor_reg(double* A, double* dinv, double* colbuf, int lane) {
   return true;
 }
 
+// Backward solve L^T x = z, z = the forward-substituted RHS rows. Lane l keeps
+// x_l and x_{l+32} in registers; column j (descending) broadcasts x_j by a
+// shuffle and every lane updates its entries with row j of L (a contiguous
+// shared-memory row, conflict-free). Writes C directly (coalesced for M = 1).
 template <int K, int M>
-__device__ void back_solve_reg(double* A, const double* dinv, int lane) {
+__device__ void back_solve_reg(const double* A, const double* dinv, double* __restrict__ Crow, int lane) {
   using Sh = RegShape<K, M>;
+  static_assert(K <= 64, "two register slots per lane");
+#pragma unroll 1
   for (int c = 0; c < M; ++c) {
-    double* y = A + Sh::row_off(K + c);
+    const double* z = A + Sh::row_off(K + c);
+    double y0 = lane < K ? z[lane] : 0.0;
+    double y1 = lane + 32 < K ? z[lane + 32] : 0.0;
+#pragma unroll
     for (int j = K - 1; j >= 0; --j) {
+      const double yj = __shfl_sync(0xffffffffu, j < 32 ? y0 : y1, j & 31);
+      const double xj = yj * dinv[j];
       const double* Lj = A + ro_r(j);
-      const double xj = y[j] * dinv[j];
-      __syncwarp();
-      for (int i = lane; i < j; i += kWarp) y[i] = fma(-Lj[i], xj, y[i]);
-      if (lane == 0) y[j] = xj;
-      __syncwarp();
+      if (j < 32) {
+        if (lane == j) y0 = xj;
+        if (lane < j) y0 = fma(-Lj[lane], xj, y0);
+      } else {
+        if (lane == j - 32) y1 = xj;
+        if (lane < 32) y0 = fma(-Lj[lane], xj, y0);
+        if (lane + 32 < j) y1 = fma(-Lj[lane + 32], xj, y1);
+      }
     }
+    if (lane < K) Crow[lane * M + c] = y0;
+    if (lane + 32 < K) Crow[(lane + 32) * M + c] = y1;
   }
 }
 
-template <int K, int M>
+template <int K, int M, int D>
 __global__ void __launch_bounds__(64)
 solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
                  int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
@@ -216,7 +281,12 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
   const int lane = threadIdx.x % kWarp;
   const int warp = threadIdx.x / kWarp;
   const int warps = blockDim.x / kWarp;
-  double* A = smem + warp * Sh::kPerWarp;
+  uint32_t* ptab = reinterpret_cast<uint32_t*>(smem);
+  if constexpr (D > 0) {
+    fill_pair_table<K>(ptab);
+    __syncthreads();
+  }
+  double* A = smem + (D > 0 ? Sh::kTabDoubles : 0) + warp * Sh::kPerWarp;
   double* dinv = A + Sh::kAug;
   double* colbuf = dinv + ((K + 1) & ~1);
   double* xs = colbuf + Sh::kCol;
@@ -227,7 +297,10 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
     __syncwarp();
     bool ok = false;
     for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
-      build_reg<K, M>(X, Y, d, sr, kp, attempt, A, xs, lane);
+      if constexpr (D > 0)
+        build_small<K, M, D>(X, Y, sr, kp, attempt, A, xs, ptab, lane);
+      else
+        build_reg<K, M>(X, Y, d, sr, kp, attempt, A, xs, lane);
       ok = factor_reg<K, M>(A, dinv, colbuf, lane);
       __syncwarp();
     }
@@ -236,31 +309,27 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
       __syncwarp();
       continue;
     }
-    back_solve_reg<K, M>(A, dinv, lane);
-    for (int e = lane; e < K * M; e += kWarp) {
-      const int t = e / M, c = e - t * M;
-      C[r * K * M + e] = A[Sh::row_off(K + c) + t];
-    }
+    back_solve_reg<K, M>(A, dinv, C + r * K * M, lane);
     __syncwarp();
   }
 }
 
-template <int K, int M>
+template <int K, int M, int D>
 cudaError_t launch_reg(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows, int64_t row_begin,
                        const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
   using Sh = RegShape<K, M>;
   constexpr int kWarps = 2;
-  const size_t smem = sizeof(double) * Sh::kPerWarp * kWarps;
-  cudaError_t err = cudaFuncSetAttribute(solve_reg_kernel<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = sizeof(double) * ((D > 0 ? Sh::kTabDoubles : 0) + Sh::kPerWarp * kWarps);
+  cudaError_t err = cudaFuncSetAttribute(solve_reg_kernel<K, M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   int per_sm = 0;
-  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_reg_kernel<K, M>, kWarps * kWarp, smem);
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_reg_kernel<K, M, D>, kWarps * kWarp, smem);
   if (err != cudaSuccess) return err;
   if (per_sm < 1) per_sm = 1;
   const int64_t need = (nrows + kWarps - 1) / kWarps;
   const int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(num_sms) * per_sm);
-  solve_reg_kernel<K, M><<<static_cast<unsigned>(grid), kWarps * kWarp, smem, stream>>>(X, Y, d, S, nrows, row_begin,
+  solve_reg_kernel<K, M, D><<<static_cast<unsigned>(grid), kWarps * kWarp, smem, stream>>>(X, Y, d, S, nrows, row_begin,
                                                                                         kp, C, fail_min);
   note_launches(1);
   return cudaGetLastError();
@@ -277,9 +346,20 @@ cudaError_t fused_solve_reg(const double* X, const double* Y, int d, int m, cons
                             int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
                             int num_sms, cudaStream_t stream) {
   if (nrows <= 0) return cudaSuccess;
-  if (k == 50 && m == 1) return launch_reg<50, 1>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
-  if (k == 30 && m == 1) return launch_reg<30, 1>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
-  if (k == 30 && m == 10) return launch_reg<30, 10>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+#define FMGP_REG_CASE(KK, MM, DD) \
+  return launch_reg<KK, MM, DD>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream)
+  if (k == 50 && m == 1) {
+    if (d == 2) FMGP_REG_CASE(50, 1, 2);
+    if (d == 3) FMGP_REG_CASE(50, 1, 3);
+    FMGP_REG_CASE(50, 1, 0);
+  }
+  if (k == 30 && m == 1) {
+    if (d == 2) FMGP_REG_CASE(30, 1, 2);
+    if (d == 3) FMGP_REG_CASE(30, 1, 3);
+    FMGP_REG_CASE(30, 1, 0);
+  }
+  if (k == 30 && m == 10) FMGP_REG_CASE(30, 10, 0);
+#undef FMGP_REG_CASE
   return cudaErrorInvalidValue;
 }
 

@@ -159,21 +159,24 @@ def test_linear_in_y_and_sigma_invariant(fm):
     assert np.abs(s - a).max() <= 1e-10
 
 
-def test_numeric_error_names_lowest_failing_row(fm, port):
+@pytest.mark.parametrize("k,d", [(8, 2), (30, 2), (50, 2), (50, 3), (100, 2), (100, 40)])
+def test_numeric_error_names_lowest_failing_row(fm, port, k, d):
     # Exact duplicates with tau = 0 give an exactly singular block; with sigma = 1e6
     # the jitter rungs (<= 1e-6) are below one ulp of the diagonal, so the ladder
     # is exhausted -> NumericError naming the lowest failing row (linalg.cpp:28-30,
-    # fast_predict.cpp:105; threads = 1 semantics).
+    # fast_predict.cpp:105; threads = 1 semantics). k = 30/50 run the register
+    # solve, k = 100 the CTA solve, k = 8 the scalar one.
     from oracle.oracle import OracleError
-    X = np.zeros((40, 2))
-    X[:, 0] = np.arange(40) * 10.0
-    X[21] = X[20]
-    Y = np.arange(40, dtype=np.float64)
+    n = 2 * k + 40
+    X = np.zeros((n, d))
+    X[:, 0] = np.arange(n) * 10.0
+    X[k + 21] = X[k + 20]
+    Y = np.arange(n, dtype=np.float64)
     p = fm.KernelParams(1e6, 1.0, 2.5, 0.0)
     with pytest.raises(OracleError) as eo:
-        port.precompute_rows(X, Y, 1, 1e6, 1.0, 2.5, 0.0, 8)
+        port.precompute_rows(X, Y, 1, 1e6, 1.0, 2.5, 0.0, k)
     with pytest.raises(fm.NumericError) as ei:
-        fm.precompute(fm.TrainingSet(X, Y, 0.0), fm.FittedParams(p, fm.KernelKind.RBF), fm.NeighborIndex.build(X), 8)
+        fm.precompute(fm.TrainingSet(X, Y, 0.0), fm.FittedParams(p, fm.KernelKind.RBF), fm.NeighborIndex.build(X), k)
     assert ei.value.failed_row == eo.value.failed_row
     assert str(ei.value) == (f"Cholesky factorization failed in precompute row {eo.value.failed_row} "
                              "after jitter escalation up to 1e-6")
