@@ -50,7 +50,9 @@ namespace {
 constexpr int kBM = 128;  // queries per tile (TMEM lanes)
 constexpr int kBN = 128;  // reference points per tile (TMEM columns per buffer)
 constexpr int kBK = 64;   // fp16 dims per k-block (one 128 B swizzle row)
-constexpr int kStages = 2;
+constexpr int kStages = 2;       // A+B stages when the query tile streams (KB > 1)
+constexpr int kBStagesRes = 3;   // B-only stages when the query tile is resident (KB == 1)
+constexpr int kTBufs = 4;        // TMEM accumulator buffers (4 x 128 columns)
 constexpr int kCapMax = 128;  // candidate-list capacity per query (kk <= kCapMax - 29)
 constexpr int kThreads = 192;
 constexpr int kScrStride = 36;  // floats per lane scratch row (16 B aligned, spreads banks)
@@ -82,21 +84,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-// Back-off variant for the producer-side roles (TMA, MMA): when the epilogue
-// is the bottleneck their spin would otherwise take its issue slots.
+// Producer-side roles (TMA, MMA) wait with a suspend-time hint: the thread
+// sleeps in the barrier unit until the phase completes instead of spinning
+// on the issue slots the epilogue warps need.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
-  for (;;) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok)
-        : "r"(su32(bar)), "r"(phase)
-        : "memory");
-    if (ok) return;
-    __nanosleep(128);
-  }
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONES_%=;\n\t"
+      "bra WAITS_%=;\n\t"
+      "DONES_%=:\n\t}" ::"r"(su32(bar)),
+      "r"(phase), "r"(1000000u)
+      : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -230,17 +230,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmP, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                                 // kStages x 16 KB
-  uint8_t* sB = smem + kStages * kABytes;             // kStages x 16 KB
-  float* lk = reinterpret_cast<float*>(sB + kStages * kBBytes);  // [cap][128] candidate D~ (column = query)
+  // 4 x 16 KB operand slots: streaming mode (KB > 1) stage s = (A slot s, B slot 2 + s);
+  // resident mode (KB == 1) A = slot 0 (loaded once per query tile), B stages = slots 1..3
+  uint8_t* slots = smem;
+  const bool ares = a.KB == 1;
+  const int nst = ares ? kBStagesRes : kStages;
+  float* lk = reinterpret_cast<float*>(slots + 4 * kABytes);  // [cap][128] candidate D~ (column = query)
   int32_t* li = reinterpret_cast<int32_t*>(lk + a.cap * kBM);   // [cap][128] candidate index
   float* pn_stage = reinterpret_cast<float*>(li + a.cap * kBM);      // [4 warps][kBN]
   float* scratch = pn_stage + 4 * kBN;                                // [4 warps][32 lanes][kScrStride]
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 4 * 32 * kScrStride);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;  // 2 TMEM buffers
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* empty = full + kBStagesRes;
+  uint64_t* tfull = empty + kBStagesRes;  // kTBufs TMEM buffers
+  uint64_t* tempty = tfull + kTBufs;
+  uint64_t* afull = tempty + kTBufs;      // resident query tile
+  uint64_t* aempty = afull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -248,19 +253,21 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   const int64_t npt = (a.np + kBN - 1) / kBN;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kBStagesRes; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kTBufs; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 128);
     }
+    mbar_init(afull, 1);
+    mbar_init(aempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                 "r"(2 * kBN));
+                 "r"(kTBufs * kBN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -272,16 +279,27 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     // ---------------- TMA producer
     if (lane == 0) {
       int stage = 0;
-      uint32_t phase = 0;
+      uint32_t phase = 0, aphase = 0;
       for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
         const int64_t pt_end = a.debug_G ? 1 : npt;
+        if (ares) {
+          mbar_wait_sleep(aempty, aphase ^ 1);
+          mbar_expect_tx(afull, kABytes);
+          tma_load_2d(slots, &tmQ, afull, 0, static_cast<int>(qt * kBM));
+          aphase ^= 1;
+        }
         for (int64_t pt = 0; pt < pt_end; ++pt) {
           for (int kb = 0; kb < a.KB; ++kb) {
             mbar_wait_sleep(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], kStageBytes);
-            tma_load_2d(sA + stage * kABytes, &tmQ, &full[stage], kb * kBK, static_cast<int>(qt * kBM));
-            tma_load_2d(sB + stage * kBBytes, &tmP, &full[stage], kb * kBK, static_cast<int>(pt * kBN));
-            if (++stage == kStages) {
+            if (ares) {
+              mbar_expect_tx(&full[stage], kBBytes);
+              tma_load_2d(slots + (1 + stage) * kABytes, &tmP, &full[stage], 0, static_cast<int>(pt * kBN));
+            } else {
+              mbar_expect_tx(&full[stage], kStageBytes);
+              tma_load_2d(slots + stage * kABytes, &tmQ, &full[stage], kb * kBK, static_cast<int>(qt * kBM));
+              tma_load_2d(slots + (2 + stage) * kABytes, &tmP, &full[stage], kb * kBK, static_cast<int>(pt * kBN));
+            }
+            if (++stage == nst) {
               stage = 0;
               phase ^= 1;
             }
@@ -292,11 +310,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   } else if (warp == 1) {
     // ---------------- MMA issuer
     int stage = 0;
-    uint32_t phase = 0;
+    uint32_t phase = 0, aphase = 0;
     int buf = 0;
     uint32_t tphase = 0;
     for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
       const int64_t pt_end = a.debug_G ? 1 : npt;
+      if (ares) {
+        mbar_wait(afull, aphase);
+        aphase ^= 1;
+      }
       for (int64_t pt = 0; pt < pt_end; ++pt) {
         mbar_wait_sleep(&tempty[buf], tphase ^ 1);
         tc_fence_after();
@@ -305,8 +327,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
-            const uint64_t ad = sdesc_sw128(su32(sA + stage * kABytes));
-            const uint64_t bd = sdesc_sw128(su32(sB + stage * kBBytes));
+            const uint64_t ad = sdesc_sw128(su32(ares ? slots : slots + stage * kABytes));
+            const uint64_t bd = sdesc_sw128(su32(slots + (ares ? 1 + stage : 2 + stage) * kABytes));
 #pragma unroll
             for (int k16 = 0; k16 < kBK / 16; ++k16)
               tc_mma_f16(d_tmem, ad + 2 * k16, bd + 2 * k16, kIdesc, (kb > 0 || k16 > 0) ? 1u : 0u);
@@ -314,15 +336,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             if (kb == a.KB - 1) tc_commit(&tfull[buf]);
           }
           __syncwarp();
-          if (++stage == kStages) {
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (++buf == 2) {
+        if (++buf == kTBufs) {
           buf = 0;
           tphase ^= 1;
         }
+      }
+      if (ares) {
+        if (lane == 0) tc_commit(aempty);  // query tile free once this tile's MMAs complete
+        __syncwarp();
       }
     }
   } else {
@@ -513,7 +539,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
-        if (++buf == 2) {
+        if (++buf == kTBufs) {
           buf = 0;
           tphase ^= 1;
         }
@@ -536,7 +562,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kBN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTBufs * kBN));
   }
 }
 
