@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define FMGP_ABI_VERSION 1
+#define FMGP_ABI_VERSION 2
 
 enum fmgp_status { FMGP_OK = 0, FMGP_EINVAL = 1, FMGP_ENUMERIC = 2, FMGP_ECUDA = 3 };
 
@@ -168,6 +168,64 @@ int fmgp_kernel_values(const double* dist, int64_t ndist, const fmgp_kernel_para
  * with *failed_index = the lowest failing matrix. */
 int fmgp_solve_spd_batched(const double* K, const double* B, int64_t batch, int32_t k, int32_t m,
                            double* X_out, double* applied_jitter, int64_t* failed_index);
+
+/* ---- MuyGPs training and the localized baseline ---------
+ * muygps.cpp:32-62 local_prediction for b batch entries at once: entry t
+ * predicts Y[batch_idx[t]] from its neighbour list nbr[t*k .. t*k+k) (the
+ * caller's NeighborList indices, which must not contain batch_idx[t]) and
+ * the list's distances dist[t*k ..] (cross-covariance = kernel(distance), as
+ * the reference uses NeighborList.distances):
+ *   preds_out[t] = cross_t . K(X[nbr_t])^{-1} Y[nbr_t]   (Y: n values)
+ * One fused gather -> K -> jitter-ladder Cholesky -> solve per entry, then a
+ * cross-covariance dot. FMGP_ENUMERIC: *failed_entry = the lowest failing t
+ * (the first entry the reference's sequential loop would throw on).
+ * Replaces local_prediction (muygps.hpp:50-52, muygps.cpp:32-62). */
+int fmgp_local_predictions(const double* X, const double* Y, int64_t n, int32_t d, const int32_t* batch_idx,
+                           const int32_t* nbr, const double* dist, int64_t b, int32_t k,
+                           const fmgp_kernel_params* params, double* preds_out, int64_t* failed_entry);
+
+/* Device-resident leave-one-out session for the optimizer loop (muygps.cpp:
+ * 64-78 loocv_loss, evaluated up to max_evals times by train): X, Y, the
+ * batch, its neighbour lists and distances are uploaded once; each
+ * evaluation uploads the kernel parameters only and reads back b
+ * predictions. loss_out = sum_t (Y[i_t] - pred_t)^2 / b accumulated on the
+ * host in batch order (the reference's bit-stable order). preds_out
+ * (nullable, b). */
+typedef struct fmgp_loocv fmgp_loocv;
+int fmgp_loocv_create(const double* X, const double* Y, int64_t n, int32_t d, const int32_t* batch_idx,
+                      const int32_t* nbr, const double* dist, int64_t b, int32_t k, fmgp_loocv** out);
+int fmgp_loocv_eval(fmgp_loocv* session, const fmgp_kernel_params* params, double* loss_out, double* preds_out,
+                    int64_t* failed_entry);
+void fmgp_loocv_destroy(fmgp_loocv* session);
+
+/* train (muygps.cpp:214-270): neighbour lists of the batch (k exact
+ * neighbours, self excluded) computed once on the device, then a bounded
+ * Nelder-Mead over log10(rho), nu, tau (each free when its has_* flag is
+ * set) minimising the device LOOCV loss; never returns a loss above the
+ * initial one. kind is fixed. Outputs the fitted parameters (theta_out),
+ * the final loss, the number of loss evaluations and whether the initial
+ * guess was improved. Errors: FMGP_EINVAL with the reference's messages
+ * ("train: k must be at least 2", "train: invalid bounds", ...),
+ * FMGP_ENUMERIC when a local solve fails ("local_prediction at index i"). */
+typedef struct {
+  int32_t k;
+  int32_t kind;
+  int32_t has_rho, has_nu, has_tau;
+  double rho_lo, rho_hi, nu_lo, nu_hi, tau_lo, tau_hi;
+  int32_t max_evals;
+  double tol;
+} fmgp_train_config;
+int fmgp_train(const double* X, const double* Y, int64_t n, int32_t d, const int32_t* batch_idx, int64_t b,
+               const fmgp_kernel_params* initial, const fmgp_train_config* config, fmgp_kernel_params* theta_out,
+               double* final_loss, int32_t* evaluations, int32_t* improved);
+
+/* muygps_predict (muygps.cpp:272-295), the localized baseline predictor:
+ * each test point's own k exact neighbours (device kNN), one k x k solve,
+ * cross-covariance dot, + mean_offset. FMGP_ENUMERIC names the lowest
+ * failing test row in *failed_row ("muygps_predict" context). */
+int fmgp_muygps_predict(const double* X, const double* Y, int64_t n, int32_t d, const double* Z, int64_t nz,
+                        int32_t k, const fmgp_kernel_params* params, double mean_offset, double* out,
+                        int64_t* failed_row);
 
 /* ---- diagnostics ---------------------------------------------------------
  * D~ (the tensor-core filter value n^_q + n^_p - 2 q^.p^ in the scaled fp16

@@ -338,3 +338,72 @@ int fmgp_oracle_predict(const double* X, const int32_t* S, const double* C,
   free(tids);
   return 0;
 }
+
+/* muygps.cpp:32-62 local_prediction for b entries (k-neighbour lists nbr,
+ * their distances dist): cross = kernel_value(dist), coeff = solve_spd(
+ * cov_matrix_self(X[nbr]), Y[nbr]), pred = cross . coeff (sequential sum).
+ * Returns 0, or 2 with *failed_entry = the first failing entry (the
+ * reference's sequential loop order). Validation is the caller's job. */
+int fmgp_oracle_local_predictions(const double* X, const double* Y, int64_t n,
+                                  int d, const int32_t* nbr, const double* dist,
+                                  int64_t b, int k, int kind, double sigma,
+                                  double rho, double nu, double tau,
+                                  double* preds, int64_t* failed_entry) {
+  (void)n;
+  double* xs = (double*)malloc(sizeof(double) * (size_t)k * (size_t)d);
+  double* K = (double*)malloc(sizeof(double) * (size_t)k * (size_t)k);
+  double* y = (double*)malloc(sizeof(double) * (size_t)k);
+  int rc = 0;
+  if (failed_entry) *failed_entry = -1;
+  for (int64_t t = 0; t < b && rc == 0; ++t) {
+    for (int j = 0; j < k; ++j) {
+      const int64_t r = nbr[t * k + j];
+      memcpy(xs + (size_t)j * d, X + r * d, sizeof(double) * (size_t)d);
+      y[j] = Y[r];
+    }
+    fmgp_oracle_cov_self(xs, k, d, kind, sigma, rho, nu, tau, K);
+    if (fmgp_oracle_cholesky_jitter(K, k, NULL) != 0) {
+      if (failed_entry) *failed_entry = t;
+      rc = 2;
+      break;
+    }
+    llt_solve(K, k, y, 1);
+    double acc = 0.0;
+    for (int j = 0; j < k; ++j)
+      acc += fmgp_oracle_kernel_value(dist[t * k + j], kind, sigma, rho, nu, tau) * y[j];
+    preds[t] = acc;
+  }
+  free(xs);
+  free(K);
+  free(y);
+  return rc;
+}
+
+/* muygps.cpp:272-295: each test point's own k exact neighbours
+ * (query_knn, distances sqrt(dist_sq)), then local_prediction's arithmetic
+ * + mean_offset. Returns 0 or 2 (*failed_row = first failing test point). */
+int fmgp_oracle_muygps_predict(const double* X, const double* Y, int64_t n,
+                               int d, double mean_offset, const double* Z,
+                               int64_t nz, int k, int kind, double sigma,
+                               double rho, double nu, double tau, double* out,
+                               int64_t* failed_row) {
+  int32_t* idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)k);
+  double* ds = (double*)malloc(sizeof(double) * (size_t)k);
+  int rc = 0;
+  if (failed_row) *failed_row = -1;
+  for (int64_t t = 0; t < nz && rc == 0; ++t) {
+    fmgp_oracle_query_knn(X, n, d, Z + t * d, k, -1, idx, ds);
+    for (int j = 0; j < k; ++j) ds[j] = sqrt(ds[j]);
+    int64_t fe = -1;
+    if (fmgp_oracle_local_predictions(X, Y, n, d, idx, ds, 1, k, kind, sigma, rho,
+                                      nu, tau, out + t, &fe) != 0) {
+      if (failed_row) *failed_row = t;
+      rc = 2;
+      break;
+    }
+    out[t] += mean_offset;
+  }
+  free(idx);
+  free(ds);
+  return rc;
+}

@@ -42,6 +42,17 @@ int fmgp_oracle_predict(const double* X, const int32_t* S, const double* C,
                         const double* Z, int64_t nz, int threads, double* out,
                         int32_t* nn_out);
 
+int fmgp_oracle_local_predictions(const double* X, const double* Y, int64_t n,
+                                  int d, const int32_t* nbr, const double* dist,
+                                  int64_t b, int k, int kind, double sigma,
+                                  double rho, double nu, double tau,
+                                  double* preds, int64_t* failed_entry);
+int fmgp_oracle_muygps_predict(const double* X, const double* Y, int64_t n,
+                               int d, double mean_offset, const double* Z,
+                               int64_t nz, int k, int kind, double sigma,
+                               double rho, double nu, double tau, double* out,
+                               int64_t* failed_row);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,10 @@
 //                               NeighborIndex::query_knn, cov_matrix_self, solve_spd
 //   fmgp_ref_predict         -> fast_predict_batch / fast_predict_one (fast_predict.cpp:132-156)
 //   fmgp_ref_query_knn, fmgp_ref_nearest, fmgp_ref_kernel_value -> nn_index.cpp / kernel.cpp
+//   fmgp_ref_local_predictions -> local_prediction per entry     (muygps.cpp:32-62)
+//   fmgp_ref_loocv_loss      -> loocv_loss                       (muygps.cpp:64-78)
+//   fmgp_ref_train           -> BatchSpec::sample + train        (muygps.cpp:15-30, :214-270)
+//   fmgp_ref_muygps_predict  -> muygps_predict                   (muygps.cpp:272-295)
 // Multi-output (BASELINE cfg3, m > 1): the reference is single-output
 // (dataset.hpp:14); the harness shares S and passes the k x m right-hand
 // sides to the reference's own solve_spd (linalg.hpp:19-20), which solves
@@ -27,6 +31,7 @@
 #include "fastmuygps/fast_predict.hpp"
 #include "fastmuygps/kernel.hpp"
 #include "fastmuygps/linalg.hpp"
+#include "fastmuygps/muygps.hpp"
 #include "fastmuygps/nn_index.hpp"
 
 using namespace fastmuygps;
@@ -40,6 +45,12 @@ Eigen::MatrixXd from_rm(const double* a, int64_t n, int d) {
   for (int64_t i = 0; i < n; ++i)
     for (int j = 0; j < d; ++j) X(i, j) = a[i * d + j];
   return X;
+}
+
+Eigen::VectorXd vec_from(const double* a, int64_t n) {
+  Eigen::VectorXd v(n);
+  for (int64_t i = 0; i < n; ++i) v(i) = a[i];
+  return v;
 }
 
 template <typename F>
@@ -223,6 +234,77 @@ int fmgp_ref_nearest(const double* X_rm, int64_t n, int d, const double* Q_rm,
       for (int j = 0; j < d; ++j) qq(j) = Q_rm[t * d + j];
       out[t] = index.nearest_training_point(qq);
     }
+  });
+}
+
+int fmgp_ref_local_predictions(const double* X_rm, const double* Y, int64_t n, int d, const int32_t* batch,
+                               const int32_t* nbr, const double* dist, int64_t b, int k, int kind, double sigma,
+                               double rho, double nu, double tau, double* preds) {
+  return guard([&] {
+    TrainingSet ts{from_rm(X_rm, n, d), vec_from(Y, n), 0.0};
+    KernelParams p(sigma, rho, nu, tau);
+    for (int64_t t = 0; t < b; ++t) {
+      NeighborList nl;
+      nl.indices.assign(nbr + t * k, nbr + t * k + k);
+      nl.distances.assign(dist + t * k, dist + t * k + k);
+      preds[t] = local_prediction(ts, batch[t], nl, static_cast<KernelKind>(kind), p);
+    }
+  });
+}
+
+int fmgp_ref_loocv_loss(const double* X_rm, const double* Y, int64_t n, int d, const int32_t* batch,
+                        const int32_t* nbr, const double* dist, int64_t b, int k, int kind, double sigma, double rho,
+                        double nu, double tau, double* loss) {
+  return guard([&] {
+    TrainingSet ts{from_rm(X_rm, n, d), vec_from(Y, n), 0.0};
+    BatchSpec bs{static_cast<int>(b), 0, std::vector<int>(batch, batch + b)};
+    std::vector<NeighborList> lists(b);
+    for (int64_t t = 0; t < b; ++t) {
+      lists[t].indices.assign(nbr + t * k, nbr + t * k + k);
+      lists[t].distances.assign(dist + t * k, dist + t * k + k);
+    }
+    *loss = loocv_loss(ts, bs, lists, static_cast<KernelKind>(kind), KernelParams(sigma, rho, nu, tau));
+  });
+}
+
+// bounds: [has_rho, has_nu, has_tau] flags and [rho_lo, rho_hi, nu_lo, nu_hi, tau_lo, tau_hi].
+int fmgp_ref_train(const double* X_rm, const double* Y, int64_t n, int d, int batch_b, uint64_t batch_seed, int k,
+                   int kind, double sigma, double rho, double nu, double tau, const int32_t* has,
+                   const double* bounds, int max_evals, double tol, double* theta_out /*sigma,rho,nu,tau*/,
+                   double* final_loss, int32_t* evaluations, int32_t* improved, int32_t* batch_out) {
+  return guard([&] {
+    TrainingSet ts{from_rm(X_rm, n, d), vec_from(Y, n), 0.0};
+    NeighborIndex index = NeighborIndex::build(ts.X, IndexMode::Exact);
+    BatchSpec bs = BatchSpec::sample(static_cast<int>(n), batch_b, batch_seed);
+    std::copy(bs.indices.begin(), bs.indices.end(), batch_out);
+    TrainConfig cfg;
+    cfg.k = k;
+    cfg.kind = static_cast<KernelKind>(kind);
+    if (has[0]) cfg.rho_bounds = Bounds{bounds[0], bounds[1]};
+    if (has[1]) cfg.nu_bounds = Bounds{bounds[2], bounds[3]};
+    if (has[2]) cfg.tau_bounds = Bounds{bounds[4], bounds[5]};
+    cfg.max_evals = max_evals;
+    cfg.tol = tol;
+    FittedParams f = train(ts, KernelParams(sigma, rho, nu, tau), cfg, bs, index);
+    theta_out[0] = f.theta_hat.sigma();
+    theta_out[1] = f.theta_hat.rho();
+    theta_out[2] = f.theta_hat.nu();
+    theta_out[3] = f.theta_hat.tau();
+    *final_loss = f.final_loss;
+    *evaluations = f.evaluations;
+    *improved = f.improved ? 1 : 0;
+  });
+}
+
+int fmgp_ref_muygps_predict(const double* X_rm, const double* Y, int64_t n, int d, double mean_offset,
+                            const double* Z_rm, int64_t nz, int k, int kind, double sigma, double rho, double nu,
+                            double tau, double* out) {
+  return guard([&] {
+    TrainingSet ts{from_rm(X_rm, n, d), vec_from(Y, n), mean_offset};
+    NeighborIndex index = NeighborIndex::build(ts.X, IndexMode::Exact);
+    FittedParams f{KernelParams(sigma, rho, nu, tau), static_cast<KernelKind>(kind), 0.0, 0, false};
+    Eigen::VectorXd r = muygps_predict(ts, from_rm(Z_rm, nz, d), f, index, k);
+    for (int64_t t = 0; t < nz; ++t) out[t] = r(t);
   });
 }
 

@@ -65,7 +65,41 @@ class Port:
         L.fmgp_oracle_predict.restype = C.c_int
         L.fmgp_oracle_predict.argtypes = ([_V, _V, _V, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int] +
                                           [C.c_double] * 5 + [_V, C.c_int64, C.c_int, _V, _V])
+        L.fmgp_oracle_local_predictions.restype = C.c_int
+        L.fmgp_oracle_local_predictions.argtypes = ([_V, _V, C.c_int64, C.c_int, _V, _V, C.c_int64, C.c_int,
+                                                     C.c_int] + [C.c_double] * 4 + [_V, _V])
+        L.fmgp_oracle_muygps_predict.restype = C.c_int
+        L.fmgp_oracle_muygps_predict.argtypes = ([_V, _V, C.c_int64, C.c_int, C.c_double, _V, C.c_int64, C.c_int,
+                                                  C.c_int] + [C.c_double] * 4 + [_V, _V])
         self.L = L
+
+    def local_predictions(self, X, Y, nbr, dist, kind, sigma, rho, nu, tau):
+        """muygps.cpp:32-62 per entry (no argument validation)."""
+        X = _f64(X)
+        Y = _f64(Y).reshape(-1)
+        nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+        dist = _f64(dist)
+        b, k = nbr.shape
+        out = np.empty(b, dtype=np.float64)
+        fe = C.c_int64(-1)
+        rc = self.L.fmgp_oracle_local_predictions(_p(X), _p(Y), X.shape[0], X.shape[1], _p(nbr), _p(dist), b, k,
+                                                  kind, sigma, rho, nu, tau, _p(out), C.byref(fe))
+        if rc != 0:
+            raise OracleError(rc, "local_prediction: Cholesky factorization failed", fe.value)
+        return out
+
+    def muygps_predict(self, X, Y, mean_offset, Z, k, kind, sigma, rho, nu, tau):
+        """muygps.cpp:272-295."""
+        X = _f64(X)
+        Y = _f64(Y).reshape(-1)
+        Z = _f64(Z)
+        out = np.empty(Z.shape[0], dtype=np.float64)
+        fr = C.c_int64(-1)
+        rc = self.L.fmgp_oracle_muygps_predict(_p(X), _p(Y), X.shape[0], X.shape[1], mean_offset, _p(Z), Z.shape[0],
+                                               k, kind, sigma, rho, nu, tau, _p(out), C.byref(fr))
+        if rc != 0:
+            raise OracleError(rc, "muygps_predict: Cholesky factorization failed", fr.value)
+        return out
 
     def kernel_value(self, dist, kind, sigma, rho, nu, tau):
         return self.L.fmgp_oracle_kernel_value(dist, kind, sigma, rho, nu, tau)
@@ -161,7 +195,68 @@ class Reference:
         L.fmgp_ref_query_knn.argtypes = [_V, C.c_int64, C.c_int, _V, C.c_int, C.c_int, _V, _V]
         L.fmgp_ref_nearest.restype = C.c_int
         L.fmgp_ref_nearest.argtypes = [_V, C.c_int64, C.c_int, _V, C.c_int64, _V]
+        L.fmgp_ref_local_predictions.restype = C.c_int
+        L.fmgp_ref_local_predictions.argtypes = ([_V, _V, C.c_int64, C.c_int, _V, _V, _V, C.c_int64, C.c_int,
+                                                  C.c_int] + [C.c_double] * 4 + [_V])
+        L.fmgp_ref_loocv_loss.restype = C.c_int
+        L.fmgp_ref_loocv_loss.argtypes = ([_V, _V, C.c_int64, C.c_int, _V, _V, _V, C.c_int64, C.c_int, C.c_int] +
+                                          [C.c_double] * 4 + [_V])
+        L.fmgp_ref_train.restype = C.c_int
+        L.fmgp_ref_train.argtypes = ([_V, _V, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int] +
+                                     [C.c_double] * 4 + [_V, _V, C.c_int, C.c_double, _V, _V, _V, _V, _V])
+        L.fmgp_ref_muygps_predict.restype = C.c_int
+        L.fmgp_ref_muygps_predict.argtypes = ([_V, _V, C.c_int64, C.c_int, C.c_double, _V, C.c_int64, C.c_int,
+                                               C.c_int] + [C.c_double] * 4 + [_V])
         self.L = L
+
+    def local_predictions(self, X, Y, batch, nbr, dist, kind, sigma, rho, nu, tau):
+        X = _f64(X)
+        Y = _f64(Y).reshape(-1)
+        bi = np.ascontiguousarray(batch, dtype=np.int32)
+        nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+        dist = _f64(dist)
+        out = np.empty(bi.size, dtype=np.float64)
+        self._check(self.L.fmgp_ref_local_predictions(_p(X), _p(Y), X.shape[0], X.shape[1], _p(bi), _p(nbr),
+                                                      _p(dist), bi.size, nbr.shape[1], kind, sigma, rho, nu, tau,
+                                                      _p(out)))
+        return out
+
+    def loocv_loss(self, X, Y, batch, nbr, dist, kind, sigma, rho, nu, tau):
+        X = _f64(X)
+        Y = _f64(Y).reshape(-1)
+        bi = np.ascontiguousarray(batch, dtype=np.int32)
+        nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+        dist = _f64(dist)
+        loss = C.c_double(0.0)
+        self._check(self.L.fmgp_ref_loocv_loss(_p(X), _p(Y), X.shape[0], X.shape[1], _p(bi), _p(nbr), _p(dist),
+                                               bi.size, nbr.shape[1], kind, sigma, rho, nu, tau, C.byref(loss)))
+        return loss.value
+
+    def train(self, X, Y, b, seed, k, kind, sigma, rho, nu, tau, bounds, max_evals=200, tol=1e-8):
+        """bounds: dict with optional 'rho'/'nu'/'tau' -> (lo, hi). Returns
+        ((sigma, rho, nu, tau), final_loss, evaluations, improved, batch indices)."""
+        X = _f64(X)
+        Y = _f64(Y).reshape(-1)
+        has = np.array([int(n in bounds) for n in ("rho", "nu", "tau")], dtype=np.int32)
+        bnd = np.array([v for n in ("rho", "nu", "tau") for v in bounds.get(n, (0.0, 0.0))], dtype=np.float64)
+        theta = np.empty(4, dtype=np.float64)
+        loss = C.c_double(0.0)
+        ev = C.c_int32(0)
+        imp = C.c_int32(0)
+        batch = np.empty(b, dtype=np.int32)
+        self._check(self.L.fmgp_ref_train(_p(X), _p(Y), X.shape[0], X.shape[1], b, seed, k, kind, sigma, rho, nu,
+                                          tau, _p(has), _p(bnd), max_evals, tol, _p(theta), C.byref(loss),
+                                          C.byref(ev), C.byref(imp), _p(batch)))
+        return tuple(theta.tolist()), loss.value, ev.value, bool(imp.value), batch.tolist()
+
+    def muygps_predict(self, X, Y, mean_offset, Z, k, kind, sigma, rho, nu, tau):
+        X = _f64(X)
+        Y = _f64(Y).reshape(-1)
+        Z = _f64(Z)
+        out = np.empty(Z.shape[0], dtype=np.float64)
+        self._check(self.L.fmgp_ref_muygps_predict(_p(X), _p(Y), X.shape[0], X.shape[1], mean_offset, _p(Z),
+                                                   Z.shape[0], k, kind, sigma, rho, nu, tau, _p(out)))
+        return out
 
     def _check(self, rc):
         if rc != 0:

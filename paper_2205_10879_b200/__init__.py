@@ -1,4 +1,5 @@
-"""B200-native FastMuyGPs posterior-mean path (precompute + predict).
+"""B200-native FastMuyGPs posterior-mean path (precompute + predict), plus the
+MuyGPs training inner loop and localized predictor built from the same kernels.
 
 Public names mirror the reference C++ API (namespace fastmuygps); they are
 loaded lazily from `api` so that `python -m paper_2205_10879_b200.build` works
@@ -14,7 +15,8 @@ _API = {
     "NeighborList", "PrecomputedModel", "precompute", "fast_predict_one", "fast_predict_batch",
     "kernel_value", "kernel_values", "matern_value", "rbf_value", "cov_matrix", "cov_matrix_self",
     "solve_spd", "solve_spd_batched", "precompute_device", "predict_device", "DomainError", "NumericError",
-    "CudaError", "FmgpError",
+    "CudaError", "FmgpError", "BatchSpec", "Bounds", "TrainConfig", "local_prediction", "local_predictions",
+    "loocv_loss", "LoocvSession", "train", "muygps_predict",
 }
 
 __all__ = sorted(_API)

@@ -20,6 +20,13 @@ class KernelParamsC(C.Structure):
                 ("nu", C.c_double), ("tau", C.c_double)]
 
 
+class TrainConfigC(C.Structure):
+    _fields_ = [("k", C.c_int32), ("kind", C.c_int32), ("has_rho", C.c_int32), ("has_nu", C.c_int32),
+                ("has_tau", C.c_int32), ("rho_lo", C.c_double), ("rho_hi", C.c_double), ("nu_lo", C.c_double),
+                ("nu_hi", C.c_double), ("tau_lo", C.c_double), ("tau_hi", C.c_double), ("max_evals", C.c_int32),
+                ("tol", C.c_double)]
+
+
 _d = C.POINTER(C.c_double)
 _i32 = C.POINTER(C.c_int32)
 _i64 = C.POINTER(C.c_int64)
@@ -57,6 +64,16 @@ SIGNATURES: dict[str, tuple] = {
     "fmgp_cov_matrix": (C.c_int, [_vp, C.c_int64, _vp, C.c_int64, C.c_int32, _kp, _vp]),
     "fmgp_kernel_values": (C.c_int, [_vp, C.c_int64, _kp, _vp]),
     "fmgp_solve_spd_batched": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _vp, _vp, _i64]),
+    "fmgp_local_predictions": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp, _vp, _vp, C.c_int64, C.c_int32,
+                                         _kp, _vp, _i64]),
+    "fmgp_loocv_create": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp, _vp, _vp, C.c_int64, C.c_int32,
+                                    C.POINTER(_vp)]),
+    "fmgp_loocv_eval": (C.c_int, [_vp, _kp, _d, _vp, _i64]),
+    "fmgp_loocv_destroy": (None, [_vp]),
+    "fmgp_train": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp, C.c_int64, _kp, C.POINTER(TrainConfigC), _kp,
+                             _d, _i32, _i32]),
+    "fmgp_muygps_predict": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp, C.c_int64, C.c_int32, _kp, C.c_double,
+                                      _vp, _i64]),
     "fmgp_debug_tc_tile": (C.c_int, [_vp, C.c_int64, _vp, C.c_int64, C.c_int32, _vp]),
 }
 

@@ -367,3 +367,177 @@ def predict_device(X, S, Cmat, fitted: FittedParams, mean_offset, Z, out, nn_out
     rc = N.LIB.fmgp_predict_device(_dp(X), _dp(S), _dp(Cmat), n, d, k, m, C.byref(kp), _ptr(mo), _dp(Z), Z.shape[0],
                                    _dp(out), None if nn_out is None else _dp(nn_out), C.c_void_p(s.cuda_stream))
     N.check(rc)
+
+
+# ------------------------------------------------------------------ MuyGPs
+# muygps.hpp: the training inner loop (LOOCV over a batch, Nelder-Mead) and
+# the localized baseline predictor, on the device (include/fmgp_b200.h).
+
+@dataclass
+class BatchSpec:
+    """muygps.hpp:15-21."""
+    b: int = 0
+    seed: int = 0
+    indices: list = field(default_factory=list)
+
+    @staticmethod
+    def sample(n: int, b: int, seed: int) -> "BatchSpec":
+        """muygps.cpp:15-30 (partial Fisher-Yates over std::mt19937_64)."""
+        from . import datagen
+        if b < 1 or b > n:
+            raise DomainError(N.FMGP_EINVAL, "BatchSpec: batch size out of range")
+        return BatchSpec(b, seed, datagen.batch_sample(n, b, seed))
+
+
+@dataclass
+class Bounds:
+    lo: float
+    hi: float
+
+
+@dataclass
+class TrainConfig:
+    """muygps.hpp:28-39."""
+    k: int = 50
+    kind: KernelKind = KernelKind.Matern
+    rho_bounds: Bounds | None = None
+    nu_bounds: Bounds | None = None
+    tau_bounds: Bounds | None = None
+    max_evals: int = 200
+    tol: float = 1e-8
+
+
+def _lists_to_arrays(neighbor_lists) -> tuple[np.ndarray, np.ndarray]:
+    k = len(neighbor_lists[0].indices)
+    nbr = np.array([list(nl.indices) for nl in neighbor_lists], dtype=np.int32).reshape(len(neighbor_lists), k)
+    dist = np.array([list(nl.distances) for nl in neighbor_lists], dtype=np.float64).reshape(len(neighbor_lists), k)
+    return nbr, dist
+
+
+def local_predictions(train: TrainingSet, batch_indices, nbr, dist, kind: KernelKind, p: KernelParams) -> np.ndarray:
+    """fmgp_local_predictions: local_prediction (muygps.cpp:32-62) for b entries with k-neighbour lists."""
+    X = _f64(train.X)
+    Y = _f64(train.Y)
+    bi = np.ascontiguousarray(batch_indices, dtype=np.int32)
+    nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+    dist = _f64(dist)
+    b = bi.shape[0]
+    k = nbr.shape[1] if nbr.ndim == 2 else 0
+    out = np.empty(b, dtype=np.float64)
+    failed = C.c_int64(-1)
+    kp = p.c(kind)
+    rc = N.LIB.fmgp_local_predictions(_ptr(X), _ptr(Y), X.shape[0], X.shape[1], _ptr(bi), _ptr(nbr), _ptr(dist),
+                                      b, k, C.byref(kp), _ptr(out), C.byref(failed))
+    N.check(rc, failed.value)
+    return out
+
+
+def local_prediction(train: TrainingSet, i: int, neighbors: NeighborList, kind: KernelKind,
+                     p: KernelParams) -> float:
+    """muygps.cpp:32-62 (one entry)."""
+    k = len(neighbors.indices)
+    nbr = np.asarray(neighbors.indices, dtype=np.int32).reshape(1, k)
+    dist = np.asarray(neighbors.distances, dtype=np.float64).reshape(1, k)
+    return float(local_predictions(train, [i], nbr, dist, kind, p)[0])
+
+
+def loocv_loss(train: TrainingSet, batch: BatchSpec, neighbor_lists, kind: KernelKind, p: KernelParams) -> float:
+    """muygps.cpp:64-78: mean squared leave-one-out residual over the batch (sequential sum)."""
+    if len(neighbor_lists) != len(batch.indices) or not batch.indices:
+        raise DomainError(N.FMGP_EINVAL, "loocv_loss: batch and neighbor lists disagree")
+    sizes = {len(nl.indices) for nl in neighbor_lists}
+    Y = np.asarray(train.Y, dtype=np.float64)
+    if len(sizes) == 1:
+        nbr, dist = _lists_to_arrays(neighbor_lists)
+        preds = local_predictions(train, batch.indices, nbr, dist, kind, p)
+    else:  # ragged lists: entry by entry, in batch order (the reference's error order)
+        preds = [local_prediction(train, i, nl, kind, p) for i, nl in zip(batch.indices, neighbor_lists)]
+    s = 0.0
+    for i, pr in zip(batch.indices, preds):
+        r = float(Y[i]) - float(pr)
+        s += r * r
+    return s / float(len(batch.indices))
+
+
+class LoocvSession:
+    """fmgp_loocv_*: device-resident LOOCV data for repeated loss evaluations."""
+
+    def __init__(self, train: TrainingSet, batch: BatchSpec, neighbor_lists):
+        if len(neighbor_lists) != len(batch.indices) or not batch.indices:
+            raise DomainError(N.FMGP_EINVAL, "loocv_loss: batch and neighbor lists disagree")
+        X = _f64(train.X)
+        Y = _f64(train.Y)
+        bi = np.ascontiguousarray(batch.indices, dtype=np.int32)
+        nbr, dist = _lists_to_arrays(neighbor_lists)
+        h = C.c_void_p()
+        N.check(N.LIB.fmgp_loocv_create(_ptr(X), _ptr(Y), X.shape[0], X.shape[1], _ptr(bi), _ptr(nbr), _ptr(dist),
+                                        bi.shape[0], nbr.shape[1], C.byref(h)))
+        self._h = h
+        self.b = bi.shape[0]
+
+    def loss(self, kind: KernelKind, p: KernelParams, with_predictions: bool = False):
+        kp = p.c(kind)
+        val = C.c_double(0.0)
+        failed = C.c_int64(-1)
+        preds = np.empty(self.b, dtype=np.float64) if with_predictions else None
+        N.check(N.LIB.fmgp_loocv_eval(self._h, C.byref(kp), C.byref(val), _ptr(preds), C.byref(failed)),
+                failed.value)
+        return (val.value, preds) if with_predictions else val.value
+
+    def close(self):
+        if self._h:
+            N.LIB.fmgp_loocv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
+
+
+def train(data: TrainingSet, initial: KernelParams, config: TrainConfig, batch: BatchSpec,
+          index: NeighborIndex) -> FittedParams:
+    """muygps.cpp:214-270 — neighbour lists and every LOOCV evaluation on the device."""
+    X = _f64(data.X)
+    Y = _f64(data.Y)
+    if config.k < 2:
+        raise DomainError(N.FMGP_EINVAL, "train: k must be at least 2")
+    if index.size() != X.shape[0]:
+        raise DomainError(N.FMGP_EINVAL, "train: index was not built on the training set")
+    bi = np.ascontiguousarray(batch.indices, dtype=np.int32)
+    cfg = N.TrainConfigC()
+    cfg.k, cfg.kind, cfg.max_evals, cfg.tol = config.k, int(config.kind), config.max_evals, config.tol
+    for name in ("rho", "nu", "tau"):
+        bnd = getattr(config, name + "_bounds")
+        setattr(cfg, "has_" + name, 1 if bnd is not None else 0)
+        if bnd is not None:
+            setattr(cfg, name + "_lo", bnd.lo)
+            setattr(cfg, name + "_hi", bnd.hi)
+    kp0 = initial.c(config.kind)
+    th = N.KernelParamsC()
+    loss = C.c_double(0.0)
+    evals = C.c_int32(0)
+    imp = C.c_int32(0)
+    N.check(N.LIB.fmgp_train(_ptr(X), _ptr(Y), X.shape[0], X.shape[1], _ptr(bi), bi.shape[0], C.byref(kp0),
+                             C.byref(cfg), C.byref(th), C.byref(loss), C.byref(evals), C.byref(imp)))
+    theta = KernelParams(th.sigma, th.rho, th.nu, th.tau)
+    return FittedParams(theta, config.kind, loss.value, evals.value, bool(imp.value))
+
+
+def muygps_predict(train: TrainingSet, Z, fitted: FittedParams, index: NeighborIndex, k: int) -> np.ndarray:
+    """muygps.cpp:272-295: each test point conditioned on its own k exact neighbours."""
+    X = _f64(train.X)
+    Y = _f64(train.Y)
+    Z = _f64(Z)
+    if Z.ndim == 1:
+        Z = Z.reshape(1, -1)
+    if Z.shape[1] != X.shape[1]:
+        raise DomainError(N.FMGP_EINVAL, "muygps_predict: test dimension mismatch")
+    out = np.empty(Z.shape[0], dtype=np.float64)
+    failed = C.c_int64(-1)
+    kp = fitted.theta_hat.c(fitted.kind)
+    rc = N.LIB.fmgp_muygps_predict(_ptr(X), _ptr(Y), X.shape[0], X.shape[1], _ptr(Z), Z.shape[0], k, C.byref(kp),
+                                   float(np.asarray(train.mean_offset).reshape(-1)[0]), _ptr(out), C.byref(failed))
+    N.check(rc, failed.value)
+    return out

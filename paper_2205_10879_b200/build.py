@@ -27,9 +27,9 @@ CPP = PKG / "cpp"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SOURCES = ["knn.cu", "knn_grid.cu", "knn_tc.cu", "solve.cu", "solve_big.cu", "solve_tc.cu", "solve_reg.cu", "solve_cta.cu", "predict.cu", "misc.cu", "capi.cu"]
+CUDA_SOURCES = ["knn.cu", "knn_grid.cu", "knn_tc.cu", "solve.cu", "solve_big.cu", "solve_tc.cu", "solve_reg.cu", "solve_cta.cu", "predict.cu", "misc.cu", "capi.cu", "muygps.cu"]
 FACADE_SOURCES = ["facade_kernel.cpp", "facade_linalg.cpp", "facade_nn_index.cpp", "facade_fast_predict.cpp",
-                  "facade_dataset.cpp"]
+                  "facade_dataset.cpp", "facade_muygps.cpp"]
 
 
 def _run(cmd: list[str], cwd: Path | None = None) -> None:
@@ -83,6 +83,8 @@ def build_oracle() -> None:
     _run(["make", "-s", "-C", str(REPO / "oracle")])
     if Path("/root/reference/proj/core/src/fast_predict.cpp").exists():
         _run(["make", "-s", "-C", str(REPO / "oracle"), "ref"])
+        # the reference's own test sources compiled against the facade (drop-in check)
+        _run(["make", "-s", "-C", str(REPO / "tests" / "cpp")])
 
 
 def build(product_only: bool = False, force: bool = False) -> None:

@@ -84,19 +84,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-// Producer-side roles (TMA, MMA) wait with a suspend-time hint: the thread
-// sleeps in the barrier unit until the phase completes instead of spinning
-// on the issue slots the epilogue warps need.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAITS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@P1 bra DONES_%=;\n\t"
-      "bra WAITS_%=;\n\t"
-      "DONES_%=:\n\t}" ::"r"(su32(bar)),
-      "r"(phase), "r"(1000000u)
-      : "memory");
+// Producer-side roles (TMA, MMA) waits. mode 0: spin on try_wait; 1: back off
+// with nanosleep; 2: try_wait with a suspend-time hint (the thread sleeps in
+// the barrier unit until the phase completes). 1 and 2 keep the roles' spin
+// off the issue slots the epilogue warps need (FMGP_TC_WAIT selects, A/B).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, int mode) {
+  if (mode == 2) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONES_%=;\n\t"
+        "bra WAITS_%=;\n\t"
+        "DONES_%=:\n\t}" ::"r"(su32(bar)),
+        "r"(phase), "r"(1000000u)
+        : "memory");
+    return;
+  }
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(su32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+    if (mode == 1) __nanosleep(64);
+  }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -209,6 +225,7 @@ struct TcArgs {
   int64_t self_offset;   // exclude p == q + self_offset when >= 0
   const int32_t* excl;   // or per-query exclusion (nullable)
   int with_self;
+  int wait_mode;         // producer-side wait (see mbar_wait_sleep)
   int32_t* out;          // nq x (kk + with_self)
   double* out_d;         // nq x kk (nullable)
   int32_t* cand;         // [cap][nq] candidate ids, column-major (coalesced stores)
@@ -283,14 +300,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
         const int64_t pt_end = a.debug_G ? 1 : npt;
         if (ares) {
-          mbar_wait_sleep(aempty, aphase ^ 1);
+          mbar_wait_sleep(aempty, aphase ^ 1, a.wait_mode);
           mbar_expect_tx(afull, kABytes);
           tma_load_2d(slots, &tmQ, afull, 0, static_cast<int>(qt * kBM));
           aphase ^= 1;
         }
         for (int64_t pt = 0; pt < pt_end; ++pt) {
           for (int kb = 0; kb < a.KB; ++kb) {
-            mbar_wait_sleep(&empty[stage], phase ^ 1);
+            mbar_wait_sleep(&empty[stage], phase ^ 1, a.wait_mode);
             if (ares) {
               mbar_expect_tx(&full[stage], kBBytes);
               tma_load_2d(slots + (1 + stage) * kABytes, &tmP, &full[stage], 0, static_cast<int>(pt * kBN));
@@ -320,7 +337,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         aphase ^= 1;
       }
       for (int64_t pt = 0; pt < pt_end; ++pt) {
-        mbar_wait_sleep(&tempty[buf], tphase ^ 1);
+        mbar_wait_sleep(&tempty[buf], tphase ^ 1, a.wait_mode);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * kBN);
         for (int kb = 0; kb < a.KB; ++kb) {
@@ -730,6 +747,14 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.self_offset = self_offset;
   a.excl = excl_arr;
   a.with_self = with_self;
+  {
+    static const int wm = [] {
+      const char* e = std::getenv("FMGP_TC_WAIT");
+      if (e == nullptr) return 1;
+      return e[0] == 's' && e[1] == 'p' ? 0 : (e[0] == 'h' ? 2 : 1);
+    }();
+    a.wait_mode = wm;
+  }
   a.out = out;
   a.out_d = out_d;
   a.cand = cand;

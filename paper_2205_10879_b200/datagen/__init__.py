@@ -29,6 +29,10 @@ def _load():
         lib.fmgp_generate.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64] + [C.c_void_p] * 4
         lib.fmgp_random_set.restype = None
         lib.fmgp_random_set.argtypes = [C.c_int64, C.c_int, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.fmgp_sine_set.restype = None
+        lib.fmgp_sine_set.argtypes = [C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.fmgp_batch_sample.restype = C.c_int
+        lib.fmgp_batch_sample.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_void_p]
         _lib = lib
     return _lib
 
@@ -94,3 +98,20 @@ def random_set(n: int, d: int, seed: int):
     mo = np.empty(1, dtype=np.float64)
     lib.fmgp_random_set(n, d, seed, X.ctypes.data, Y.ctypes.data, mo.ctypes.data)
     return X, Y, float(mo[0])
+
+
+def sine_set(n: int, seed: int):
+    """test_muygps.cpp:17-25: (X n x 1, detrended y, mean_offset)."""
+    X = np.empty((n, 1), dtype=np.float64)
+    Y = np.empty(n, dtype=np.float64)
+    mo = np.zeros(1, dtype=np.float64)
+    _load().fmgp_sine_set(n, seed, X.ctypes.data, Y.ctypes.data, mo.ctypes.data)
+    return X, Y, float(mo[0])
+
+
+def batch_sample(n: int, b: int, seed: int) -> list:
+    """BatchSpec::sample (muygps.cpp:15-30); raises ValueError when b is not in [1, n]."""
+    out = np.empty(max(b, 1), dtype=np.int32)
+    if _load().fmgp_batch_sample(n, b, seed, out.ctypes.data) != 0:
+        raise ValueError("BatchSpec: batch size out of range")
+    return out[:b].tolist()

@@ -161,4 +161,33 @@ void fmgp_random_set(int64_t n, int d, uint64_t seed, double* X_rm, double* Y,
   detrend(Y, n, 1, mean_offset);
 }
 
+// The MuyGPs tests' sine_set (test_muygps.cpp:17-25): x ~ U[0,1) (n x 1),
+// y = sin(8x), detrended.
+void fmgp_sine_set(int64_t n, uint64_t seed, double* X, double* Y, double* mean_offset) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u(0.0, 1.0);
+  for (int64_t i = 0; i < n; ++i) X[i] = u(rng);
+  for (int64_t i = 0; i < n; ++i) Y[i] = std::sin(8.0 * X[i]);
+  detrend(Y, n, 1, mean_offset);
+}
+
+// BatchSpec::sample (muygps.cpp:15-30): a uniform sample of b of the n
+// training indices without replacement, by a partial Fisher-Yates shuffle of
+// 0..n-1 driven by std::mt19937_64(seed). Returns 1 when b is out of [1, n].
+int fmgp_batch_sample(int32_t n, int32_t b, uint64_t seed, int32_t* out) {
+  if (b < 1 || b > n) return 1;
+  std::vector<int> pool(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) pool[i] = i;
+  std::mt19937_64 rng(seed);
+  for (int i = 0; i < b; ++i) {
+    std::uniform_int_distribution<int> pick(i, n - 1);
+    const int j = pick(rng);
+    const int t = pool[i];
+    pool[i] = pool[j];
+    pool[j] = t;
+  }
+  for (int i = 0; i < b; ++i) out[i] = pool[i];
+  return 0;
+}
+
 }  // extern "C"

@@ -50,7 +50,7 @@ def test_built_for_sm100a_only():
 
 def test_abi_version():
     from paper_2205_10879_b200 import _native
-    assert _native.LIB.fmgp_abi_version() == 1
+    assert _native.LIB.fmgp_abi_version() == 2
 
 
 def _kp(kind=0, sigma=1.0, rho=0.5, nu=1.5, tau=0.1):

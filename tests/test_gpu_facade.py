@@ -1,5 +1,5 @@
 """GPU: the drop-in boundary. The reference's own hot-path test sources
-(proj/tests/test_{kernel,nn_index,fast_predict}.cpp), compiled unmodified
+(proj/tests/test_{kernel,nn_index,fast_predict,muygps}.cpp), compiled unmodified
 against this repo's C++ facade headers (tests/cpp/Makefile), run on the GPU.
 
 Expected failures are listed explicitly with the reason; everything else in
@@ -32,7 +32,7 @@ def parse(stdout):
     return res
 
 
-@pytest.mark.parametrize("suite", ["test_kernel", "test_nn_index", "test_fast_predict"])
+@pytest.mark.parametrize("suite", ["test_kernel", "test_nn_index", "test_fast_predict", "test_muygps"])
 def test_reference_suite_against_gpu_facade(suite, tmp_path):
     exe = BUILD / f"ref_{suite}"
     if not exe.exists():

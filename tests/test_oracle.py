@@ -125,7 +125,7 @@ def test_threads_do_not_change_results(port):
     assert np.array_equal(S1, S4) and np.array_equal(C1, C4)
 
 
-@pytest.mark.parametrize("suite", ["test_kernel", "test_nn_index", "test_fast_predict"])
+@pytest.mark.parametrize("suite", ["test_kernel", "test_nn_index", "test_fast_predict", "test_muygps"])
 def test_reference_own_suites_pass_against_shim_build(suite, tmp_path):
     exe = REF_DIR / suite
     if not exe.exists():
@@ -133,3 +133,35 @@ def test_reference_own_suites_pass_against_shim_build(suite, tmp_path):
     r = subprocess.run([str(exe)], cwd=tmp_path, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "failed: 0" in r.stdout
+
+
+@pytest.mark.parametrize("kind,nu,tau", [(0, 0.5, 0.0), (0, 1.5, 0.1), (0, 2.5, 1e-3), (1, 2.5, 0.05)])
+def test_port_muygps_matches_reference(port, ref, kind, nu, tau):
+    # the restatement of local_prediction / muygps_predict (muygps.cpp:32-62,
+    # :272-295) is bit-identical to the reference's own TU
+    rng = np.random.default_rng(int(nu * 10) + kind)
+    X = rng.random((400, 2))
+    Y = np.sin(5 * X[:, 0]) - X[:, 1]
+    batch = list(range(0, 400, 9))
+    nbr, dist = [], []
+    for i in batch:
+        idx, dsq = port.query_knn(X, X[i], 12, i)
+        nbr.append(idx)
+        dist.append(np.sqrt(dsq))
+    nbr, dist = np.array(nbr), np.array(dist)
+    a = port.local_predictions(X, Y, nbr, dist, kind, 1.0, 0.2, nu, tau)
+    b = ref.local_predictions(X, Y, batch, nbr, dist, kind, 1.0, 0.2, nu, tau)
+    assert np.array_equal(a, b)
+    Z = rng.random((50, 2))
+    assert np.array_equal(port.muygps_predict(X, Y, 0.25, Z, 15, kind, 1.0, 0.2, nu, tau),
+                          ref.muygps_predict(X, Y, 0.25, Z, 15, kind, 1.0, 0.2, nu, tau))
+
+
+def test_batch_sampler_matches_reference(ref):
+    # BatchSpec::sample (muygps.cpp:15-30): the host sampler is bit-exact
+    from paper_2205_10879_b200 import datagen
+    X = np.random.default_rng(0).random((300, 1))
+    Y = np.sin(8 * X[:, 0])
+    for b, seed in [(100, 1), (300, 7), (1, 0)]:
+        *_, batch = ref.train(X, Y, b, seed, 5, 0, 1.0, 0.3, 1.5, 0.1, {}, max_evals=10)
+        assert datagen.batch_sample(300, b, seed) == batch
