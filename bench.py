@@ -253,18 +253,16 @@ def main():
             return out
         state["P"] = sharded_predict(nt, pshard)
 
-    def knn_step():
-        idx = torch.empty((n, k - 1), dtype=torch.int32, device=dev)
-        N.check(N.LIB.fmgp_query_knn_device(C.c_void_p(X.data_ptr()), n, d, C.c_void_p(X.data_ptr()), n, k - 1, 0,
-                                            C.c_void_p(idx.data_ptr()), None, C.c_void_p(stream.cuda_stream)))
-
-    def timed(fn, steps, warmup):
+    def timed(fn, steps, warmup, stage_events=False):
         for _ in range(warmup):
             fn()
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
         ms = []
+        if stage_events:  # kernel-stage CUDA events on the launch stream, inside the timed region
+            N.LIB.fmgp_stage_times(None, None, None)
+            N.LIB.fmgp_set_stage_timing(1)
         l0 = N.LIB.fmgp_launch_count()
         for _ in range(steps):
             flush.fill_(1.0)
@@ -276,6 +274,12 @@ def main():
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
         launches = N.LIB.fmgp_launch_count() - l0
+        if stage_events:
+            N.LIB.fmgp_set_stage_timing(0)
+            a, b, c = C.c_double(0), C.c_double(0), C.c_int64(0)
+            N.check(N.LIB.fmgp_stage_times(C.byref(a), C.byref(b), C.byref(c)))
+            state["stage"] = {"knn_ms_per_launch": a.value / max(c.value, 1),
+                              "solve_ms_per_launch": b.value / max(c.value, 1), "launches": c.value}
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
@@ -285,12 +289,12 @@ def main():
         return float(t.item()) / steps, ms, launches
 
     with ClockSampler(local) as clk:
-        pre_ms, pre_all, pre_launch = timed(precompute_step, args.steps, args.warmup)
+        pre_ms, pre_all, pre_launch = timed(precompute_step, args.steps, args.warmup, stage_events=True)
         pred_ms, pred_all, pred_launch = timed(predict_step, args.steps, args.warmup)
     clocks = clk.summary()
-    knn_ms = None
-    if ws == 1:
-        knn_ms, _, _ = timed(knn_step, max(1, min(3, args.steps)), 1)
+    stage = state.get("stage", {})
+    knn_ms = stage.get("knn_ms_per_launch")
+    solve_ms = stage.get("solve_ms_per_launch")
 
     value = n / (pre_ms / 1e3)
     pred_value = nt / (pred_ms / 1e3)
@@ -324,28 +328,34 @@ def main():
                "d2h_bytes_per_step": int(Sh.numel() * 4 + Ch.numel() * 8),
                "api": "fmgp_precompute (include/fmgp_b200.h), pinned host buffers"}
 
-    # roofline of the dominant kernel of the step
+    # roofline of the dominant kernel of the step: algorithmic work per launch /
+    # that kernel's average launch duration (CUDA events on its stream, above)
     pk = peaks()
     fp64 = pk["fp64"] or {}
-    solve_ms = pre_ms - knn_ms if knn_ms is not None else None
+    traffic = load_json(REPO / "profiles" / "r01" / "traffic.json") or {}
     roof = None
-    if solve_ms is not None:
+    if solve_ms is not None and knn_ms is not None:
         rows_per_rank = (n + ws - 1) // ws
         if solve_ms >= knn_ms:
             flops = solve_flops_per_row(info) * rows_per_rank
             achieved = flops / (solve_ms / 1e3) / 1e12
             peak = fp64.get("fp64_dfma_tflops")
-            roof = {"bound": "fp64", "kernel": "solve_reg_kernel (fused gather / kernel build / register-row "
-                    "jitter-Cholesky / solve, FP64 pipe)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak if peak else None, "traffic": None,
+            tr = traffic.get(f"cfg{info.cfg}", {}).get("solve")
+            roof = {"bound": "fp64", "kernel": "fused solve (gather / kernel build / jitter-Cholesky / solve, "
+                    "FP64 pipe)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak if peak else None,
+                    "traffic": tr["dram_bytes_per_launch"] * rows_per_rank / tr["rows"] if tr else None,
+                    "traffic_source": tr.get("source") if tr else None,
                     "work": f"{solve_flops_per_row(info):.0f} fp64 flops per training row (SURVEY 8(d): k^3/3 + "
                             f"2k^2m + 3d k(k-1)/2; kernel evaluations not counted) x {rows_per_rank} rows",
                     "kernel_ms": solve_ms, "share_of_step": solve_ms / pre_ms,
                     "peak_source": "profiles/fp64_peak.json: measured DFMA rate on this B200 (neither HBM nor the "
                                    "tensor pipe bounds an fp64 Cholesky; MEASURED_PEAKS.json has no fp64 figure)"}
         else:
-            roof = {"bound": "fp64", "kernel": "grid_query_kernel (exact cell-grid kNN)", "achieved": None,
-                    "peak": fp64.get("fp64_tops_nonfma"), "unit": "TFLOP/s", "frac": None, "traffic": None,
+            tr = traffic.get(f"cfg{info.cfg}", {}).get("knn")
+            roof = {"bound": "fp64", "kernel": "kNN stage", "achieved": None,
+                    "peak": fp64.get("fp64_tops_nonfma"), "unit": "TFLOP/s", "frac": None,
+                    "traffic": tr["dram_bytes_per_launch"] if tr else None,
                     "kernel_ms": knn_ms, "share_of_step": knn_ms / pre_ms}
     pred_bytes = predict_bytes_per_point(info) * ((nt + ws - 1) // ws)
     pred_gbs = pred_bytes / (pred_ms / 1e3) / 1e9

@@ -228,6 +228,14 @@ int fmgp_muygps_predict(const double* X, const double* Y, int64_t n, int32_t d, 
                         int64_t* failed_row);
 
 /* ---- diagnostics ---------------------------------------------------------
+ * Stage timing for benchmarks: while enabled, every precompute call records
+ * CUDA events on its launch stream around the kNN stage (K1) and the fused
+ * solve (K2); fmgp_stage_times synchronises those events and returns the
+ * summed kernel-stage times (ms) and the number of calls since the last read. */
+void fmgp_set_stage_timing(int on);
+int fmgp_stage_times(double* knn_ms, double* solve_ms, int64_t* calls);
+
+/* ---- diagnostics (tensor-core kNN) ----------------------------------------
  * D~ (the tensor-core filter value n^_q + n^_p - 2 q^.p^ in the scaled fp16
  * space) of the first 128 x 256 (query, point) tile of the tcgen05 kNN, for
  * validating the GEMM plumbing. G_out: 128 x 256 fp32 (host). d >= 4. */

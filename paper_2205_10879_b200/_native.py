@@ -74,6 +74,8 @@ SIGNATURES: dict[str, tuple] = {
                              _d, _i32, _i32]),
     "fmgp_muygps_predict": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp, C.c_int64, C.c_int32, _kp, C.c_double,
                                       _vp, _i64]),
+    "fmgp_set_stage_timing": (None, [C.c_int]),
+    "fmgp_stage_times": (C.c_int, [_d, _d, _i64]),
     "fmgp_debug_tc_tile": (C.c_int, [_vp, C.c_int64, _vp, C.c_int64, C.c_int32, _vp]),
 }
 

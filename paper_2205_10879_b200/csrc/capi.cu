@@ -23,6 +23,16 @@ using namespace fmgp_capi;
 
 namespace {
 
+// Opt-in stage timing (fmgp_set_stage_timing): CUDA events recorded on the
+// launching stream around the kNN and fused-solve launches of each
+// precompute call, resolved after the caller's timed region.
+std::atomic<int> g_stage_timing{0};
+std::mutex g_stage_mu;
+struct StageEvents {
+  cudaEvent_t e[3];
+};
+std::vector<StageEvents> g_stage_events;
+
 int precompute_device_impl(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
                            const fmgp::KParams& kp, int32_t k, int64_t row_begin, int64_t row_end, int32_t* S_out,
                            double* C_out, int64_t* failed_row, cudaStream_t stream) {
@@ -30,6 +40,12 @@ int precompute_device_impl(const double* X, const double* Y, int64_t n, int32_t 
   if (failed_row) *failed_row = -1;
   if (nrows <= 0) return FMGP_OK;
   const int sms = num_sms_current();
+  StageEvents ev{};
+  const bool timing = g_stage_timing.load(std::memory_order_relaxed) != 0;
+  if (timing) {
+    for (auto& e : ev.e) FMGP_CUDA(cudaEventCreate(&e));
+    FMGP_CUDA(cudaEventRecord(ev.e[0], stream));
+  }
   if (k > 1) {
     FMGP_CUDA(fmgp::knn_exact(X + row_begin * d, nrows, X, n, d, k - 1, row_begin, nullptr, 1, S_out, nullptr,
                                    sms, stream));
@@ -39,7 +55,13 @@ int precompute_device_impl(const double* X, const double* Y, int64_t n, int32_t 
   DevBuf<unsigned long long> fmin;
   FMGP_CUDA(fmin.alloc(1, stream));
   FMGP_CUDA(cudaMemsetAsync(fmin.p, 0xFF, sizeof(unsigned long long), stream));
+  if (timing) FMGP_CUDA(cudaEventRecord(ev.e[1], stream));
   FMGP_CUDA(fmgp::fused_solve(X, Y, d, m, S_out, nrows, row_begin, k, kp, C_out, nullptr, fmin.p, sms, stream));
+  if (timing) {
+    FMGP_CUDA(cudaEventRecord(ev.e[2], stream));
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    g_stage_events.push_back(ev);
+  }
   unsigned long long host_min = ~0ull;
   FMGP_CUDA(cudaMemcpyAsync(&host_min, fmin.p, sizeof(host_min), cudaMemcpyDeviceToHost, stream));
   FMGP_CUDA(cudaStreamSynchronize(stream));
@@ -110,6 +132,34 @@ struct fmgp_model {
 extern "C" {
 
 int fmgp_abi_version(void) { return FMGP_ABI_VERSION; }
+
+void fmgp_set_stage_timing(int on) { g_stage_timing.store(on ? 1 : 0); }
+
+int fmgp_stage_times(double* knn_ms, double* solve_ms, int64_t* calls) {
+  std::vector<StageEvents> evs;
+  {
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    evs.swap(g_stage_events);
+  }
+  double a = 0.0, b = 0.0;
+  int rc = FMGP_OK;
+  for (auto& ev : evs) {
+    float t01 = 0.f, t12 = 0.f;
+    if (rc == FMGP_OK) {
+      cudaError_t e = cudaEventSynchronize(ev.e[2]);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&t01, ev.e[0], ev.e[1]);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&t12, ev.e[1], ev.e[2]);
+      if (e != cudaSuccess) rc = cuda_fail(e, "fmgp_stage_times");
+    }
+    a += t01;
+    b += t12;
+    for (auto& x : ev.e) cudaEventDestroy(x);
+  }
+  if (knn_ms) *knn_ms = a;
+  if (solve_ms) *solve_ms = b;
+  if (calls) *calls = static_cast<int64_t>(evs.size());
+  return rc;
+}
 const char* fmgp_last_error(void) { return g_err.c_str(); }
 int64_t fmgp_launch_count(void) { return fmgp::g_launches.load(); }
 

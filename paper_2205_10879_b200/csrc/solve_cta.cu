@@ -123,8 +123,8 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
         if (!(dg > 0.0)) {
           misc[0] = 1.0;
         } else {
-          const double l00 = sqrt(dg);
-          invd[0] = 1.0 / l00;
+          invd[0] = rsqrt(dg);
+          const double l00 = dg * invd[0];
           tri[0] = l00;
           a[0] = l00;
         }
@@ -160,8 +160,9 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
                 if (!(dacc > 0.0)) {
                   misc[0] = 1.0;
                 } else {
-                  const double ljj = sqrt(dacc);
-                  invd[j + 1] = 1.0 / ljj;
+                  const double inv = rsqrt(dacc);
+                  const double ljj = dacc * inv;
+                  invd[j + 1] = inv;
                   tri[ro_c(tid) + tid] = ljj;
                   a[j + 1] = ljj;
                 }

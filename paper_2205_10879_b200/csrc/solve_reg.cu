@@ -217,8 +217,8 @@ __device__ bool factor_reg(double* A, double* dinv, double* colbuf, int lane) {
     const double mine = j < 32 ? s0 : s1;
     const double piv = __shfl_sync(0xffffffffu, mine, j & 31);
     if (!(piv > 0.0)) return false;
-    const double ljj = sqrt(piv);
-    const double inv = 1.0 / ljj;
+    const double inv = rsqrt(piv);  // 1/L_jj and L_jj = piv/L_jj from one reciprocal square root
+    const double ljj = piv * inv;
     if (j < Sh::kN0) {
       if (has0 && r0 >= j) {
         const double v = r0 == j ? ljj : s0 * inv;
