@@ -357,6 +357,8 @@ def main():
                     "peak": fp64.get("fp64_tops_nonfma"), "unit": "TFLOP/s", "frac": None,
                     "traffic": tr["dram_bytes_per_launch"] if tr else None,
                     "kernel_ms": knn_ms, "share_of_step": knn_ms / pre_ms}
+    tr_pred = traffic.get(f"cfg{info.cfg}", {}).get("predict")
+    pred_traffic = tr_pred["dram_bytes_per_launch"] * ((nt + ws - 1) // ws) / tr_pred["points"] if tr_pred else None
     pred_bytes = predict_bytes_per_point(info) * ((nt + ws - 1) // ws)
     pred_gbs = pred_bytes / (pred_ms / 1e3) / 1e9
 
@@ -371,7 +373,7 @@ def main():
                     "roofline": {"bound": "hbm", "achieved": pred_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                                  "frac": pred_gbs / pk["hbm_gbs"], "peak_source": pk["hbm_src"],
                                  "work": f"{predict_bytes_per_point(info)} B per test point (SURVEY §8(d)); the "
-                                         "stage also runs the grid 1-NN", "traffic": None},
+                                         "stage also runs the grid 1-NN", "traffic": pred_traffic},
                     "gpu_launches": pred_launch},
         "stages_ms": {"knn": knn_ms, "solve": solve_ms, "precompute": pre_ms, "predict": pred_ms},
         "e2e": e2e,

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -43,6 +44,19 @@ inline int require_device() {
   if (e != cudaSuccess || n < 1)
     return fail(FMGP_ECUDA, std::string("no usable CUDA device (") + cudaGetErrorString(e) +
                                 "); the FastMuyGPs B200 path has no CPU fallback");
+  // Stage scratch comes from the stream-ordered allocator; keep freed blocks in
+  // the device's default pool (release threshold = max) so repeated calls do not
+  // re-map tens of MB on the host while the GPU waits.
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev < 64 && !(configured.load() & (1ull << dev))) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    configured.fetch_or(1ull << dev);
+  }
   return FMGP_OK;
 }
 

@@ -5,28 +5,30 @@
 // :254-287 query_knn, :351-366 nearest).
 //
 // Data path
-//   prep      x^ = fp16(s (x - mu)) row-major, zero-padded to DP = 64*KB
-//             columns (one 128-byte swizzle row per 64 dims); n^ = ||x^||^2 (fp32).
-//             mu = mean of the reference points, s = 2^e so max |x^| ~ 2^14
-//             (exact scaling, no fp16 subnormals in practice).
-//   GEMM      per CTA one 128-query tile (TMEM lanes) x a stream of 256-point
-//             tiles (TMEM columns): tcgen05.mma.cta_group::1.kind::f16,
-//             M=128 N=256 K=16, fp32 accumulators in TMEM (two 256-column
-//             buffers, 512 columns), A/B staged by TMA (SWIZZLE_128B, 4 stages).
-//   filter    D~ = n^_q + n^_p - 2 G~ (fp32) approximates s^2 D (D = exact key):
+//   prep      x^ = fp16(s (x - mu)) row-major, zero-padded to DP = 64*KB columns
+//             (one 128-byte swizzle row per 64 dims), mu = mean of the points,
+//             s = 2^e the largest power of two with max|x^| <= 2^14 and
+//             max_p ||p^||^2 <= 2^16. Three spare columns carry the point norm:
+//             points hold the fp16 hi/mid/lo split of -||p^||^2/2, queries hold 1,
+//             so the GEMM yields g = q^.p^ - n^_p/2 and v = -2g = D~ - n^_q directly.
+//   GEMM      per CTA one 128-query tile (TMEM lanes) x a stream of 128-point
+//             tiles (TMEM columns): tcgen05.mma.cta_group::1.kind::f16, M=N=128,
+//             K=16, fp32 accumulators in TMEM (4 buffers of 128 columns); TMA
+//             (SWIZZLE_128B) feeds a resident query tile + 3 point stages when
+//             DP == 64, else 2 stages of (query, point) k-blocks.
+//   filter    D~ = n^_q + v approximates s^2 D (D = exact key):
 //             |D~ - s^2 D| <= E(D) = 2 eta s sqrt(D) + eta^2 + eps with
 //             eta_q = 2^-11 (||q^|| + max||p^||)(1+1e-3) + 2^-24 sqrt(DP) (fp16 input
-//             rounding, subnormals included) and eps_q = (DP+8) 2^-22 (n^_q + max n^_p)
-//             (fp32 accumulation even with truncating adds, and the combination).
-//   epilogue  per query a shared-memory list, sorted by D~, that keeps every point
-//             with D~ <= W = T~ + 2 E(T~) (T~ = kk-th smallest D~ in the list): any
-//             point of the exact top-kk satisfies this at every moment, so it is
-//             never dropped. No fp64 work during the scan.
-//   recheck   at the end of a query tile each list entry (kk + a few) gets its
-//             exact fp64 key from the original coordinates; the exact top-kk by
-//             (key, index) is selected — the reference's order. A list that
-//             would overflow its capacity flags the query, which is then redone
-//             by the exact fp64 brute-force kernel.
+//             rounding, subnormals included) and eps_q = (2 DP + 32) 2^-22
+//             (n^_q + max n^_p)(1+1e-3) + 2^-20 (fp32 accumulation of the dot and
+//             norm terms even with truncating adds, the norm split, n^_q in fp32).
+//   epilogue  per query a max-heap of the kk smallest v plus a buffer of the points
+//             with v <= W - n^_q, W = T~ + 2 E(T~) (T~ = heap root + n^_q): every
+//             point of the exact top-kk is in heap u buffer at all times. Per
+//             32-column chunk one max over g decides whether any lane needs it.
+//   recheck   tc_recheck_kernel: exact fp64 keys of heap u buffer from the original
+//             coordinates, top-kk by (key, index) — the reference's order. A
+//             buffer that would overflow flags its query for the fp64 brute force.
 // Roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
 // issuer (one elected lane), warps 2-5 epilogue (thread = TMEM lane = query).
 #include <cuda.h>
@@ -111,7 +113,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, i
         : "r"(su32(bar)), "r"(phase)
         : "memory");
     if (ok) return;
-    if (mode == 1) __nanosleep(64);
+    if (mode == 1) __nanosleep(200);
   }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -185,29 +187,67 @@ __global__ void maxabs_kernel(const double* __restrict__ A, int64_t n, int d, co
   if ((threadIdx.x & 31) == 0) atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
-// x^ rows (fp16, DP wide) and n^ = ||x^||^2; also max ||x^|| into pmax (as bits).
+// max_p ||p - mu||^2 (as bits) for the norm-range part of the scale.
+__global__ void rownorm_kernel(const double* __restrict__ A, int64_t n, int d, const double* __restrict__ sums,
+                               int64_t np, unsigned long long* __restrict__ bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  double m = 0.0;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    double acc = 0.0;
+    for (int t = lane; t < d; t += 32) {
+      const double v = A[i * d + t] - sums[t] / static_cast<double>(np);
+      acc += v * v;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    m = fmax(m, acc);
+  }
+  if (lane == 0) atomicMax(bits, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+__device__ __forceinline__ double tc_scale(const unsigned long long* bits) {
+  const double maxabs = __longlong_as_double(static_cast<long long>(bits[0]));
+  const double maxn2 = __longlong_as_double(static_cast<long long>(bits[2]));
+  double s = maxabs > 0.0 ? exp2(floor(log2(16384.0 / maxabs))) : 1.0;
+  if (maxn2 > 0.0) s = fmin(s, exp2(floor(0.5 * log2(65536.0 / maxn2))));
+  return s;
+}
+
+// x^ rows (fp16, DP wide) and n^ = ||x^||^2 (fp32, queries); points also get the
+// fp16 split of -n^/2 in columns d..d+2 and max ||x^|| into pmax (as bits),
+// queries get 1 in those columns.
 __global__ void convert_kernel(const double* __restrict__ A, int64_t n, int d, int DP, const double* __restrict__ sums,
-                               int64_t np, const unsigned long long* __restrict__ maxbits, __half* __restrict__ H,
-                               float* __restrict__ norms, unsigned long long* __restrict__ pmax_bits) {
-  const double maxabs = __longlong_as_double(static_cast<long long>(*maxbits));
-  const double s = maxabs > 0.0 ? exp2(floor(log2(16384.0 / maxabs))) : 1.0;
+                               int64_t np, const unsigned long long* __restrict__ bits, int is_point,
+                               __half* __restrict__ H, float* __restrict__ norms,
+                               unsigned long long* __restrict__ pmax_bits) {
+  const double s = tc_scale(bits);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t i = warp; i < n; i += nwarps) {
     double acc = 0.0;
     for (int t = lane; t < DP; t += 32) {
-      __half h = __float2half_rn(0.0f);
       if (t < d) {
-        h = __double2half((A[i * d + t] - sums[t] / static_cast<double>(np)) * s);
+        const __half h = __double2half((A[i * d + t] - sums[t] / static_cast<double>(np)) * s);
         const double v = static_cast<double>(__half2float(h));
         acc += v * v;
+        H[i * DP + t] = h;
+      } else if (t >= d + 3 || !is_point) {
+        H[i * DP + t] = __float2half_rn(t < d + 3 ? 1.0f : 0.0f);
       }
-      H[i * DP + t] = h;
     }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (is_point && lane < 3) {  // -acc/2 = c1 + c2 + c3 (+ < 2^-33 relative)
+      const double v = -0.5 * acc;
+      const __half c1 = __double2half(v);
+      const double r1 = v - static_cast<double>(__half2float(c1));
+      const __half c2 = __double2half(r1);
+      const __half c3 = __double2half(r1 - static_cast<double>(__half2float(c2)));
+      H[i * DP + d + lane] = lane == 0 ? c1 : (lane == 1 ? c2 : c3);
+    }
     if (lane == 0) {
-      norms[i] = static_cast<float>(acc);
+      if (norms) norms[i] = static_cast<float>(acc);
       if (pmax_bits) atomicMax(pmax_bits, static_cast<unsigned long long>(__double_as_longlong(sqrt(acc))));
     }
   }
@@ -254,8 +294,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   const int nst = ares ? kBStagesRes : kStages;
   float* lk = reinterpret_cast<float*>(slots + 4 * kABytes);  // [cap][128] candidate D~ (column = query)
   int32_t* li = reinterpret_cast<int32_t*>(lk + a.cap * kBM);   // [cap][128] candidate index
-  float* pn_stage = reinterpret_cast<float*>(li + a.cap * kBM);      // [4 warps][kBN]
-  float* scratch = pn_stage + 4 * kBN;                                // [4 warps][32 lanes][kScrStride]
+  float* scratch = reinterpret_cast<float*>(li + a.cap * kBM);       // [4 warps][32 lanes][kScrStride]
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 4 * 32 * kScrStride);
   uint64_t* empty = full + kBStagesRes;
   uint64_t* tfull = empty + kBStagesRes;  // kTBufs TMEM buffers
@@ -374,25 +413,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     const int row = quarter * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
     const double pmax = __longlong_as_double(static_cast<long long>(*a.pmax_bits));
-    float* pns = pn_stage + (warp - 2) * kBN;          // this warp's copy of the tile's point norms
     float* scr = scratch + ((warp - 2) * 32 + lane) * kScrStride;  // this lane's hot-chunk values
     float* mk = lk + row;    // this query's column of the candidate list (stride kBM)
     int32_t* mi = li + row;
     int buf = 0;
     uint32_t tphase = 0;
-    float pnext[kBN / 32];  // norms of the next point tile
-#pragma unroll
-    for (int ch = 0; ch < kBN / 32; ++ch) {
-      const int64_t j = ch * 32 + lane;
-      pnext[ch] = j < a.np ? __ldg(a.pn + j) : __int_as_float(0x7fffffff);
-    }
     for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
       const int64_t q = qt * kBM + row;
       const bool valid = q < a.nq;
       const double nq_hat = valid ? static_cast<double>(a.qn[q]) : 0.0;
       const float nqf = static_cast<float>(nq_hat);
       const double eta = 4.8828125e-4 * (sqrt(nq_hat) + pmax) * 1.001 + 5.9604644775390625e-8 * sqrt(double(a.DP));
-      const double eps = (a.DP + 8) * 2.384185791015625e-7 * (nq_hat + pmax * pmax);
+      const double eps = (2 * a.DP + 32) * 2.384185791015625e-7 * (nq_hat + pmax * pmax) * 1.001 + 9.5367431640625e-7;
       const int64_t excl = a.excl != nullptr ? (valid ? a.excl[q] : -1)
                                              : (a.self_offset >= 0 ? q + a.self_offset : -1);
       // Candidate state (shared memory, column `row`, stride kBM):
@@ -410,24 +442,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       float root = INFINITY;
       const int64_t pt_end = a.debug_G ? 1 : npt;
       for (int64_t pt = 0; pt < pt_end; ++pt) {
-        // point norms of this tile (prefetched into registers during the previous
-        // tile), staged in this warp's smem slice and read back as float4
-        // broadcasts; points past np are NaN (never admitted, ignored by fminf)
-        __syncwarp();
-#pragma unroll
-        for (int ch = 0; ch < kBN / 32; ++ch) pns[ch * 32 + lane] = pnext[ch];
-        __syncwarp();
-        {
-          const int64_t nxt = pt + 1 < pt_end ? pt + 1 : 0;  // next tile (or tile 0 of the next query tile)
-#pragma unroll
-          for (int ch = 0; ch < kBN / 32; ++ch) {
-            const int64_t j = nxt * kBN + ch * 32 + lane;
-            pnext[ch] = j < a.np ? __ldg(a.pn + j) : __int_as_float(0x7fffffff);
-          }
-        }
         mbar_wait(&tfull[buf], tphase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + lane_addr + static_cast<uint32_t>(buf * kBN);
+        const bool tail = (pt + 1) * kBN > a.np;  // columns past np hold TMA zero fill
 #pragma unroll
         for (int h = 0; h < kBN / 64; ++h) {
           // two 32-column chunks per TMEM round trip
@@ -441,42 +459,39 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             const int ch = 2 * h + u;
             uint32_t(&r)[32] = rr[u];
             const int64_t j0 = pt * kBN + ch * 32;
+            if (tail) {  // NaN: never admitted, ignored by the max
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                if (j0 + c >= a.np) r[c] = 0x7fffffffu;
+            }
             if (a.debug_G) {
               if (qt == 0)
                 for (int c = 0; c < 32; ++c)
                   a.debug_G[row * 256 + ch * 32 + c] =
-                      j0 + c < a.np ? nqf + fmaf(-2.0f, __uint_as_float(r[c]), pns[ch * 32 + c]) : 0.0f;
+                      j0 + c < a.np ? fmaf(-2.0f, __uint_as_float(r[c]), nqf) : 0.0f;
               continue;
             }
-            // v_c = D~ - n^_q; a chunk with nothing under the window (for any lane) is skipped
-            float m0 = INFINITY, m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;
+            // g_c = q^.p^ - n^_p/2 straight from TMEM; a chunk whose max g is below
+            // -win/2 (for every lane) has nothing under the window
+            const float gthr = -0.5f * win;  // v <= win  <=>  g >= -win/2 (exact scaling)
+            float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              const float4 p4 = *reinterpret_cast<const float4*>(pns + ch * 32 + 4 * c4);
-              const float v0 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 0]), p4.x);
-              const float v1 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 1]), p4.y);
-              const float v2 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 2]), p4.z);
-              const float v3 = fmaf(-2.0f, __uint_as_float(r[4 * c4 + 3]), p4.w);
-              r[4 * c4 + 0] = __float_as_uint(v0);
-              r[4 * c4 + 1] = __float_as_uint(v1);
-              r[4 * c4 + 2] = __float_as_uint(v2);
-              r[4 * c4 + 3] = __float_as_uint(v3);
-              m0 = fminf(m0, v0);
-              m1 = fminf(m1, v1);
-              m2 = fminf(m2, v2);
-              m3 = fminf(m3, v3);
+            for (int c = 0; c < 32; c += 4) {
+              m0 = fmaxf(m0, fmaxf(__uint_as_float(r[c]), __uint_as_float(r[c + 1])));
+              m1 = fmaxf(m1, fmaxf(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])));
             }
-            const float vmin = fminf(fminf(m0, m1), fminf(m2, m3));
-            if (!__any_sync(0xffffffffu, vmin <= win)) continue;
-            // hot chunk: per-lane bit mask of admissible columns; values parked in this
+            if (!__any_sync(0xffffffffu, fmaxf(m0, m1) >= gthr)) continue;
+            // hot chunk: per-lane bit mask of admissible columns; v = -2g parked in this
             // lane's scratch row so the admission loop visits only the set bits
             uint32_t mask = 0;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) mask |= (__uint_as_float(r[c]) <= win ? 1u : 0u) << c;
+            for (int c = 0; c < 32; ++c) mask |= (__uint_as_float(r[c]) >= gthr ? 1u : 0u) << c;
             if (mask == 0) continue;
 #pragma unroll
             for (int c4 = 0; c4 < 8; ++c4)
-              *reinterpret_cast<uint4*>(scr + 4 * c4) = make_uint4(r[4 * c4], r[4 * c4 + 1], r[4 * c4 + 2], r[4 * c4 + 3]);
+              *reinterpret_cast<float4*>(scr + 4 * c4) =
+                  make_float4(-2.0f * __uint_as_float(r[4 * c4]), -2.0f * __uint_as_float(r[4 * c4 + 1]),
+                              -2.0f * __uint_as_float(r[4 * c4 + 2]), -2.0f * __uint_as_float(r[4 * c4 + 3]));
             while (mask != 0) {
               const int c = __ffs(mask) - 1;
               mask &= mask - 1;
@@ -702,33 +717,34 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
                    const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
                    cudaStream_t s, float* debug_G) {
   if (nq <= 0) return cudaSuccess;
-  const int KB = (d + kBK - 1) / kBK;
+  const int KB = (d + 3 + kBK - 1) / kBK;  // + 3 columns for the point-norm split
   const int DP = KB * kBK;
   const int cap = std::min(kCapMax, ((kk + 29 + 3) / 4) * 4);
   __half *Qh = nullptr, *Ph = nullptr;
   float *qn = nullptr, *pn = nullptr;
   double* sums = nullptr;
   int32_t *cand = nullptr, *ccount = nullptr, *ovf = nullptr;
-  unsigned long long* bits = nullptr;  // [0] maxabs, [1] pmax
+  unsigned long long* bits = nullptr;  // [0] maxabs, [1] pmax, [2] max ||p - mu||^2
   cudaError_t err = cudaMallocAsync(&Qh, sizeof(__half) * nq * DP, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&Ph, sizeof(__half) * np * DP, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&qn, sizeof(float) * nq, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&pn, sizeof(float) * np, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&sums, sizeof(double) * d, s);
-  if (err == cudaSuccess) err = cudaMallocAsync(&bits, sizeof(unsigned long long) * 2, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&bits, sizeof(unsigned long long) * 3, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&cand, sizeof(int32_t) * nq * cap, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&ccount, sizeof(int32_t) * nq, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&ovf, sizeof(int32_t) * (nq + 1), s);
   if (err != cudaSuccess) return err;
   cudaMemsetAsync(sums, 0, sizeof(double) * d, s);
-  cudaMemsetAsync(bits, 0, sizeof(unsigned long long) * 2, s);
+  cudaMemsetAsync(bits, 0, sizeof(unsigned long long) * 3, s);
   cudaMemsetAsync(ovf, 0, sizeof(int32_t), s);
   mean_kernel<<<dim3(256, (d + 255) / 256), 256, 0, s>>>(P, np, d, sums);
   maxabs_kernel<<<g1(np * d), 256, 0, s>>>(P, np, d, sums, np, bits);
   if (Q != P) maxabs_kernel<<<g1(nq * d), 256, 0, s>>>(Q, nq, d, sums, np, bits);
-  convert_kernel<<<g1(np * 32), 256, 0, s>>>(P, np, d, DP, sums, np, bits, Ph, pn, bits + 1);
-  convert_kernel<<<g1(nq * 32), 256, 0, s>>>(Q, nq, d, DP, sums, np, bits, Qh, qn, nullptr);
-  note_launches(Q != P ? 5 : 4);
+  rownorm_kernel<<<g1(np * 32), 256, 0, s>>>(P, np, d, sums, np, bits + 2);
+  convert_kernel<<<g1(np * 32), 256, 0, s>>>(P, np, d, DP, sums, np, bits, 1, Ph, pn, bits + 1);
+  convert_kernel<<<g1(nq * 32), 256, 0, s>>>(Q, nq, d, DP, sums, np, bits, 0, Qh, qn, nullptr);
+  note_launches(Q != P ? 6 : 5);
 
   CUtensorMap mq, mp;
   if (!make_map(&mq, Qh, nq, DP, kBM) || !make_map(&mp, Ph, np, DP, kBN)) return cudaErrorInvalidValue;
@@ -764,7 +780,7 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.pmax_bits = bits + 1;
   a.debug_G = debug_G;
   const size_t smem = 1024 + kStages * kStageBytes + static_cast<size_t>(cap) * kBM * 8 +
-                      sizeof(float) * 4 * (kBN + 32 * kScrStride) + 256;
+                      sizeof(float) * 4 * 32 * kScrStride + 256;
   err = cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   const int64_t nqt = (nq + kBM - 1) / kBM;

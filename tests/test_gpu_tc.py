@@ -1,9 +1,10 @@
 """GPU: the tcgen05 (tensor-core) exact kNN used for d >= 4 (kk <= 99).
 
-1. Plumbing: the filter value D~ = n^_q + n^_p - 2 q^.p^ of the first 128x256
-   tile, produced by TMA -> tcgen05.mma -> TMEM -> tcgen05.ld, equals the same
-   quantity computed on the host from the same fp16-rounded operands (to fp32
-   accumulation accuracy).
+1. Plumbing: the filter value D~ = n^_q - 2 (q^.p^ - n^_p/2) of the first
+   128x256 tile (the point norm enters the GEMM through three fp16 split
+   columns), produced by TMA -> tcgen05.mma -> TMEM -> tcgen05.ld, equals
+   n^_q + n^_p - 2 q^.p^ computed on the host from the same fp16-rounded
+   operands (to fp32 accumulation accuracy).
 2. Exactness: indices and keys equal the oracle's for several d (one and many
    64-wide k-blocks, ragged tails), k up to 100, ties/duplicates and row shards.
 """
@@ -16,9 +17,13 @@ pytestmark = pytest.mark.gpu
 
 
 def host_filter_tile(Q, P):
+    # prep of knn_tc.cu: s = 2^e with max|x^| <= 2^14 and max ||p^||^2 <= 2^16;
+    # the GEMM folds -n^_p/2 in through three fp16 columns, so the device value
+    # is D~ = n^_q - 2 (q^.p^ - n^_p/2)
     mu = P.mean(axis=0)
     maxabs = max(np.abs(P - mu).max(), np.abs(Q - mu).max())
-    s = 2.0 ** np.floor(np.log2(16384.0 / maxabs))
+    maxn2 = ((P - mu) ** 2).sum(1).max()
+    s = min(2.0 ** np.floor(np.log2(16384.0 / maxabs)), 2.0 ** np.floor(0.5 * np.log2(65536.0 / maxn2)))
     qh = ((Q[:128] - mu) * s).astype(np.float16).astype(np.float64)
     ph = ((P[:256] - mu) * s).astype(np.float16).astype(np.float64)
     nq = (qh ** 2).sum(1)
