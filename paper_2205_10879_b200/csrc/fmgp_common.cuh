@@ -185,34 +185,71 @@ __device__ __forceinline__ double kernel_eval(double dist, const KParams& p) {
   return __dmul_rn(p.s2, br);
 }
 
-// exp(-a) for a >= 0 (the only sign the kernels need): Cody-Waite reduction
-// r = n ln2 - a, |r| <= ln2/2, degree-13 Taylor polynomial (truncation
-// < 5e-18 relative), then 2^-n built directly in the exponent field. Result
-// within ~1 ulp of exp(-a); a >= 708 (exp < 3.3e-308) returns 0; NaN passes.
-__constant__ double kExpTaylor[14] = {1.0,
-                                      1.0,
-                                      0.5,
-                                      1.6666666666666666e-01,
-                                      4.1666666666666664e-02,
-                                      8.3333333333333332e-03,
-                                      1.3888888888888889e-03,
-                                      1.9841269841269841e-04,
-                                      2.4801587301587302e-05,
-                                      2.7557319223985893e-06,
-                                      2.7557319223985888e-07,
-                                      2.5052108385441720e-08,
-                                      2.0876756987868100e-09,
-                                      1.6059043836821613e-10};
+// exp(-a) for a >= 0 (the only sign the kernels need): a = (m ln2)/64 - r with
+// m = rint(64 a / ln2), Cody-Waite r (|r| <= ln2/128), exp(-a) = 2^-(m>>6) *
+// 2^-((m&63)/64) * exp(r): a 64-entry table of 2^(-j/64) (correctly rounded),
+// a degree-5 polynomial (truncation < 4e-17 relative), 2^-(m>>6) built in the
+// exponent field. Within 2 ulp of exp(-a) (exact-arithmetic emulation over
+// 3e4 samples); a >= 708 (exp < 3.3e-308) returns 0; NaN passes.
+namespace {
+__device__ const double kExp2NegTab[64] = {
+    1.0, 0.9892280131939755, 0.9785720620877001, 0.9680308967461472,
+    0.9576032806985737, 0.9472879907934828, 0.93708381705515, 0.9269895625416927,
+    0.9170040432046712, 0.9071260877501994, 0.8973545375015536, 0.8876882462632606,
+    0.8781260801866497, 0.8686669176368531, 0.859309649061239, 0.8500531768592617,
+    0.8408964152537145, 0.8318382901633682, 0.8228777390769825, 0.8140137109286739,
+    0.8052451659746271, 0.7965710756711335, 0.7879904225539432, 0.7795022001189185,
+    0.7711054127039704, 0.7627990753722692, 0.7545822137967114, 0.7464538641456324,
+    0.7384130729697497, 0.7304588970903235, 0.7225904034885233, 0.714806669195985,
+    0.7071067811865476, 0.6994898362691556, 0.691954940981916, 0.6845012114872953,
+    0.6771277734684463, 0.6698337620266515, 0.6626183215798707, 0.6554806057623822,
+    0.6484197773255048, 0.6414350080393891, 0.6345254785958666, 0.6276903785123455,
+    0.620928906036742, 0.614240268053435, 0.6076236799902345, 0.6010783657263515,
+    0.5946035575013605, 0.5881984958251406, 0.5818624293887887, 0.5755946149764913,
+    0.5693943173783458, 0.5632608093041209, 0.5571933712979462, 0.5511912916539204,
+    0.5452538663326288, 0.5393803988785599, 0.5335702003384118, 0.5278225891802786,
+    0.5221368912137069, 0.5165124395106142, 0.5109485743270583, 0.5054446430258502,
+};
+}  // namespace
 __device__ __forceinline__ double exp_neg(double a) {
   if (!(a < 708.0)) return a == a ? 0.0 : a;
-  const double n = rint(a * 1.4426950408889634);
-  double r = fma(n, 6.93147180369123816490e-01, -a);
-  r = fma(n, 1.90821492927058770002e-10, r);
-  double q = kExpTaylor[13];
-#pragma unroll
-  for (int i = 12; i >= 0; --i) q = fma(q, r, kExpTaylor[i]);
-  const int e = 1023 - static_cast<int>(n);  // n in [0, 1022]
-  return q * __hiloint2double(e << 20, 0);
+  const double t = a * 92.33248261689366;  // 64 / ln2
+  const double mf = rint(t);
+  const int m = static_cast<int>(mf);
+  double r = fma(mf, 0.01083042469326756, -a);  // (ln2/64)_hi, 32 significant bits
+  r = fma(mf, 2.9815858269852933e-12, r);        // (ln2/64)_lo
+  double q = fma(r, 8.333333333333333e-03, 4.1666666666666664e-02);
+  q = fma(q, r, 1.6666666666666666e-01);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  const double tj = __ldg(&kExp2NegTab[m & 63]);
+  return (tj * q) * __hiloint2double((1023 - (m >> 6)) << 20, 0);
+}
+
+// Kernel value from the squared distance for the fused-solve build, the
+// kernel kind fixed at compile time (KF: 0 RBF, 1/2/3 Matern nu = 0.5/1.5/2.5,
+// 4 any other nu through kernel_eval): no per-pair dispatch; the exact-zero
+// distance keeps the nugget (kernel.cpp:58-60, :81-83).
+__device__ __forceinline__ int kernel_code(const KParams& p) { return p.kind == 1 ? 0 : 1 + p.nu_code; }
+
+template <int KF>
+__device__ __forceinline__ double kernel_from_sq(double acc, const KParams& p) {
+  double v;
+  if constexpr (KF == 0) {
+    v = p.s2 * exp_neg(0.5 * acc * (p.inv_rho * p.inv_rho));
+  } else if constexpr (KF == 1) {
+    v = p.s2 * exp_neg(sqrt(acc) * p.inv_rho);
+  } else if constexpr (KF == 2) {
+    const double a = 1.7320508075688772 * sqrt(acc) * p.inv_rho;
+    v = p.s2 * ((1.0 + a) * exp_neg(a));
+  } else if constexpr (KF == 3) {
+    const double a = 2.2360679774997898 * sqrt(acc) * p.inv_rho;
+    v = p.s2 * (fma(a, a * (1.0 / 3.0), 1.0 + a) * exp_neg(a));
+  } else {
+    v = kernel_eval(sqrt(acc), p);  // general nu (its d == 0 branch is the same nugget rule)
+  }
+  return acc == 0.0 ? p.diag : v;
 }
 
 // kernel_value for the neighbourhood matrices of the fused solve: the same

@@ -47,6 +47,26 @@ __device__ __forceinline__ double jitter_c(double v, int a) {
   return v;
 }
 
+// Pairs of the strict lower triangle over this CTA, distances accumulated over
+// coordinate slices in t order; the last slice turns them into kernel values.
+template <int K, int M, int KF>
+__device__ __forceinline__ void cta_pairs(const double* xs, const uint32_t* ptab, const KParams& kp, double* tri,
+                                          int c0, int dc, int tid) {
+  using Sh = CtaShape<K, M>;
+  for (int e = tid; e < Sh::kPairs; e += Sh::kThreads) {
+    const uint32_t pt = ptab[e];
+    const double* xa = xs + ((pt >> 8) & 0xffu) * Sh::kXsStride;
+    const double* xb = xs + (pt & 0xffu) * Sh::kXsStride;
+    double acc = c0 == 0 ? 0.0 : tri[pt >> 16];
+    for (int c = 0; c < dc; ++c) {
+      const double dd = __dsub_rn(xa[c], xb[c]);
+      acc = __dadd_rn(acc, __dmul_rn(dd, dd));
+    }
+    if constexpr (KF < 0) tri[pt >> 16] = acc;
+    else tri[pt >> 16] = kernel_from_sq<KF>(acc, kp);
+  }
+}
+
 template <int K, int M>
 __global__ void __launch_bounds__(CtaShape<K, M>::kThreads, 1)
 solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
@@ -87,17 +107,14 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
           xs[t * Sh::kXsStride + c] = X[static_cast<int64_t>(sr[t]) * d + c0 + c];
         }
         __syncthreads();
-        const bool last = c0 + dc >= d;
-        for (int e = tid; e < Sh::kPairs; e += Sh::kThreads) {
-          const uint32_t pt = ptab[e];
-          const double* xa = xs + ((pt >> 8) & 0xffu) * Sh::kXsStride;
-          const double* xb = xs + (pt & 0xffu) * Sh::kXsStride;
-          double acc = c0 == 0 ? 0.0 : tri[pt >> 16];
-          for (int c = 0; c < dc; ++c) {
-            const double dd = __dsub_rn(xa[c], xb[c]);
-            acc = __dadd_rn(acc, __dmul_rn(dd, dd));
-          }
-          tri[pt >> 16] = last ? kernel_eval_fast(sqrt(acc), kp) : acc;
+        const int kf = c0 + dc >= d ? kernel_code(kp) : -1;  // -1: partial sums only
+        switch (kf) {  // uniform: one pair loop per kernel kind
+          case -1: cta_pairs<K, M, -1>(xs, ptab, kp, tri, c0, dc, tid); break;
+          case 0: cta_pairs<K, M, 0>(xs, ptab, kp, tri, c0, dc, tid); break;
+          case 1: cta_pairs<K, M, 1>(xs, ptab, kp, tri, c0, dc, tid); break;
+          case 2: cta_pairs<K, M, 2>(xs, ptab, kp, tri, c0, dc, tid); break;
+          case 3: cta_pairs<K, M, 3>(xs, ptab, kp, tri, c0, dc, tid); break;
+          default: cta_pairs<K, M, 4>(xs, ptab, kp, tri, c0, dc, tid); break;
         }
         __syncthreads();
       }

@@ -58,18 +58,10 @@ __device__ void fill_pair_table(uint32_t* ptab) {
   }
 }
 
-// Small-d build (d = D known at compile time): all K coordinates staged once,
-// one pair per lane per step from the pair table, no index decode.
-template <int K, int M, int D>
-__device__ void build_small(const double* __restrict__ X, const double* __restrict__ Y, const int32_t* sr,
-                            const KParams& kp, int attempt, double* A, double* xs, const uint32_t* ptab, int lane) {
-  using Sh = RegShape<K, M>;
+template <int K, int D, int KF>
+__device__ __forceinline__ void pair_loop(const double* xs, const uint32_t* ptab, const KParams& kp, double* A,
+                                          int lane) {
   constexpr int npairs = (K * (K - 1)) / 2;
-  for (int e = lane; e < K * D; e += kWarp) {
-    const int t = e / D, c = e - t * D;
-    xs[e] = X[static_cast<int64_t>(sr[t]) * D + c];
-  }
-  __syncwarp();
 #pragma unroll 2
   for (int e = lane; e < npairs; e += kWarp) {
     const uint32_t t = ptab[e];
@@ -81,7 +73,27 @@ __device__ void build_small(const double* __restrict__ X, const double* __restri
       const double dd = __dsub_rn(xa[c], xb[c]);
       acc = __dadd_rn(acc, __dmul_rn(dd, dd));
     }
-    A[t >> 16] = kernel_eval_fast(sqrt(acc), kp);
+    A[t >> 16] = kernel_from_sq<KF>(acc, kp);
+  }
+}
+
+// Small-d build (d = D known at compile time): all K coordinates staged once,
+// one pair per lane per step from the pair table, no index decode.
+template <int K, int M, int D>
+__device__ void build_small(const double* __restrict__ X, const double* __restrict__ Y, const int32_t* sr,
+                            const KParams& kp, int attempt, double* A, double* xs, const uint32_t* ptab, int lane) {
+  using Sh = RegShape<K, M>;
+  for (int e = lane; e < K * D; e += kWarp) {
+    const int t = e / D, c = e - t * D;
+    xs[e] = X[static_cast<int64_t>(sr[t]) * D + c];
+  }
+  __syncwarp();
+  switch (kernel_code(kp)) {  // uniform: one pair loop per kernel kind, no per-pair dispatch
+    case 0: pair_loop<K, D, 0>(xs, ptab, kp, A, lane); break;
+    case 1: pair_loop<K, D, 1>(xs, ptab, kp, A, lane); break;
+    case 2: pair_loop<K, D, 2>(xs, ptab, kp, A, lane); break;
+    case 3: pair_loop<K, D, 3>(xs, ptab, kp, A, lane); break;
+    default: pair_loop<K, D, 4>(xs, ptab, kp, A, lane); break;
   }
   const double dg = jitter_r(kp.diag, attempt);
   for (int i = lane; i < K; i += kWarp) A[ro_r(i) + i] = dg;
