@@ -144,7 +144,7 @@ struct WarpSmem {
 
 __host__ __device__ __forceinline__ size_t per_warp_doubles(int k, int dchunk, int m) {
   const size_t aug = static_cast<size_t>(ro(k)) + static_cast<size_t>(m) * ((k + 1) & ~1);
-  const size_t n = aug + k + static_cast<size_t>(k) * dchunk + (k + 1) / 2 + 2;
+  const size_t n = aug + k + static_cast<size_t>(k) * (dchunk | 1) + (k + 1) / 2 + 2;
   return (n + 1) & ~static_cast<size_t>(1);  // even: every warp's A stays 16-byte aligned
 }
 
@@ -153,7 +153,7 @@ __device__ __forceinline__ WarpSmem carve(double* smem, int warp, int k, int dch
   w.A = smem + warp * per_warp_doubles(k, dchunk, m);
   w.dinv = w.A + ro(k) + static_cast<size_t>(m) * ((k + 1) & ~1);
   w.xs = w.dinv + k;
-  w.sr = reinterpret_cast<int32_t*>(w.xs + static_cast<size_t>(k) * dchunk);
+  w.sr = reinterpret_cast<int32_t*>(w.xs + static_cast<size_t>(k) * (dchunk | 1));
   return w;
 }
 
@@ -175,9 +175,10 @@ __device__ void build_aug(const double* __restrict__ X, const double* __restrict
   const int npairs = (k * (k - 1)) / 2;
   for (int c0 = 0; c0 < d; c0 += dchunk) {
     const int dc = min(dchunk, d - c0);
+    const int ds = dc | 1;  // odd row stride: lanes reading different rows hit different banks
     for (int e = lane; e < k * dc; e += kWarp) {
       const int t = e / dc, c = e - t * dc;
-      xs[t * dc + c] = X[static_cast<int64_t>(sr[t]) * d + c0 + c];
+      xs[t * ds + c] = X[static_cast<int64_t>(sr[t]) * d + c0 + c];
     }
     __syncwarp();
     const bool last = c0 + dc >= d;
@@ -185,8 +186,8 @@ __device__ void build_aug(const double* __restrict__ X, const double* __restrict
     pair_of(lane, i, p);
     int rowi = ro(i);
     for (int e = lane; e < npairs; e += kWarp) {
-      const double* xa = xs + i * dc;
-      const double* xb = xs + p * dc;
+      const double* xa = xs + i * ds;
+      const double* xb = xs + p * ds;
       double acc = c0 == 0 ? 0.0 : A[rowi + p];
       for (int c = 0; c < dc; ++c) {
         const double diff = __dsub_rn(xa[c], xb[c]);

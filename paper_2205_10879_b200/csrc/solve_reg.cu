@@ -36,8 +36,9 @@ struct RegShape {
   static constexpr int kN0 = K < 32 ? K : 32;          // slot-0 row entries kept (row l <= 31)
   static constexpr bool kTwo = kRows > 32;             // does slot 1 (row l + 32) exist?
   static constexpr int kDch = 16;                      // coordinate slice width staged per pass
+  static constexpr int kXsStride = kDch + 1;           // odd row stride: lanes on different rows hit different banks
   static constexpr int kCol = (K + 2) & ~1;            // colbuf (even: 16-byte aligned pairs)
-  static constexpr int kPerWarp = ((kAug + ((K + 1) & ~1) /*dinv*/ + kCol + kDch * K /*xs*/ + (K + 1) / 2 + 2) + 1) & ~1;
+  static constexpr int kPerWarp = ((kAug + ((K + 1) & ~1) /*dinv*/ + kCol + kXsStride * K /*xs*/ + (K + 1) / 2 + 2) + 1) & ~1;
   static constexpr int kTabDoubles = ((K * (K - 1) / 2 + 3) / 4) * 2;  // pair table (uint32), 16 B granules
   __host__ __device__ static constexpr int row_off(int i) { return i < K ? ro_r(i) : ro_r(K) + (i - K) * kRw; }
 };
@@ -114,7 +115,7 @@ __device__ void build_reg(const double* __restrict__ X, const double* __restrict
     const int dc = min(dchunk, d - c0);
     for (int e = lane; e < K * dc; e += kWarp) {
       const int t = e / dc, c = e - t * dc;
-      xs[t * dc + c] = X[static_cast<int64_t>(sr[t]) * d + c0 + c];
+      xs[t * Sh::kXsStride + c] = X[static_cast<int64_t>(sr[t]) * d + c0 + c];
     }
     __syncwarp();
     const bool last = c0 + dc >= d;
@@ -133,10 +134,10 @@ __device__ void build_reg(const double* __restrict__ X, const double* __restrict
     }
     for (int e = lane; e < npairs; e += 2 * kWarp) {
       const bool hb = e + kWarp < npairs;
-      const double* xa = xs + ia * dc;
-      const double* xa2 = xs + pa * dc;
-      const double* xb = xs + (hb ? ib : ia) * dc;
-      const double* xb2 = xs + (hb ? pb : pa) * dc;
+      const double* xa = xs + ia * Sh::kXsStride;
+      const double* xa2 = xs + pa * Sh::kXsStride;
+      const double* xb = xs + (hb ? ib : ia) * Sh::kXsStride;
+      const double* xb2 = xs + (hb ? pb : pa) * Sh::kXsStride;
       const int offa = ro_r(ia) + pa;
       const int offb = ro_r(hb ? ib : ia) + (hb ? pb : pa);
       double acca = c0 == 0 ? 0.0 : A[offa];
@@ -302,7 +303,7 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
   double* dinv = A + Sh::kAug;
   double* colbuf = dinv + ((K + 1) & ~1);
   double* xs = colbuf + Sh::kCol;
-  int32_t* sr = reinterpret_cast<int32_t*>(xs + Sh::kDch * K);
+  int32_t* sr = reinterpret_cast<int32_t*>(xs + Sh::kXsStride * K);
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * warps + warp; r < nrows;
        r += static_cast<int64_t>(gridDim.x) * warps) {
     for (int t = lane; t < K; t += kWarp) sr[t] = S[r * K + t];
