@@ -227,6 +227,27 @@ __device__ __forceinline__ double exp_neg(double a) {
   return (tj * q) * __hiloint2double((1023 - (m >> 6)) << 20, 0);
 }
 
+// exp(-a) for finite a >= 0 on the kernel-matrix build path: the same
+// reduction and table as exp_neg, branch-free (a clamped to 708: results
+// below 3.3e-308 are returned as exp(-708) instead of a smaller value or 0),
+// polynomial coefficients in the constant bank.
+__constant__ double kExpPoly[8] = {8.333333333333333e-03, 4.1666666666666664e-02, 1.6666666666666666e-01, 0.5,
+                                   92.33248261689366, 0.01083042469326756, 2.9815858269852933e-12, 708.0};
+__device__ __forceinline__ double exp_neg_fin(double a) {
+  a = fmin(a, kExpPoly[7]);
+  const double mf = rint(a * kExpPoly[4]);
+  const int m = static_cast<int>(mf);
+  double r = fma(mf, kExpPoly[5], -a);
+  r = fma(mf, kExpPoly[6], r);
+  double q = fma(r, kExpPoly[0], kExpPoly[1]);
+  q = fma(q, r, kExpPoly[2]);
+  q = fma(q, r, kExpPoly[3]);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  const double tj = __ldg(&kExp2NegTab[m & 63]);
+  return (tj * q) * __hiloint2double((1023 - (m >> 6)) << 20, 0);
+}
+
 // Kernel value from the squared distance for the fused-solve build, the
 // kernel kind fixed at compile time (KF: 0 RBF, 1/2/3 Matern nu = 0.5/1.5/2.5,
 // 4 any other nu through kernel_eval): no per-pair dispatch; the exact-zero
@@ -237,15 +258,15 @@ template <int KF>
 __device__ __forceinline__ double kernel_from_sq(double acc, const KParams& p) {
   double v;
   if constexpr (KF == 0) {
-    v = p.s2 * exp_neg(0.5 * acc * (p.inv_rho * p.inv_rho));
+    v = p.s2 * exp_neg_fin(0.5 * acc * (p.inv_rho * p.inv_rho));
   } else if constexpr (KF == 1) {
-    v = p.s2 * exp_neg(sqrt(acc) * p.inv_rho);
+    v = p.s2 * exp_neg_fin(sqrt(acc) * p.inv_rho);
   } else if constexpr (KF == 2) {
     const double a = 1.7320508075688772 * sqrt(acc) * p.inv_rho;
-    v = p.s2 * ((1.0 + a) * exp_neg(a));
+    v = p.s2 * ((1.0 + a) * exp_neg_fin(a));
   } else if constexpr (KF == 3) {
     const double a = 2.2360679774997898 * sqrt(acc) * p.inv_rho;
-    v = p.s2 * (fma(a, a * (1.0 / 3.0), 1.0 + a) * exp_neg(a));
+    v = p.s2 * (fma(a, a * (1.0 / 3.0), 1.0 + a) * exp_neg_fin(a));
   } else {
     v = kernel_eval(sqrt(acc), p);  // general nu (its d == 0 branch is the same nugget rule)
   }

@@ -36,9 +36,13 @@ struct RegShape {
   static constexpr int kN0 = K < 32 ? K : 32;          // slot-0 row entries kept (row l <= 31)
   static constexpr bool kTwo = kRows > 32;             // does slot 1 (row l + 32) exist?
   static constexpr int kDch = 16;                      // coordinate slice width staged per pass
-  static constexpr int kXsStride = kDch + 1;           // odd row stride: lanes on different rows hit different banks
+  static constexpr int kXsStride = kDch + 2;           // = 2 mod 4 doubles: conflict-light 128-bit row loads
   static constexpr int kCol = (K + 2) & ~1;            // colbuf (even: 16-byte aligned pairs)
-  static constexpr int kPerWarp = ((kAug + ((K + 1) & ~1) /*dinv*/ + kCol + kXsStride * K /*xs*/ + (K + 1) / 2 + 2) + 1) & ~1;
+  // xs holds K x D coordinates for the small-d build (D > 0), K x kXsStride slices otherwise
+  __host__ __device__ static constexpr int xs_doubles(int D) { return D > 0 ? ((K * D + 1) & ~1) : kXsStride * K; }
+  __host__ __device__ static constexpr int per_warp(int D) {
+    return ((kAug + ((K + 1) & ~1) /*dinv*/ + kCol + xs_doubles(D) + (K + 1) / 2 + 2) + 1) & ~1;
+  }
   static constexpr int kTabDoubles = ((K * (K - 1) / 2 + 3) / 4) * 2;  // pair table (uint32), 16 B granules
   __host__ __device__ static constexpr int row_off(int i) { return i < K ? ro_r(i) : ro_r(K) + (i - K) * kRw; }
 };
@@ -142,11 +146,22 @@ __device__ void build_reg(const double* __restrict__ X, const double* __restrict
       const int offb = ro_r(hb ? ib : ia) + (hb ? pb : pa);
       double acca = c0 == 0 ? 0.0 : A[offa];
       double accb = c0 == 0 ? 0.0 : A[offb];
-      for (int c = 0; c < dc; ++c) {
-        const double da = __dsub_rn(xa[c], xa2[c]);
-        const double db = __dsub_rn(xb[c], xb2[c]);
-        acca = __dadd_rn(acca, __dmul_rn(da, da));
-        accb = __dadd_rn(accb, __dmul_rn(db, db));
+      int c = 0;
+      for (; c + 1 < dc; c += 2) {  // t-ordered, fused multiply-add (matrix entries within ~1 ulp)
+        const double2 ua = *reinterpret_cast<const double2*>(xa + c);
+        const double2 wa = *reinterpret_cast<const double2*>(xa2 + c);
+        const double2 ub = *reinterpret_cast<const double2*>(xb + c);
+        const double2 wb = *reinterpret_cast<const double2*>(xb2 + c);
+        const double da0 = ua.x - wa.x, da1 = ua.y - wa.y, db0 = ub.x - wb.x, db1 = ub.y - wb.y;
+        acca = fma(da0, da0, acca);
+        accb = fma(db0, db0, accb);
+        acca = fma(da1, da1, acca);
+        accb = fma(db1, db1, accb);
+      }
+      if (c < dc) {
+        const double da = xa[c] - xa2[c], db = xb[c] - xb2[c];
+        acca = fma(da, da, acca);
+        accb = fma(db, db, accb);
       }
       if (last) {
         const double va = kernel_eval_fast(sqrt(acca), kp);
@@ -193,40 +208,68 @@ __device__ bool factor_reg(double* A, double* dinv, double* colbuf, int lane) {
   const bool has1 = Sh::kTwo && r1 < kRows;
   double a0[Sh::kN0];
   double a1[Sh::kTwo ? K : 1];
+  // Slot-1 entries p >= 32 are loaded only when column 32 starts (they are
+  // still the original values in shared memory then): their registers reuse
+  // the dead slot-0 rows, which keeps the peak register count down.
+  const double* R1 = A + Sh::row_off(has1 ? r1 : 0);
   {
     const double* R0 = A + Sh::row_off(has0 ? r0 : 0);
 #pragma unroll
     for (int p = 0; p < Sh::kN0; ++p) a0[p] = (has0 && (p <= r0 || r0 >= K)) ? R0[p] : 0.0;
     if constexpr (Sh::kTwo) {
-      const double* R1 = A + Sh::row_off(has1 ? r1 : 0);
 #pragma unroll
-      for (int p = 0; p < K; ++p) a1[p] = (has1 && (p <= r1 || r1 >= K)) ? R1[p] : 0.0;
+      for (int p = 0; p < Sh::kN0; ++p) a1[p] = (has1 && (p <= r1 || r1 >= K)) ? R1[p] : 0.0;
     }
   }
 #pragma unroll
   for (int j = 0; j < K; ++j) {
+    if constexpr (Sh::kTwo) {
+      if (j == Sh::kN0) {
+#pragma unroll
+        for (int p = Sh::kN0; p < K; ++p) a1[p] = (has1 && (p <= r1 || r1 >= K)) ? R1[p] : 0.0;
+      }
+    }
     const double* Lj = A + ro_r(j);  // pivot row j (entries < j are final)
-    double s0a = 0.0, s0b = 0.0, s1a = 0.0, s1b = 0.0;
+    // four independent accumulators per row slot (DFMA latency chains of j/4)
+    double s0a = 0.0, s0b = 0.0, s0c = 0.0, s0d = 0.0, s1a = 0.0, s1b = 0.0, s1c = 0.0, s1d = 0.0;
     if (j < Sh::kN0) s0a = a0[j < Sh::kN0 ? j : 0];
     if constexpr (Sh::kTwo) s1a = a1[j];
 #pragma unroll
-    for (int p = 0; p + 1 < j; p += 2) {
+    for (int p = 0; p + 3 < j; p += 4) {
       const double2 l = *reinterpret_cast<const double2*>(Lj + p);
+      const double2 m = *reinterpret_cast<const double2*>(Lj + p + 2);
       if (j < Sh::kN0) {
         s0a = fma(-a0[p], l.x, s0a);
         s0b = fma(-a0[p + 1], l.y, s0b);
+        s0c = fma(-a0[p + 2], m.x, s0c);
+        s0d = fma(-a0[p + 3], m.y, s0d);
       }
       if constexpr (Sh::kTwo) {
         s1a = fma(-a1[p], l.x, s1a);
         s1b = fma(-a1[p + 1], l.y, s1b);
+        s1c = fma(-a1[p + 2], m.x, s1c);
+        s1d = fma(-a1[p + 3], m.y, s1d);
       }
     }
-    if (j & 1) {
-      const double l = Lj[j - 1];
-      if (j < Sh::kN0) s0a = fma(-a0[j - 1], l, s0a);
-      if constexpr (Sh::kTwo) s1a = fma(-a1[j - 1], l, s1a);
+    {  // up to three leftover columns (j is a compile-time constant here)
+      const int p0 = j & ~3;
+      if ((j & 3) >= 1) {
+        const double l = Lj[p0];
+        if (j < Sh::kN0) s0a = fma(-a0[p0 < Sh::kN0 ? p0 : 0], l, s0a);
+        if constexpr (Sh::kTwo) s1a = fma(-a1[p0], l, s1a);
+      }
+      if ((j & 3) >= 2) {
+        const double l = Lj[p0 + 1];
+        if (j < Sh::kN0) s0b = fma(-a0[(p0 + 1) < Sh::kN0 ? p0 + 1 : 0], l, s0b);
+        if constexpr (Sh::kTwo) s1b = fma(-a1[p0 + 1], l, s1b);
+      }
+      if ((j & 3) >= 3) {
+        const double l = Lj[p0 + 2];
+        if (j < Sh::kN0) s0c = fma(-a0[(p0 + 2) < Sh::kN0 ? p0 + 2 : 0], l, s0c);
+        if constexpr (Sh::kTwo) s1c = fma(-a1[p0 + 2], l, s1c);
+      }
     }
-    const double s0 = s0a + s0b, s1 = s1a + s1b;
+    const double s0 = (s0a + s0b) + (s0c + s0d), s1 = (s1a + s1b) + (s1c + s1d);
     const double mine = j < 32 ? s0 : s1;
     const double piv = __shfl_sync(0xffffffffu, mine, j & 31);
     if (!(piv > 0.0)) return false;
@@ -285,7 +328,7 @@ __device__ void back_solve_reg(const double* A, const double* dinv, double* __re
 }
 
 template <int K, int M, int D>
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(64, 6)
 solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
                  int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
                  unsigned long long* __restrict__ fail_min) {
@@ -299,11 +342,11 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
     fill_pair_table<K>(ptab);
     __syncthreads();
   }
-  double* A = smem + (D > 0 ? Sh::kTabDoubles : 0) + warp * Sh::kPerWarp;
+  double* A = smem + (D > 0 ? Sh::kTabDoubles : 0) + warp * Sh::per_warp(D);
   double* dinv = A + Sh::kAug;
   double* colbuf = dinv + ((K + 1) & ~1);
   double* xs = colbuf + Sh::kCol;
-  int32_t* sr = reinterpret_cast<int32_t*>(xs + Sh::kXsStride * K);
+  int32_t* sr = reinterpret_cast<int32_t*>(xs + Sh::xs_doubles(D));
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * warps + warp; r < nrows;
        r += static_cast<int64_t>(gridDim.x) * warps) {
     for (int t = lane; t < K; t += kWarp) sr[t] = S[r * K + t];
@@ -332,7 +375,7 @@ cudaError_t launch_reg(const double* X, const double* Y, int d, const int32_t* S
                        const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
   using Sh = RegShape<K, M>;
   constexpr int kWarps = 2;
-  const size_t smem = sizeof(double) * ((D > 0 ? Sh::kTabDoubles : 0) + Sh::kPerWarp * kWarps);
+  const size_t smem = sizeof(double) * ((D > 0 ? Sh::kTabDoubles : 0) + Sh::per_warp(D) * kWarps);
   cudaError_t err = cudaFuncSetAttribute(solve_reg_kernel<K, M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
