@@ -474,24 +474,35 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             // g_c = q^.p^ - n^_p/2 straight from TMEM; a chunk whose max g is below
             // -win/2 (for every lane) has nothing under the window
             const float gthr = -0.5f * win;  // v <= win  <=>  g >= -win/2 (exact scaling)
-            float m0 = -INFINITY, m1 = -INFINITY;
+            // per-lane maxima of the four 8-column sub-chunks
+            float sm[4];
 #pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-              m0 = fmaxf(m0, fmaxf(__uint_as_float(r[c]), __uint_as_float(r[c + 1])));
-              m1 = fmaxf(m1, fmaxf(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])));
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int c = 8 * q4;
+              sm[q4] = fmaxf(fmaxf(fmaxf(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
+                                   fmaxf(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]))),
+                             fmaxf(fmaxf(__uint_as_float(r[c + 4]), __uint_as_float(r[c + 5])),
+                                   fmaxf(__uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]))));
             }
-            if (!__any_sync(0xffffffffu, fmaxf(m0, m1) >= gthr)) continue;
-            // hot chunk: per-lane bit mask of admissible columns; v = -2g parked in this
-            // lane's scratch row so the admission loop visits only the set bits
+            if (!__any_sync(0xffffffffu, fmaxf(fmaxf(sm[0], sm[1]), fmaxf(sm[2], sm[3])) >= gthr)) continue;
+            // hot chunk: only the sub-chunks some lane needs get a per-lane bit mask, and
+            // their v = -2g are parked in this lane's scratch row, so the admission
+            // loop visits only the set bits
             uint32_t mask = 0;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) mask |= (__uint_as_float(r[c]) >= gthr ? 1u : 0u) << c;
-            if (mask == 0) continue;
+            for (int q4 = 0; q4 < 4; ++q4) {
+              if (!__any_sync(0xffffffffu, sm[q4] >= gthr)) continue;
+              const int c = 8 * q4;
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4)
-              *reinterpret_cast<float4*>(scr + 4 * c4) =
-                  make_float4(-2.0f * __uint_as_float(r[4 * c4]), -2.0f * __uint_as_float(r[4 * c4 + 1]),
-                              -2.0f * __uint_as_float(r[4 * c4 + 2]), -2.0f * __uint_as_float(r[4 * c4 + 3]));
+              for (int t = 0; t < 8; ++t) mask |= (__uint_as_float(r[c + t]) >= gthr ? 1u : 0u) << (c + t);
+              *reinterpret_cast<float4*>(scr + c) =
+                  make_float4(-2.0f * __uint_as_float(r[c]), -2.0f * __uint_as_float(r[c + 1]),
+                              -2.0f * __uint_as_float(r[c + 2]), -2.0f * __uint_as_float(r[c + 3]));
+              *reinterpret_cast<float4*>(scr + c + 4) =
+                  make_float4(-2.0f * __uint_as_float(r[c + 4]), -2.0f * __uint_as_float(r[c + 5]),
+                              -2.0f * __uint_as_float(r[c + 6]), -2.0f * __uint_as_float(r[c + 7]));
+            }
+            if (mask == 0) continue;
             while (mask != 0) {
               const int c = __ffs(mask) - 1;
               mask &= mask - 1;
