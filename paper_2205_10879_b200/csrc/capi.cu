@@ -4,6 +4,7 @@
 // entry point returns FMGP_ECUDA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -195,11 +196,55 @@ int fmgp_precompute(const double* X, const double* Y, int64_t n, int32_t d, int3
   FMGP_CUDA(dC.alloc(static_cast<size_t>(n) * k * m, st.s));
   FMGP_CUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * n * d, cudaMemcpyHostToDevice, st.s));
   FMGP_CUDA(cudaMemcpyAsync(dY.p, Y, sizeof(double) * n * m, cudaMemcpyHostToDevice, st.s));
-  rc = precompute_device_impl(dX.p, dY.p, n, d, m, kp, k, 0, n, dS.p, dC.p, failed_row, st.s);
-  if (rc != FMGP_OK) return rc;
-  FMGP_CUDA(cudaMemcpyAsync(S_out, dS.p, sizeof(int32_t) * n * k, cudaMemcpyDeviceToHost, st.s));
-  FMGP_CUDA(cudaMemcpyAsync(C_out, dC.p, sizeof(double) * n * k * m, cudaMemcpyDeviceToHost, st.s));
+  // K1 for all rows, then K2 in row chunks; a second stream reads S back as
+  // soon as K1 is done and each chunk's C rows as soon as that chunk is solved,
+  // so the host read-back (the largest transfer: n*k*m doubles) overlaps the solve.
+  const int sms = num_sms_current();
+  if (k > 1) {
+    FMGP_CUDA(fmgp::knn_exact(dX.p, n, dX.p, n, d, k - 1, 0, nullptr, 1, dS.p, nullptr, sms, st.s));
+  } else {
+    FMGP_CUDA(fmgp::self_rows_launch(dS.p, n, 0, st.s));
+  }
+  Stream rb_st;
+  FMGP_CUDA(rb_st.create());
+  std::vector<cudaEvent_t> evs;
+  struct EvGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EvGuard() {
+      for (auto e : v) cudaEventDestroy(e);
+    }
+  } evg{evs};
+  auto handoff = [&]() -> cudaError_t {  // rb_st waits for everything issued on st so far
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (err != cudaSuccess) return err;
+    evs.push_back(e);
+    err = cudaEventRecord(e, st.s);
+    return err == cudaSuccess ? cudaStreamWaitEvent(rb_st.s, e, 0) : err;
+  };
+  FMGP_CUDA(handoff());
+  FMGP_CUDA(cudaMemcpyAsync(S_out, dS.p, sizeof(int32_t) * n * k, cudaMemcpyDeviceToHost, rb_st.s));
+  DevBuf<unsigned long long> fmin;
+  FMGP_CUDA(fmin.alloc(1, st.s));
+  FMGP_CUDA(cudaMemsetAsync(fmin.p, 0xFF, sizeof(unsigned long long), st.s));
+  const int64_t chunk = std::max<int64_t>(int64_t(1) << 16, (n + 7) / 8);
+  for (int64_t rb = 0; rb < n; rb += chunk) {
+    const int64_t re = std::min(n, rb + chunk);
+    const size_t c0 = static_cast<size_t>(rb) * k * m, cn = static_cast<size_t>(re - rb) * k * m;
+    FMGP_CUDA(fmgp::fused_solve(dX.p, dY.p, d, m, dS.p + static_cast<size_t>(rb) * k, re - rb, rb, k, kp,
+                                dC.p + c0, nullptr, fmin.p, sms, st.s));
+    FMGP_CUDA(handoff());
+    FMGP_CUDA(cudaMemcpyAsync(C_out + c0, dC.p + c0, sizeof(double) * cn, cudaMemcpyDeviceToHost, rb_st.s));
+  }
+  unsigned long long host_min = ~0ull;
+  FMGP_CUDA(cudaMemcpyAsync(&host_min, fmin.p, sizeof(host_min), cudaMemcpyDeviceToHost, st.s));
   FMGP_CUDA(cudaStreamSynchronize(st.s));
+  FMGP_CUDA(cudaStreamSynchronize(rb_st.s));
+  if (host_min != ~0ull) {
+    if (failed_row) *failed_row = static_cast<int64_t>(host_min);
+    return fail(FMGP_ENUMERIC, "Cholesky factorization failed in precompute row " + std::to_string(host_min) +
+                                   " after jitter escalation up to 1e-6");
+  }
   return FMGP_OK;
 }
 

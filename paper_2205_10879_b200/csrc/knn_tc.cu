@@ -446,18 +446,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         tc_fence_after();
         const uint32_t tbase = tmem_base + lane_addr + static_cast<uint32_t>(buf * kBN);
         const bool tail = (pt + 1) * kBN > a.np;  // columns past np hold TMA zero fill
-#pragma unroll
-        for (int h = 0; h < kBN / 64; ++h) {
-          // two 32-column chunks per TMEM round trip
-          uint32_t rr[2][32];
+        // one 32-column chunk per iteration; the loop is deliberately not unrolled so
+        // the epilogue (chunk filter + admission + heap code) stays small in the I-cache
+#pragma unroll 1
+        for (int h = 0; h < kBN / 32; ++h) {
+          uint32_t r[32];
           __syncwarp();  // tcgen05.ld is warp-collective; the admission loop diverges
-          tmem_ld32_nw(tbase + h * 64, rr[0]);
-          tmem_ld32_nw(tbase + h * 64 + 32, rr[1]);
+          tmem_ld32_nw(tbase + h * 32, r);
           tmem_wait_ld();
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int ch = 2 * h + u;
-            uint32_t(&r)[32] = rr[u];
+          {
+            const int ch = h;
             const int64_t j0 = pt * kBN + ch * 32;
             if (tail) {  // NaN: never admitted, ignored by the max
 #pragma unroll
