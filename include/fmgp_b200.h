@@ -88,6 +88,13 @@ int fmgp_precompute(const double* X, const double* Y, int64_t n, int32_t d, int3
                     const fmgp_kernel_params* params, int32_t k, int32_t* S_out, double* C_out,
                     int64_t* failed_row);
 
+/* Row shard [row_begin, row_end) of precompute with HOST buffers (one process
+ * per GPU: each rank passes the full X, Y and receives its rows of S and C;
+ * same semantics and failure rule as fmgp_precompute, row ids global). */
+int fmgp_precompute_rows(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                         const fmgp_kernel_params* params, int32_t k, int64_t row_begin, int64_t row_end,
+                         int32_t* S_out, double* C_out, int64_t* failed_row);
+
 /* Row shard [row_begin, row_end) of precompute with everything in HBM:
  * X (n*d) and Y (n*m) are the full, replicated training set; S_out and C_out
  * hold (row_end-row_begin) rows. Reads back one status word, so it returns

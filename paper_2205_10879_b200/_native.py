@@ -41,6 +41,8 @@ SIGNATURES: dict[str, tuple] = {
     "fmgp_device_count": (C.c_int, []),
     "fmgp_validate_kernel": (C.c_int, [_kp]),
     "fmgp_precompute": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _kp, C.c_int32, _vp, _vp, _i64]),
+    "fmgp_precompute_rows": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _kp, C.c_int32, C.c_int64,
+                                       C.c_int64, _vp, _vp, _i64]),
     "fmgp_precompute_device": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _kp, C.c_int32, C.c_int64,
                                          C.c_int64, _vp, _vp, _i64, _vp]),
     "fmgp_query_knn": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, C.c_int32, _vp, _vp, _vp]),

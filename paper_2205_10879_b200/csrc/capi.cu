@@ -130,6 +130,85 @@ struct fmgp_model {
   double* mo = nullptr;
 };
 
+// Host-buffer precompute of rows [row_begin, row_end) (X, Y full; S_out and
+// C_out hold the shard's rows). K1 for the shard, then K2 in row chunks; a
+// second stream reads S back as soon as K1 is done and each chunk's C rows as
+// soon as that chunk is solved, so the host read-back (the largest transfer:
+// rows*k*m doubles) overlaps the solve.
+static int precompute_host_rows(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                                const fmgp_kernel_params* params, int32_t k, int64_t row_begin, int64_t row_end,
+                                int32_t* S_out, double* C_out, int64_t* failed_row) {
+  if (failed_row) *failed_row = -1;
+  fmgp::KParams kp;
+  int rc;
+  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
+  if (k < 1 || k > n) return fail(FMGP_EINVAL, "precompute: k out of range");
+  if ((rc = check_points(X, n, d)) != FMGP_OK) return rc;
+  if ((rc = check_solve_shape(k, d, m)) != FMGP_OK) return rc;
+  if (row_begin < 0 || row_end > n || row_begin > row_end) return fail(FMGP_EINVAL, "precompute: bad row range");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  const int64_t rows = row_end - row_begin;
+  if (rows == 0) return FMGP_OK;
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dX, dY, dC;
+  DevBuf<int32_t> dS;
+  FMGP_CUDA(dX.alloc(static_cast<size_t>(n) * d, st.s));
+  FMGP_CUDA(dY.alloc(static_cast<size_t>(n) * m, st.s));
+  FMGP_CUDA(dS.alloc(static_cast<size_t>(rows) * k, st.s));
+  FMGP_CUDA(dC.alloc(static_cast<size_t>(rows) * k * m, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * n * d, cudaMemcpyHostToDevice, st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dY.p, Y, sizeof(double) * n * m, cudaMemcpyHostToDevice, st.s));
+  const int sms = num_sms_current();
+  if (k > 1) {
+    FMGP_CUDA(fmgp::knn_exact(dX.p + static_cast<size_t>(row_begin) * d, rows, dX.p, n, d, k - 1, row_begin, nullptr,
+                              1, dS.p, nullptr, sms, st.s));
+  } else {
+    FMGP_CUDA(fmgp::self_rows_launch(dS.p, rows, row_begin, st.s));
+  }
+  Stream rb_st;
+  FMGP_CUDA(rb_st.create());
+  std::vector<cudaEvent_t> evs;
+  struct EvGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EvGuard() {
+      for (auto e : v) cudaEventDestroy(e);
+    }
+  } evg{evs};
+  auto handoff = [&]() -> cudaError_t {  // rb_st waits for everything issued on st so far
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (err != cudaSuccess) return err;
+    evs.push_back(e);
+    err = cudaEventRecord(e, st.s);
+    return err == cudaSuccess ? cudaStreamWaitEvent(rb_st.s, e, 0) : err;
+  };
+  FMGP_CUDA(handoff());
+  FMGP_CUDA(cudaMemcpyAsync(S_out, dS.p, sizeof(int32_t) * rows * k, cudaMemcpyDeviceToHost, rb_st.s));
+  DevBuf<unsigned long long> fmin;
+  FMGP_CUDA(fmin.alloc(1, st.s));
+  FMGP_CUDA(cudaMemsetAsync(fmin.p, 0xFF, sizeof(unsigned long long), st.s));
+  const int64_t chunk = std::max<int64_t>(int64_t(1) << 16, (rows + 7) / 8);
+  for (int64_t rb = 0; rb < rows; rb += chunk) {
+    const int64_t re = std::min(rows, rb + chunk);
+    const size_t c0 = static_cast<size_t>(rb) * k * m, cn = static_cast<size_t>(re - rb) * k * m;
+    FMGP_CUDA(fmgp::fused_solve(dX.p, dY.p, d, m, dS.p + static_cast<size_t>(rb) * k, re - rb, row_begin + rb, k, kp,
+                                dC.p + c0, nullptr, fmin.p, sms, st.s));
+    FMGP_CUDA(handoff());
+    FMGP_CUDA(cudaMemcpyAsync(C_out + c0, dC.p + c0, sizeof(double) * cn, cudaMemcpyDeviceToHost, rb_st.s));
+  }
+  unsigned long long host_min = ~0ull;
+  FMGP_CUDA(cudaMemcpyAsync(&host_min, fmin.p, sizeof(host_min), cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  FMGP_CUDA(cudaStreamSynchronize(rb_st.s));
+  if (host_min != ~0ull) {
+    if (failed_row) *failed_row = static_cast<int64_t>(host_min);
+    return fail(FMGP_ENUMERIC, "Cholesky factorization failed in precompute row " + std::to_string(host_min) +
+                                   " after jitter escalation up to 1e-6");
+  }
+  return FMGP_OK;
+}
+
 extern "C" {
 
 int fmgp_abi_version(void) { return FMGP_ABI_VERSION; }
@@ -178,74 +257,13 @@ int fmgp_validate_kernel(const fmgp_kernel_params* p) {
 int fmgp_precompute(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
                     const fmgp_kernel_params* params, int32_t k, int32_t* S_out, double* C_out,
                     int64_t* failed_row) {
-  if (failed_row) *failed_row = -1;
-  fmgp::KParams kp;
-  int rc;
-  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
-  if (k < 1 || k > n) return fail(FMGP_EINVAL, "precompute: k out of range");
-  if ((rc = check_points(X, n, d)) != FMGP_OK) return rc;
-  if ((rc = check_solve_shape(k, d, m)) != FMGP_OK) return rc;
-  if ((rc = require_device()) != FMGP_OK) return rc;
-  Stream st;
-  FMGP_CUDA(st.create());
-  DevBuf<double> dX, dY, dC;
-  DevBuf<int32_t> dS;
-  FMGP_CUDA(dX.alloc(static_cast<size_t>(n) * d, st.s));
-  FMGP_CUDA(dY.alloc(static_cast<size_t>(n) * m, st.s));
-  FMGP_CUDA(dS.alloc(static_cast<size_t>(n) * k, st.s));
-  FMGP_CUDA(dC.alloc(static_cast<size_t>(n) * k * m, st.s));
-  FMGP_CUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * n * d, cudaMemcpyHostToDevice, st.s));
-  FMGP_CUDA(cudaMemcpyAsync(dY.p, Y, sizeof(double) * n * m, cudaMemcpyHostToDevice, st.s));
-  // K1 for all rows, then K2 in row chunks; a second stream reads S back as
-  // soon as K1 is done and each chunk's C rows as soon as that chunk is solved,
-  // so the host read-back (the largest transfer: n*k*m doubles) overlaps the solve.
-  const int sms = num_sms_current();
-  if (k > 1) {
-    FMGP_CUDA(fmgp::knn_exact(dX.p, n, dX.p, n, d, k - 1, 0, nullptr, 1, dS.p, nullptr, sms, st.s));
-  } else {
-    FMGP_CUDA(fmgp::self_rows_launch(dS.p, n, 0, st.s));
-  }
-  Stream rb_st;
-  FMGP_CUDA(rb_st.create());
-  std::vector<cudaEvent_t> evs;
-  struct EvGuard {
-    std::vector<cudaEvent_t>& v;
-    ~EvGuard() {
-      for (auto e : v) cudaEventDestroy(e);
-    }
-  } evg{evs};
-  auto handoff = [&]() -> cudaError_t {  // rb_st waits for everything issued on st so far
-    cudaEvent_t e;
-    cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    if (err != cudaSuccess) return err;
-    evs.push_back(e);
-    err = cudaEventRecord(e, st.s);
-    return err == cudaSuccess ? cudaStreamWaitEvent(rb_st.s, e, 0) : err;
-  };
-  FMGP_CUDA(handoff());
-  FMGP_CUDA(cudaMemcpyAsync(S_out, dS.p, sizeof(int32_t) * n * k, cudaMemcpyDeviceToHost, rb_st.s));
-  DevBuf<unsigned long long> fmin;
-  FMGP_CUDA(fmin.alloc(1, st.s));
-  FMGP_CUDA(cudaMemsetAsync(fmin.p, 0xFF, sizeof(unsigned long long), st.s));
-  const int64_t chunk = std::max<int64_t>(int64_t(1) << 16, (n + 7) / 8);
-  for (int64_t rb = 0; rb < n; rb += chunk) {
-    const int64_t re = std::min(n, rb + chunk);
-    const size_t c0 = static_cast<size_t>(rb) * k * m, cn = static_cast<size_t>(re - rb) * k * m;
-    FMGP_CUDA(fmgp::fused_solve(dX.p, dY.p, d, m, dS.p + static_cast<size_t>(rb) * k, re - rb, rb, k, kp,
-                                dC.p + c0, nullptr, fmin.p, sms, st.s));
-    FMGP_CUDA(handoff());
-    FMGP_CUDA(cudaMemcpyAsync(C_out + c0, dC.p + c0, sizeof(double) * cn, cudaMemcpyDeviceToHost, rb_st.s));
-  }
-  unsigned long long host_min = ~0ull;
-  FMGP_CUDA(cudaMemcpyAsync(&host_min, fmin.p, sizeof(host_min), cudaMemcpyDeviceToHost, st.s));
-  FMGP_CUDA(cudaStreamSynchronize(st.s));
-  FMGP_CUDA(cudaStreamSynchronize(rb_st.s));
-  if (host_min != ~0ull) {
-    if (failed_row) *failed_row = static_cast<int64_t>(host_min);
-    return fail(FMGP_ENUMERIC, "Cholesky factorization failed in precompute row " + std::to_string(host_min) +
-                                   " after jitter escalation up to 1e-6");
-  }
-  return FMGP_OK;
+  return precompute_host_rows(X, Y, n, d, m, params, k, 0, n, S_out, C_out, failed_row);
+}
+
+int fmgp_precompute_rows(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                         const fmgp_kernel_params* params, int32_t k, int64_t row_begin, int64_t row_end,
+                         int32_t* S_out, double* C_out, int64_t* failed_row) {
+  return precompute_host_rows(X, Y, n, d, m, params, k, row_begin, row_end, S_out, C_out, failed_row);
 }
 
 int fmgp_precompute_device(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,

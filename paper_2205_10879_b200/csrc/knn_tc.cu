@@ -286,7 +286,9 @@ __device__ __forceinline__ float window_of(float T, double eta, double eps) {
 __global__ void __launch_bounds__(kThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmP, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (SWIZZLE_128B operands) by offsetting the __shared__ pointer itself,
+  // so the compiler keeps the shared address space (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   // 4 x 16 KB operand slots: streaming mode (KB > 1) stage s = (A slot s, B slot 2 + s);
   // resident mode (KB == 1) A = slot 0 (loaded once per query tile), B stages = slots 1..3
   uint8_t* slots = smem;

@@ -199,3 +199,25 @@ def test_solve_widths_match_oracle(fm, port, k, m):
     assert np.array_equal(model.S[rows], S_o)
     err = row_rel_err(model.C.reshape(n, k, -1)[rows], C_o)
     assert err.max() <= C_TOL, err.max()
+
+
+def test_host_row_shards_equal_full_precompute(fm):
+    # fmgp_precompute_rows (one process per GPU, host buffers): shards are
+    # bit-identical to the corresponding rows of the full precompute, for any split
+    import ctypes as C
+    from paper_2205_10879_b200 import _native as N, datagen
+    ds = datagen.generate(2, 20000, 10)
+    i = ds.info
+    n, d, k = ds.X.shape[0], ds.X.shape[1], i.k
+    p = fm.KernelParams(i.sigma, i.rho, i.nu, i.tau)
+    model = fm.precompute(fm.TrainingSet(ds.X, ds.Y, ds.mean_offset), fm.FittedParams(p, fm.KernelKind(i.kind)),
+                          fm.NeighborIndex.build(ds.X), k)
+    kp = p.c(fm.KernelKind(i.kind))
+    for b, e in [(0, 7000), (7000, 13001), (13001, 20000), (5, 6)]:
+        S = np.empty((e - b, k), dtype=np.int32)
+        Cm = np.empty((e - b, k), dtype=np.float64)
+        failed = C.c_int64(-1)
+        N.check(N.LIB.fmgp_precompute_rows(ds.X.ctypes.data, ds.Y.ctypes.data, n, d, 1, C.byref(kp), k, b, e,
+                                           S.ctypes.data, Cm.ctypes.data, C.byref(failed)), failed.value)
+        assert np.array_equal(S, model.S[b:e])
+        assert np.array_equal(Cm, model.C[b:e])
