@@ -83,7 +83,11 @@ int fmgp_validate_kernel(const fmgp_kernel_params* p);
  * reference's Exact NeighborIndex. C_out[i] = K(X_S_i, X_S_i)^-1 Y_S_i with
  * the nugget/jitter conventions of kernel.cpp:58-60 and linalg.cpp:10-31.
  * Errors: k not in [1, n] or n < 1 or d < 1 or m < 1 or non-finite X
- * (fast_predict.cpp:74-76, nn_index.cpp:56-62) -> FMGP_EINVAL. */
+ * (fast_predict.cpp:74-76, nn_index.cpp:56-62) -> FMGP_EINVAL.
+ * Multi-GPU in one process (the reference's `threads` knob):
+ * with FMGP_DEVICES="0,1,..." the rows are split contiguously over the listed
+ * devices (one host thread each); S and C are identical for any device list
+ * and a numeric failure names the lowest failing row over all shards. */
 int fmgp_precompute(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
                     const fmgp_kernel_params* params, int32_t k, int32_t* S_out, double* C_out,
                     int64_t* failed_row);

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/fmgp_b200.h"
@@ -257,7 +258,58 @@ int fmgp_validate_kernel(const fmgp_kernel_params* p) {
 int fmgp_precompute(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
                     const fmgp_kernel_params* params, int32_t k, int32_t* S_out, double* C_out,
                     int64_t* failed_row) {
-  return precompute_host_rows(X, Y, n, d, m, params, k, 0, n, S_out, C_out, failed_row);
+  // FMGP_DEVICES="0,1,..." (several entries): rows split contiguously over the
+  // listed devices, one host thread per device running the shard path into
+  // the caller's buffers. Rows are independent, so S and C are identical for
+  // any device list; a failure reports the lowest failing row over all shards.
+  std::vector<int> devs;
+  if (const char* e = std::getenv("FMGP_DEVICES")) {
+    for (const char* p = e; *p;) {
+      char* end = nullptr;
+      const long v = std::strtol(p, &end, 10);
+      if (end == p) break;
+      devs.push_back(static_cast<int>(v));
+      p = (*end == ',') ? end + 1 : end;
+    }
+  }
+  if (devs.size() <= 1) {
+    if (devs.size() == 1 && cudaSetDevice(devs[0]) != cudaSuccess)
+      return fail(FMGP_ECUDA, "FMGP_DEVICES names an unusable device");
+    return precompute_host_rows(X, Y, n, d, m, params, k, 0, n, S_out, C_out, failed_row);
+  }
+  if (failed_row) *failed_row = -1;
+  int caller_dev = 0;
+  cudaGetDevice(&caller_dev);
+  const int g = static_cast<int>(devs.size());
+  const int64_t per = (n + g - 1) / g;
+  std::vector<int> rcs(g, FMGP_OK);
+  std::vector<int64_t> fails(g, -1);
+  std::vector<std::string> msgs(g);
+  std::vector<std::thread> th;
+  for (int r = 0; r < g; ++r) {
+    th.emplace_back([&, r] {
+      const int64_t b = std::min<int64_t>(n, r * per), e = std::min<int64_t>(n, b + per);
+      if (cudaSetDevice(devs[r]) != cudaSuccess) {
+        rcs[r] = FMGP_ECUDA;
+        msgs[r] = "FMGP_DEVICES names an unusable device";
+        return;
+      }
+      rcs[r] = precompute_host_rows(X, Y, n, d, m, params, k, b, e, S_out + static_cast<size_t>(b) * k,
+                                    C_out + static_cast<size_t>(b) * k * m, &fails[r]);
+      if (rcs[r] != FMGP_OK) msgs[r] = g_err;  // thread-local error text of this worker
+    });
+  }
+  for (auto& t : th) t.join();
+  cudaSetDevice(caller_dev);
+  int worst = -1;
+  for (int r = 0; r < g; ++r) {
+    if (rcs[r] == FMGP_OK) continue;
+    // argument errors are identical on every shard; numeric failures: the lowest row
+    if (worst < 0 || (rcs[r] == FMGP_ENUMERIC && rcs[worst] == FMGP_ENUMERIC && fails[r] < fails[worst])) worst = r;
+  }
+  if (worst < 0) return FMGP_OK;
+  if (failed_row) *failed_row = fails[worst];
+  return fail(rcs[worst], msgs[worst]);
 }
 
 int fmgp_precompute_rows(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,

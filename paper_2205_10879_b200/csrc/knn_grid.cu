@@ -343,7 +343,7 @@ constexpr int kSlots = 64;  // ranges per chunk: 2 per lane (one cell-row per la
 // and Q == nullptr, or external coordinates Q[w] (no exclusion). Output row
 // index: original index - row_offset (self modes) or qout[w] / w.
 template <int D, int E>
-__global__ void __launch_bounds__(kQueryThreads, 2)
+__global__ void __launch_bounds__(kQueryThreads, 3)
 grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
                   const int32_t* __restrict__ cstart, int64_t nq, const int32_t* __restrict__ qpos,
                   const double* __restrict__ Q, const int32_t* __restrict__ qout, const int32_t* __restrict__ excl_arr,
@@ -482,7 +482,7 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
 // evaluates the k cross-covariances and the dot with C_j in the reference's
 // sequential order, without writing the 1-NN index out in between.
 template <int D>
-__global__ void __launch_bounds__(kQueryThreads)
+__global__ void __launch_bounds__(kQueryThreads, 4)
 grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
                     const int32_t* __restrict__ cstart, int64_t nq, const double* __restrict__ Qs,
                     const int32_t* __restrict__ qout, const double* __restrict__ X, const int32_t* __restrict__ S,

@@ -220,4 +220,35 @@ def test_host_row_shards_equal_full_precompute(fm):
         N.check(N.LIB.fmgp_precompute_rows(ds.X.ctypes.data, ds.Y.ctypes.data, n, d, 1, C.byref(kp), k, b, e,
                                            S.ctypes.data, Cm.ctypes.data, C.byref(failed)), failed.value)
         assert np.array_equal(S, model.S[b:e])
-        assert np.array_equal(Cm, model.C[b:e])
+        assert np.array_equal(Cm, model.C[b:e].reshape(e - b, k))
+
+
+def test_fmgp_devices_split_is_bit_identical(fm, monkeypatch):
+    # FMGP_DEVICES: rows split over a device list inside one process (here the
+    # same device listed several times, exercising the shard/join logic)
+    from paper_2205_10879_b200 import datagen
+    ds = datagen.generate(2, 30000, 10)
+    i = ds.info
+    args = (fm.TrainingSet(ds.X, ds.Y, ds.mean_offset),
+            fm.FittedParams(fm.KernelParams(i.sigma, i.rho, i.nu, i.tau), fm.KernelKind(i.kind)),
+            fm.NeighborIndex.build(ds.X), i.k)
+    monkeypatch.delenv("FMGP_DEVICES", raising=False)
+    ref = fm.precompute(*args)
+    for devs in ("0,0", "0,0,0", "0"):
+        monkeypatch.setenv("FMGP_DEVICES", devs)
+        got = fm.precompute(*args)
+        assert np.array_equal(got.S, ref.S) and np.array_equal(got.C, ref.C), devs
+    # numeric failure: the lowest failing row over all shards (as with one device)
+    X = np.zeros((90, 2))
+    X[:, 0] = np.arange(90) * 10.0
+    X[71] = X[70]
+    X[21] = X[20]
+    Y = np.arange(90, dtype=np.float64)
+    p = fm.KernelParams(1e6, 1.0, 2.5, 0.0)
+    monkeypatch.delenv("FMGP_DEVICES", raising=False)
+    with pytest.raises(fm.NumericError) as e1:
+        fm.precompute(fm.TrainingSet(X, Y, 0.0), fm.FittedParams(p, fm.KernelKind.RBF), fm.NeighborIndex.build(X), 8)
+    monkeypatch.setenv("FMGP_DEVICES", "0,0,0")
+    with pytest.raises(fm.NumericError) as e3:
+        fm.precompute(fm.TrainingSet(X, Y, 0.0), fm.FittedParams(p, fm.KernelKind.RBF), fm.NeighborIndex.build(X), 8)
+    assert e1.value.failed_row == e3.value.failed_row and str(e1.value) == str(e3.value)
