@@ -241,6 +241,67 @@ __global__ void knn_merge_kernel(const double* __restrict__ wd, const int32_t* _
   }
 }
 
+// Merge for many chunks (few queries, e.g. the tensor-core path's overflow
+// redo): one warp per query, each lane owns chunks lane, lane+32, ...; every
+// output step is a warp-wide (key, index) argmin over the lanes' heads.
+__global__ void knn_merge_warp_kernel(const double* __restrict__ wd, const int32_t* __restrict__ wi, int64_t nq,
+                                      int nchunks, int kk, int with_self, int64_t self_offset,
+                                      int32_t* __restrict__ out, double* __restrict__ out_d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t qi = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (qi >= nq) return;
+  const int width = kk + (with_self ? 1 : 0);
+  int32_t* row = out + qi * width;
+  int o = 0;
+  if (with_self) {
+    if (lane == 0) row[0] = static_cast<int32_t>(qi + self_offset);
+    o = 1;
+  }
+  constexpr int kMaxPerLane = 16;  // nchunks <= 512
+  int head[kMaxPerLane];
+#pragma unroll
+  for (int s = 0; s < kMaxPerLane; ++s) head[s] = 0;
+  for (int t = 0; t < kk; ++t) {
+    // this lane's best head
+    double bd = INFINITY;
+    int32_t bi = INT_MAX;
+    int bs = -1;
+#pragma unroll
+    for (int s = 0; s < kMaxPerLane; ++s) {
+      const int c = s * 32 + lane;
+      if (c >= nchunks || head[s] >= kk) continue;
+      const int64_t e = (qi * nchunks + c) * kk + head[s];
+      const double dd = wd[e];
+      const int32_t ii = wi[e];
+      if (bs < 0 || pair_less(dd, ii, bd, bi)) {
+        bd = dd;
+        bi = ii;
+        bs = s;
+      }
+    }
+    double wdv = bd;
+    int32_t wiv = bi;
+    for (int off = 16; off > 0; off >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, wdv, off);
+      const int32_t oi = __shfl_xor_sync(0xffffffffu, wiv, off);
+      if (pair_less(od, oi, wdv, wiv)) {
+        wdv = od;
+        wiv = oi;
+      }
+    }
+    // the winning head advances (indices are unique across chunks)
+    if (bs >= 0 && bi == wiv && bd == wdv) {
+#pragma unroll
+      for (int s = 0; s < kMaxPerLane; ++s)
+        if (s == bs) ++head[s];
+    }
+    if (lane == 0) {
+      row[o + t] = wiv;
+      if (out_d) out_d[qi * kk + t] = wdv;
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t knn_bruteforce(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk,
@@ -252,7 +313,9 @@ cudaError_t knn_bruteforce(const double* Q, int64_t nq, const double* P, int64_t
   const int64_t per_block = reg ? static_cast<int64_t>(kScanThreads) * kQPT : kTileQ;
   const int64_t qblocks = (nq + per_block - 1) / per_block;
   const int64_t want_blocks = static_cast<int64_t>(num_sms) * (reg ? 16 : 4);
-  int nchunks = static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(1, want_blocks / qblocks)));
+  // few query blocks (e.g. the tensor-core overflow redo): many point chunks, warp merge
+  const int max_chunks = qblocks * 64 < want_blocks ? 512 : 64;
+  int nchunks = static_cast<int>(std::min<int64_t>(max_chunks, std::max<int64_t>(1, want_blocks / qblocks)));
   // Every chunk must hold at least kk admissible references.
   while (nchunks > 1 && np / nchunks < 2 * (kk + 1)) --nchunks;
   const int64_t chunk_len = (np + nchunks - 1) / nchunks;
@@ -284,8 +347,12 @@ cudaError_t knn_bruteforce(const double* Q, int64_t nq, const double* P, int64_t
   note_launches(1);
   err = cudaGetLastError();
   if (err != cudaSuccess) return err;
-  knn_merge_kernel<<<static_cast<unsigned>((nq + 127) / 128), 128, 0, stream>>>(
-      wd, wi, nq, nchunks, kk, with_self, self_offset, out, out_d);
+  if (nchunks > 64)
+    knn_merge_warp_kernel<<<static_cast<unsigned>((nq * 32 + 127) / 128), 128, 0, stream>>>(
+        wd, wi, nq, nchunks, kk, with_self, self_offset, out, out_d);
+  else
+    knn_merge_kernel<<<static_cast<unsigned>((nq + 127) / 128), 128, 0, stream>>>(
+        wd, wi, nq, nchunks, kk, with_self, self_offset, out, out_d);
   note_launches(1);
   err = cudaGetLastError();
   if (err != cudaSuccess) return err;

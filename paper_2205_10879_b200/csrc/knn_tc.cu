@@ -29,8 +29,11 @@
 //   recheck   tc_recheck_kernel: exact fp64 keys of heap u buffer from the original
 //             coordinates, top-kk by (key, index) — the reference's order. A
 //             buffer that would overflow flags its query for the fp64 brute force.
-// Roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer (one elected lane), warps 2-5 epilogue (thread = TMEM lane = query).
+// Roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer (one elected
+// lane), warps 2-5 epilogue (thread = TMEM lane = query). When both candidate
+// lists fit (cap <= 64, i.e. kk <= 35), warps 6-9 form a second epilogue set:
+// each set takes half of every tile's columns with its own heap + window
+// buffer per query, and the recheck merges the two candidate sets.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
@@ -56,7 +59,7 @@ constexpr int kStages = 2;       // A+B stages when the query tile streams (KB >
 constexpr int kBStagesRes = 3;   // B-only stages when the query tile is resident (KB == 1)
 constexpr int kTBufs = 4;        // TMEM accumulator buffers (4 x 128 columns)
 constexpr int kCapMax = 128;  // candidate-list capacity per query (kk <= kCapMax - 29)
-constexpr int kThreads = 192;
+constexpr int kMaxThreads = 320;  // TMA + MMA + 4 or 8 epilogue warps (8: two column halves, lists fit twice)
 constexpr int kScrStride = 36;  // floats per lane scratch row (16 B aligned, spreads banks)
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
 constexpr uint32_t kBBytes = kBN * kBK * 2;  // 16 KB
@@ -266,6 +269,7 @@ struct TcArgs {
   const int32_t* excl;   // or per-query exclusion (nullable)
   int with_self;
   int wait_mode;         // producer-side wait (see mbar_wait_sleep)
+  int halves;            // 1: 4 epilogue warps; 2: 8 (each tile's columns split, separate lists)
   int32_t* out;          // nq x (kk + with_self)
   double* out_d;         // nq x kk (nullable)
   int32_t* cand;         // [cap][nq] candidate ids, column-major (coalesced stores)
@@ -283,7 +287,7 @@ __device__ __forceinline__ float window_of(float T, double eta, double eps) {
   return static_cast<float>((t + 2.0 * E) * 1.0001 + 1e-30);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kMaxThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmP, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B operands) by offsetting the __shared__ pointer itself,
@@ -294,10 +298,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   uint8_t* slots = smem;
   const bool ares = a.KB == 1;
   const int nst = ares ? kBStagesRes : kStages;
-  float* lk = reinterpret_cast<float*>(slots + 4 * kABytes);  // [cap][128] candidate D~ (column = query)
-  int32_t* li = reinterpret_cast<int32_t*>(lk + a.cap * kBM);   // [cap][128] candidate index
-  float* scratch = reinterpret_cast<float*>(li + a.cap * kBM);       // [4 warps][32 lanes][kScrStride]
-  uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 4 * 32 * kScrStride);
+  const int halves = a.halves;
+  float* lk = reinterpret_cast<float*>(slots + 4 * kABytes);  // [halves][cap][128] candidate v (column = query)
+  int32_t* li = reinterpret_cast<int32_t*>(lk + halves * a.cap * kBM);  // [halves][cap][128] candidate index
+  float* scratch = reinterpret_cast<float*>(li + halves * a.cap * kBM);   // [4*halves warps][32][kScrStride]
+  uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 4 * halves * 32 * kScrStride);
   uint64_t* empty = full + kBStagesRes;
   uint64_t* tfull = empty + kBStagesRes;  // kTBufs TMEM buffers
   uint64_t* tempty = tfull + kTBufs;
@@ -317,7 +322,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     }
     for (int b = 0; b < kTBufs; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 128 * halves);
     }
     mbar_init(afull, 1);
     mbar_init(aempty, 1);
@@ -412,12 +417,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   } else {
     // ---------------- epilogue: thread = TMEM lane = query row of the tile
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int ew = warp - 2;       // epilogue warp 0 .. 4*halves-1
+    const int half = ew >> 2;      // which column half of every tile (and which list set) it owns
     const int row = quarter * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
     const double pmax = __longlong_as_double(static_cast<long long>(*a.pmax_bits));
-    float* scr = scratch + ((warp - 2) * 32 + lane) * kScrStride;  // this lane's hot-chunk values
-    float* mk = lk + row;    // this query's column of the candidate list (stride kBM)
-    int32_t* mi = li + row;
+    float* scr = scratch + (ew * 32 + lane) * kScrStride;  // this lane's hot-chunk values
+    float* mk = lk + half * a.cap * kBM + row;  // this query's column of its half's list (stride kBM)
+    int32_t* mi = li + half * a.cap * kBM + row;
+    const int h0 = half * (kBN / 32) / halves, h1 = (half + 1) * (kBN / 32) / halves;  // its chunks
     int buf = 0;
     uint32_t tphase = 0;
     for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
@@ -451,7 +459,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         // one 32-column chunk per iteration; the loop is deliberately not unrolled so
         // the epilogue (chunk filter + admission + heap code) stays small in the I-cache
 #pragma unroll 1
-        for (int h = 0; h < kBN / 32; ++h) {
+        for (int h = h0; h < h1; ++h) {
           uint32_t r[32];
           __syncwarp();  // tcgen05.ld is warp-collective; the admission loop diverges
           tmem_ld32_nw(tbase + h * 32, r);
@@ -593,12 +601,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       if (over) {
         const int32_t slot = atomicAdd(a.overflow, 1);
         a.overflow[1 + slot] = static_cast<int32_t>(q);
-        a.ccount[q] = -1;
+        a.ccount[half * a.nq + q] = -1;
         continue;
       }
-      for (int t = 0; t < hn; ++t) a.cand[t * a.nq + q] = hi[t * kBM];
-      for (int t = 0; t < wn; ++t) a.cand[(hn + t) * a.nq + q] = wi_[t * kBM];
-      a.ccount[q] = hn + wn;
+      int32_t* cq = a.cand + static_cast<int64_t>(half) * a.cap * a.nq + q;  // this half's rows
+      for (int t = 0; t < hn; ++t) cq[t * a.nq] = hi[t * kBM];
+      for (int t = 0; t < wn; ++t) cq[(hn + t) * a.nq] = wi_[t * kBM];
+      a.ccount[half * a.nq + q] = hn + wn;
     }
   }
   tc_fence_before();
@@ -615,15 +624,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 // the warp; rank < kk goes straight to its output slot.
 __global__ void __launch_bounds__(256) tc_recheck_kernel(const double* __restrict__ Q, const double* __restrict__ P,
                                                           int d, int64_t nq, int kk, const int32_t* __restrict__ cand,
-                                                          const int32_t* __restrict__ ccount, int with_self,
+                                                          const int32_t* __restrict__ ccount, int halves, int cap,
+                                                          int with_self,
                                                           int64_t self_offset, int32_t* __restrict__ out,
                                                           double* __restrict__ out_d) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t q = w0; q < nq; q += nw) {
-    const int cnt = ccount[q];
-    if (cnt < 0) continue;  // overflowed: redone by the brute-force path
+    const int cnt0 = ccount[q];
+    const int cnt1 = halves == 2 ? ccount[nq + q] : 0;
+    if (cnt0 < 0 || cnt1 < 0) continue;  // overflowed: redone by the brute-force path
+    const int cnt = cnt0 + cnt1;          // <= 128 (host: halves == 2 only when 2 cap <= 128)
     const double* qx = Q + q * d;
     double key[4];
     int32_t idx[4];
@@ -633,7 +645,8 @@ __global__ void __launch_bounds__(256) tc_recheck_kernel(const double* __restric
       const int t = s * 32 + lane;
       rank[s] = 0;
       if (t < cnt) {
-        idx[s] = cand[static_cast<int64_t>(t) * nq + q];
+        const int row_c = t < cnt0 ? t : cap + (t - cnt0);  // half 1's candidates start at row cap
+        idx[s] = cand[static_cast<int64_t>(row_c) * nq + q];
         key[s] = dist_sq_dyn(qx, P + static_cast<int64_t>(idx[s]) * d, d);
       } else {
         idx[s] = INT_MAX;
@@ -731,6 +744,13 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   const int KB = (d + 3 + kBK - 1) / kBK;  // + 3 columns for the point-norm split
   const int DP = KB * kBK;
   const int cap = std::min(kCapMax, ((kk + 29 + 3) / 4) * 4);
+  // 8 epilogue warps (two column halves with separate candidate lists) when both
+  // lists fit next to the operand slots and the recheck's 128-candidate warp
+  auto smem_for = [&](int hv) {
+    return static_cast<size_t>(1024) + kStages * kStageBytes + static_cast<size_t>(hv) * cap * kBM * 8 +
+           sizeof(float) * 4 * hv * 32 * kScrStride + 256;
+  };
+  const int halves = (2 * cap <= 128 && smem_for(2) <= 232448) ? 2 : 1;
   __half *Qh = nullptr, *Ph = nullptr;
   float *qn = nullptr, *pn = nullptr;
   double* sums = nullptr;
@@ -742,8 +762,8 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   if (err == cudaSuccess) err = cudaMallocAsync(&pn, sizeof(float) * np, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&sums, sizeof(double) * d, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&bits, sizeof(unsigned long long) * 3, s);
-  if (err == cudaSuccess) err = cudaMallocAsync(&cand, sizeof(int32_t) * nq * cap, s);
-  if (err == cudaSuccess) err = cudaMallocAsync(&ccount, sizeof(int32_t) * nq, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&cand, sizeof(int32_t) * nq * cap * halves, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&ccount, sizeof(int32_t) * nq * halves, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&ovf, sizeof(int32_t) * (nq + 1), s);
   if (err != cudaSuccess) return err;
   cudaMemsetAsync(sums, 0, sizeof(double) * d, s);
@@ -771,6 +791,7 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.KB = KB;
   a.kk = kk;
   a.cap = cap;
+  a.halves = halves;
   a.self_offset = self_offset;
   a.excl = excl_arr;
   a.with_self = with_self;
@@ -790,19 +811,18 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.maxabs_bits = bits;
   a.pmax_bits = bits + 1;
   a.debug_G = debug_G;
-  const size_t smem = 1024 + kStages * kStageBytes + static_cast<size_t>(cap) * kBM * 8 +
-                      sizeof(float) * 4 * 32 * kScrStride + 256;
+  const size_t smem = smem_for(halves);
   err = cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   const int64_t nqt = (nq + kBM - 1) / kBM;
   const int grid = static_cast<int>(nqt < num_sms ? nqt : num_sms);
-  knn_tc_kernel<<<debug_G ? 1 : grid, kThreads, smem, s>>>(mq, mp, a);
+  knn_tc_kernel<<<debug_G ? 1 : grid, 64 + 128 * halves, smem, s>>>(mq, mp, a);
   note_launches(1);
   err = cudaGetLastError();
   if (err == cudaSuccess && debug_G == nullptr) {
     const int64_t blocks = (nq + 7) / 8;
     tc_recheck_kernel<<<static_cast<unsigned>(blocks < num_sms * 8 ? blocks : num_sms * 8), 256, 0, s>>>(
-        Q, P, d, nq, kk, cand, ccount, with_self, self_offset, out, out_d);
+        Q, P, d, nq, kk, cand, ccount, halves, cap, with_self, self_offset, out, out_d);
     note_launches(1);
     err = cudaGetLastError();
   }

@@ -100,3 +100,20 @@ def test_grid_matches_bruteforce_at_scale(tmp_path, cfg, n, k):
     d, i = g["self_dsq"], g["self_idx"]
     assert np.all((d[:, 1:] > d[:, :-1]) | ((d[:, 1:] == d[:, :-1]) & (i[:, 1:] > i[:, :-1])))
     assert not np.any(i == np.arange(n)[:, None])
+
+
+@pytest.mark.parametrize("d", [3, 6, 40])
+def test_bruteforce_few_queries_many_points(tmp_path, port, d):
+    # few query blocks -> up to 512 point chunks and the warp-per-query merge
+    # (the shape of the tensor-core path's overflow redo)
+    rng = np.random.default_rng(d)
+    P = rng.standard_normal((200_000, d))
+    P[7] = P[3]
+    Q = np.concatenate([rng.standard_normal((6, d)), P[3:4]])
+    cases = [(P, k, Q) for k in (1, 50, 100)]
+    got = run_dump(tmp_path, cases, brute=True, tag=f"few{d}")
+    for (P_, k, Q_), g in zip(cases, got):
+        for j in range(Q_.shape[0]):
+            idx, dsq = port.query_knn(P_, Q_[j], k)
+            assert g["ext_idx"][j].tolist() == idx.tolist(), (d, k, j)
+            assert np.array_equal(g["ext_d"][j], np.sqrt(dsq)), (d, k, j)
