@@ -31,7 +31,7 @@
 //             buffer that would overflow flags its query for the fp64 brute force.
 // Roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer (one elected
 // lane), warps 2-5 epilogue (thread = TMEM lane = query). When both candidate
-// lists fit (cap <= 64, i.e. kk <= 35), warps 6-9 form a second epilogue set:
+// lists fit (cap <= 64, i.e. kk <= 35) and DP == 64, warps 6-9 form a second epilogue set:
 // each set takes half of every tile's columns with its own heap + window
 // buffer per query, and the recheck merges the two candidate sets.
 #include <cuda.h>
@@ -750,7 +750,9 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
     return static_cast<size_t>(1024) + kStages * kStageBytes + static_cast<size_t>(hv) * cap * kBM * 8 +
            sizeof(float) * 4 * hv * 32 * kScrStride + 256;
   };
-  const int halves = (2 * cap <= 128 && smem_for(2) <= 232448) ? 2 : 1;
+  // Only when the epilogue is the bound (DP == 64: resident query tile, cheap
+  // recheck); for wide rows (KB > 1) the GEMM/TMA side and the doubled recheck dominate.
+  const int halves = (KB == 1 && 2 * cap <= 128 && smem_for(2) <= 232448) ? 2 : 1;
   __half *Qh = nullptr, *Ph = nullptr;
   float *qn = nullptr, *pn = nullptr;
   double* sums = nullptr;

@@ -59,6 +59,7 @@ __device__ __forceinline__ void cta_pairs(const double* xs, const uint32_t* ptab
     const double* xb = xs + (pt & 0xffu) * Sh::kXsStride;
     double acc = c0 == 0 ? 0.0 : tri[pt >> 16];
     int c = 0;
+#pragma unroll 4
     for (; c + 1 < dc; c += 2) {  // t-ordered, fused multiply-add (matrix entries within ~1 ulp)
       const double2 u = *reinterpret_cast<const double2*>(xa + c);
       const double2 w = *reinterpret_cast<const double2*>(xb + c);

@@ -147,6 +147,7 @@ __device__ void build_reg(const double* __restrict__ X, const double* __restrict
       double acca = c0 == 0 ? 0.0 : A[offa];
       double accb = c0 == 0 ? 0.0 : A[offb];
       int c = 0;
+#pragma unroll 4
       for (; c + 1 < dc; c += 2) {  // t-ordered, fused multiply-add (matrix entries within ~1 ulp)
         const double2 ua = *reinterpret_cast<const double2*>(xa + c);
         const double2 wa = *reinterpret_cast<const double2*>(xa2 + c);
