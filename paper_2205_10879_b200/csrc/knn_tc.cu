@@ -622,12 +622,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 // candidates with the reference's sequential difference order, then each
 // candidate's rank under (key, index) by broadcasting all candidates through
 // the warp; rank < kk goes straight to its output slot.
-__global__ void __launch_bounds__(256) tc_recheck_kernel(const double* __restrict__ Q, const double* __restrict__ P,
+constexpr int kRecheckWarps = 4;
+
+__global__ void __launch_bounds__(kRecheckWarps * 32) tc_recheck_kernel(const double* __restrict__ Q, const double* __restrict__ P,
                                                           int d, int64_t nq, int kk, const int32_t* __restrict__ cand,
                                                           const int32_t* __restrict__ ccount, int halves, int cap,
                                                           int with_self,
                                                           int64_t self_offset, int32_t* __restrict__ out,
                                                           double* __restrict__ out_d) {
+  __shared__ double rtile[kRecheckWarps * (32 * 33 + 32)];
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -647,10 +650,40 @@ __global__ void __launch_bounds__(256) tc_recheck_kernel(const double* __restric
       if (t < cnt) {
         const int row_c = t < cnt0 ? t : cap + (t - cnt0);  // half 1's candidates start at row cap
         idx[s] = cand[static_cast<int64_t>(row_c) * nq + q];
-        key[s] = dist_sq_dyn(qx, P + static_cast<int64_t>(idx[s]) * d, d);
       } else {
         idx[s] = INT_MAX;
-        key[s] = INFINITY;
+      }
+      key[s] = INFINITY;
+    }
+    if (d < 16) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        if (idx[s] != INT_MAX) key[s] = dist_sq_dyn(qx, P + static_cast<int64_t>(idx[s]) * d, d);
+    } else {
+      // wide rows: 32 candidate rows x 32 dims staged through this warp's padded
+      // tile with coalesced loads; each lane then accumulates its own candidate's
+      // key over the dims in ascending order (the reference's bit-exact key)
+      double* tl = rtile + (threadIdx.x >> 5) * (32 * 33 + 32);
+      double* qt = tl + 32 * 33;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        if (s * 32 >= cnt) break;
+        double acc = 0.0;
+        for (int c0 = 0; c0 < d; c0 += 32) {
+          const int dc = min(32, d - c0);
+          __syncwarp();
+          qt[lane] = lane < dc ? qx[c0 + lane] : 0.0;
+          for (int r = 0; r < 32; ++r) {
+            const int32_t ir = __shfl_sync(0xffffffffu, idx[s], r);
+            if (ir != INT_MAX && lane < dc) tl[r * 33 + lane] = P[static_cast<int64_t>(ir) * d + c0 + lane];
+          }
+          __syncwarp();
+          for (int c = 0; c < dc; ++c) {
+            const double e = __dsub_rn(qt[c], tl[lane * 33 + c]);
+            acc = __dadd_rn(acc, __dmul_rn(e, e));
+          }
+        }
+        if (idx[s] != INT_MAX) key[s] = acc;
       }
     }
 #pragma unroll
@@ -822,8 +855,9 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   note_launches(1);
   err = cudaGetLastError();
   if (err == cudaSuccess && debug_G == nullptr) {
-    const int64_t blocks = (nq + 7) / 8;
-    tc_recheck_kernel<<<static_cast<unsigned>(blocks < num_sms * 8 ? blocks : num_sms * 8), 256, 0, s>>>(
+    const int64_t blocks = (nq + kRecheckWarps - 1) / kRecheckWarps;
+    tc_recheck_kernel<<<static_cast<unsigned>(blocks < num_sms * 16 ? blocks : num_sms * 16), kRecheckWarps * 32, 0,
+                        s>>>(
         Q, P, d, nq, kk, cand, ccount, halves, cap, with_self, self_offset, out, out_d);
     note_launches(1);
     err = cudaGetLastError();
