@@ -189,7 +189,7 @@ static int precompute_host_rows(const double* X, const double* Y, int64_t n, int
   DevBuf<unsigned long long> fmin;
   FMGP_CUDA(fmin.alloc(1, st.s));
   FMGP_CUDA(cudaMemsetAsync(fmin.p, 0xFF, sizeof(unsigned long long), st.s));
-  const int64_t chunk = std::max<int64_t>(int64_t(1) << 16, (rows + 7) / 8);
+  const int64_t chunk = std::max<int64_t>(int64_t(1) << 15, (rows + 15) / 16);
   for (int64_t rb = 0; rb < rows; rb += chunk) {
     const int64_t re = std::min(rows, rb + chunk);
     const size_t c0 = static_cast<size_t>(rb) * k * m, cn = static_cast<size_t>(re - rb) * k * m;

@@ -262,7 +262,6 @@ struct TcArgs {
   const double* Q;       // nq x d original coordinates (fp64)
   const double* P;       // np x d
   const float* qn;       // ||q^||^2
-  const float* pn;       // ||p^||^2
   int64_t nq, np;
   int d, DP, KB, kk, cap;
   int64_t self_offset;   // exclude p == q + self_offset when >= 0
@@ -787,14 +786,13 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   // recheck); for wide rows (KB > 1) the GEMM/TMA side and the doubled recheck dominate.
   const int halves = (KB == 1 && 2 * cap <= 128 && smem_for(2) <= 232448) ? 2 : 1;
   __half *Qh = nullptr, *Ph = nullptr;
-  float *qn = nullptr, *pn = nullptr;
+  float* qn = nullptr;
   double* sums = nullptr;
   int32_t *cand = nullptr, *ccount = nullptr, *ovf = nullptr;
   unsigned long long* bits = nullptr;  // [0] maxabs, [1] pmax, [2] max ||p - mu||^2
   cudaError_t err = cudaMallocAsync(&Qh, sizeof(__half) * nq * DP, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&Ph, sizeof(__half) * np * DP, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&qn, sizeof(float) * nq, s);
-  if (err == cudaSuccess) err = cudaMallocAsync(&pn, sizeof(float) * np, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&sums, sizeof(double) * d, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&bits, sizeof(unsigned long long) * 3, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&cand, sizeof(int32_t) * nq * cap * halves, s);
@@ -808,7 +806,7 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   maxabs_kernel<<<g1(np * d), 256, 0, s>>>(P, np, d, sums, np, bits);
   if (Q != P) maxabs_kernel<<<g1(nq * d), 256, 0, s>>>(Q, nq, d, sums, np, bits);
   rownorm_kernel<<<g1(np * 32), 256, 0, s>>>(P, np, d, sums, np, bits + 2);
-  convert_kernel<<<g1(np * 32), 256, 0, s>>>(P, np, d, DP, sums, np, bits, 1, Ph, pn, bits + 1);
+  convert_kernel<<<g1(np * 32), 256, 0, s>>>(P, np, d, DP, sums, np, bits, 1, Ph, nullptr, bits + 1);
   convert_kernel<<<g1(nq * 32), 256, 0, s>>>(Q, nq, d, DP, sums, np, bits, 0, Qh, qn, nullptr);
   note_launches(Q != P ? 6 : 5);
 
@@ -818,7 +816,6 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.Q = Q;
   a.P = P;
   a.qn = qn;
-  a.pn = pn;
   a.nq = nq;
   a.np = np;
   a.d = d;
@@ -889,7 +886,7 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
         if (p) cudaFreeAsync(p, s);
     }
   }
-  for (void* p : {static_cast<void*>(Qh), static_cast<void*>(Ph), static_cast<void*>(qn), static_cast<void*>(pn),
+  for (void* p : {static_cast<void*>(Qh), static_cast<void*>(Ph), static_cast<void*>(qn),
                   static_cast<void*>(sums), static_cast<void*>(bits), static_cast<void*>(cand), static_cast<void*>(ccount),
                   static_cast<void*>(ovf)})
     cudaFreeAsync(p, s);
