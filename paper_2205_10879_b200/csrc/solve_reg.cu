@@ -33,8 +33,11 @@ struct RegShape {
   static constexpr int kRows = K + M;
   static constexpr int kRw = (K + 1) & ~1;             // padded RHS row length
   static constexpr int kAug = ro_r(K) + M * kRw;       // augmented packed size (doubles)
-  static constexpr int kN0 = K < 32 ? K : 32;          // slot-0 row entries kept (row l <= 31)
-  static constexpr bool kTwo = kRows > 32;             // does slot 1 (row l + 32) exist?
+  static constexpr bool kTwo = kRows > 32;  // two row slots per lane?
+  // Rows are paired head-to-tail: lane l owns row l (slot 0) and row kRows-1-l
+  // (slot 1), so slot 0 (the short rows) is finished after column kN0 - 1 and
+  // both slots stay busy until then; one slot: lane l owns row l.
+  static constexpr int kN0 = kTwo ? (kRows + 1) / 2 : K;  // slot-0 rows 0 .. kN0-1 (their entries < kN0)
   static constexpr int kDch = 16;                      // coordinate slice width staged per pass
   static constexpr int kXsStride = kDch + 2;           // = 2 mod 4 doubles: conflict-light 128-bit row loads
   static constexpr int kCol = (K + 2) & ~1;            // colbuf (even: 16-byte aligned pairs)
@@ -204,12 +207,12 @@ __device__ bool factor_reg(double* A, double* dinv, double* colbuf, int lane) {
   (void)colbuf;
   using Sh = RegShape<K, M>;
   constexpr int kRows = Sh::kRows;
-  const int r0 = lane, r1 = lane + 32;
-  const bool has0 = r0 < kRows;
-  const bool has1 = Sh::kTwo && r1 < kRows;
+  const int r0 = lane, r1 = kRows - 1 - lane;
+  const bool has0 = Sh::kTwo ? r0 < Sh::kN0 : r0 < kRows;
+  const bool has1 = Sh::kTwo && lane < kRows - Sh::kN0;
   double a0[Sh::kN0];
   double a1[Sh::kTwo ? K : 1];
-  // Slot-1 entries p >= 32 are loaded only when column 32 starts (they are
+  // Slot-1 entries p >= kN0 are loaded only when column kN0 starts (they are
   // still the original values in shared memory then): their registers reuse
   // the dead slot-0 rows, which keeps the peak register count down.
   const double* R1 = A + Sh::row_off(has1 ? r1 : 0);
@@ -271,8 +274,8 @@ __device__ bool factor_reg(double* A, double* dinv, double* colbuf, int lane) {
       }
     }
     const double s0 = (s0a + s0b) + (s0c + s0d), s1 = (s1a + s1b) + (s1c + s1d);
-    const double mine = j < 32 ? s0 : s1;
-    const double piv = __shfl_sync(0xffffffffu, mine, j & 31);
+    const double mine = j < Sh::kN0 ? s0 : s1;
+    const double piv = __shfl_sync(0xffffffffu, mine, j < Sh::kN0 ? j : kRows - 1 - j);
     if (!(piv > 0.0)) return false;
     const double inv = rsqrt(piv);  // 1/L_jj and L_jj = piv/L_jj from one reciprocal square root
     const double ljj = piv * inv;
@@ -329,7 +332,7 @@ __device__ void back_solve_reg(const double* A, const double* dinv, double* __re
 }
 
 template <int K, int M, int D>
-__global__ void __launch_bounds__(64, 6)
+__global__ void __launch_bounds__(64, K <= 32 ? 8 : 6)
 solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
                  int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
                  unsigned long long* __restrict__ fail_min) {
