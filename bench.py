@@ -224,7 +224,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2205_10879_b200 as fm
     from paper_2205_10879_b200 import _native as N
-    from paper_2205_10879_b200.parallel import sharded_precompute, sharded_predict
+    from paper_2205_10879_b200.parallel import overlapped_precompute, sharded_precompute, sharded_predict
     dev = torch.device("cuda", local)
 
     ds = datagen.generate(args.config, n, nt)
@@ -243,8 +243,26 @@ def main():
         fm.precompute_device(X, Y, fit, k, b, e, S, Cm, stream)
         return S, Cm
 
+    kp_c = fit.theta_hat.c(fit.kind)
+    fail_word = torch.full((1,), -1, dtype=torch.int64, device=dev)  # UINT64_MAX: no failed row
+
+    def knn_rows(b, e):  # K1 for rows [b, e): precompute's S rows
+        S = torch.empty((e - b, k), dtype=torch.int32, device=dev)
+        N.check(N.LIB.fmgp_knn_rows_device(C.c_void_p(X.data_ptr()), n, d, k, b, e, C.c_void_p(S.data_ptr()),
+                                           C.c_void_p(stream.cuda_stream)))
+        return S
+
+    def solve_rows(S_rows, row_begin, C_out):  # K2 for a chunk, asynchronous (failures -> fail_word)
+        N.check(N.LIB.fmgp_solve_rows_device(C.c_void_p(X.data_ptr()), C.c_void_p(Y.data_ptr()), n, d, m,
+                                             C.byref(kp_c), k, C.c_void_p(S_rows.data_ptr()), S_rows.shape[0],
+                                             row_begin, C.c_void_p(C_out.data_ptr()),
+                                             C.c_void_p(fail_word.data_ptr()), None, C.c_void_p(stream.cuda_stream)))
+
     def precompute_step():
-        state["S"], state["C"] = sharded_precompute(n, shard)
+        if ws == 1:
+            state["S"], state["C"] = sharded_precompute(n, shard)
+        else:  # K1 per shard; S and each C chunk all-gathered while the next chunk is solved
+            state["S"], state["C"] = overlapped_precompute(n, k, m, knn_rows, solve_rows, nchunks=4, device=dev)
 
     def predict_step():
         def pshard(b, e):
@@ -292,6 +310,8 @@ def main():
         pre_ms, pre_all, pre_launch = timed(precompute_step, args.steps, args.warmup, stage_events=True)
         pred_ms, pred_all, pred_launch = timed(predict_step, args.steps, args.warmup)
     clocks = clk.summary()
+    if int(fail_word.item()) != -1:
+        raise RuntimeError(f"precompute: Cholesky factorization failed in row {int(fail_word.item()) & ((1 << 64) - 1)}")
     stage = state.get("stage", {})
     knn_ms = stage.get("knn_ms_per_launch")
     solve_ms = stage.get("solve_ms_per_launch")

@@ -99,6 +99,25 @@ int fmgp_precompute_rows(const double* X, const double* Y, int64_t n, int32_t d,
                          const fmgp_kernel_params* params, int32_t k, int64_t row_begin, int64_t row_end,
                          int32_t* S_out, double* C_out, int64_t* failed_row);
 
+/* The neighbour stage (K1) alone, device pointers: precompute's S rows
+ * [row_begin, row_end) (S[i][0] = i, then the k-1 nearest, self excluded by
+ * index), stream-ordered, no synchronisation. */
+int fmgp_knn_rows_device(const double* X, int64_t n, int32_t d, int32_t k, int64_t row_begin, int64_t row_end,
+                         int32_t* S_out, void* stream);
+
+/* The fused solve (K2) alone, device pointers: rows [row_begin, row_begin +
+ * nrows) of C from their given neighbour rows S_rows (nrows x k, S[i][0] = i
+ * as precompute produces them). With fmgp_query_knn_device this lets a caller
+ * run K1 once for a shard and K2 in chunks (e.g. to overlap a collective with
+ * the next chunk). fail_dev == NULL: synchronises `stream` and reports a
+ * failure as FMGP_ENUMERIC (*failed_row = lowest failing row); otherwise fully
+ * asynchronous: the lowest failing row is min-combined into the device word
+ * *fail_dev (initialise it to UINT64_MAX; it stays so when every row succeeds). */
+int fmgp_solve_rows_device(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                           const fmgp_kernel_params* params, int32_t k, const int32_t* S_rows, int64_t nrows,
+                           int64_t row_begin, double* C_out, uint64_t* fail_dev, int64_t* failed_row,
+                           void* stream);
+
 /* Row shard [row_begin, row_end) of precompute with everything in HBM:
  * X (n*d) and Y (n*m) are the full, replicated training set; S_out and C_out
  * hold (row_end-row_begin) rows. Reads back one status word, so it returns

@@ -45,6 +45,9 @@ SIGNATURES: dict[str, tuple] = {
                                        C.c_int64, _vp, _vp, _i64]),
     "fmgp_precompute_device": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _kp, C.c_int32, C.c_int64,
                                          C.c_int64, _vp, _vp, _i64, _vp]),
+    "fmgp_knn_rows_device": (C.c_int, [_vp, C.c_int64, C.c_int32, C.c_int32, C.c_int64, C.c_int64, _vp, _vp]),
+    "fmgp_solve_rows_device": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _kp, C.c_int32, _vp, C.c_int64,
+                                         C.c_int64, _vp, _vp, _i64, _vp]),
     "fmgp_query_knn": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, C.c_int32, _vp, _vp, _vp]),
     "fmgp_query_knn_device": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp, C.c_int64, C.c_int32, C.c_int64, _vp,
                                         _vp, _vp]),

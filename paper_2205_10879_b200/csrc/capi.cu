@@ -334,6 +334,61 @@ int fmgp_precompute_device(const double* X, const double* Y, int64_t n, int32_t 
                                 static_cast<cudaStream_t>(stream));
 }
 
+int fmgp_knn_rows_device(const double* X, int64_t n, int32_t d, int32_t k, int64_t row_begin, int64_t row_end,
+                         int32_t* S_out, void* stream) {
+  int rc;
+  if (k < 1 || k > n) return fail(FMGP_EINVAL, "precompute: k out of range");
+  if ((rc = check_points(nullptr, n, d)) != FMGP_OK) return rc;
+  if (row_begin < 0 || row_end > n || row_begin > row_end) return fail(FMGP_EINVAL, "precompute: bad row range");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  const int64_t rows = row_end - row_begin;
+  if (rows == 0) return FMGP_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (k > 1) {
+    FMGP_CUDA(fmgp::knn_exact(X + row_begin * d, rows, X, n, d, k - 1, row_begin, nullptr, 1, S_out, nullptr,
+                              num_sms_current(), st));
+  } else {
+    FMGP_CUDA(fmgp::self_rows_launch(S_out, rows, row_begin, st));
+  }
+  return FMGP_OK;
+}
+
+int fmgp_solve_rows_device(const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                           const fmgp_kernel_params* params, int32_t k, const int32_t* S_rows, int64_t nrows,
+                           int64_t row_begin, double* C_out, uint64_t* fail_dev, int64_t* failed_row,
+                           void* stream) {
+  if (failed_row) *failed_row = -1;
+  fmgp::KParams kp;
+  int rc;
+  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
+  if (k < 1 || k > n) return fail(FMGP_EINVAL, "precompute: k out of range");
+  if ((rc = check_points(nullptr, n, d)) != FMGP_OK) return rc;
+  if ((rc = check_solve_shape(k, d, m)) != FMGP_OK) return rc;
+  if (nrows < 0 || row_begin < 0) return fail(FMGP_EINVAL, "precompute: bad row range");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  if (nrows == 0) return FMGP_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (fail_dev != nullptr) {  // asynchronous: the caller min-combines and checks the word later
+    FMGP_CUDA(fmgp::fused_solve(X, Y, d, m, S_rows, nrows, row_begin, k, kp, C_out, nullptr,
+                                reinterpret_cast<unsigned long long*>(fail_dev), num_sms_current(), st));
+    return FMGP_OK;
+  }
+  DevBuf<unsigned long long> fmin;
+  FMGP_CUDA(fmin.alloc(1, st));
+  FMGP_CUDA(cudaMemsetAsync(fmin.p, 0xFF, sizeof(unsigned long long), st));
+  FMGP_CUDA(fmgp::fused_solve(X, Y, d, m, S_rows, nrows, row_begin, k, kp, C_out, nullptr, fmin.p,
+                              num_sms_current(), st));
+  unsigned long long host_min = ~0ull;
+  FMGP_CUDA(cudaMemcpyAsync(&host_min, fmin.p, sizeof(host_min), cudaMemcpyDeviceToHost, st));
+  FMGP_CUDA(cudaStreamSynchronize(st));
+  if (host_min != ~0ull) {
+    if (failed_row) *failed_row = static_cast<int64_t>(host_min);
+    return fail(FMGP_ENUMERIC, "Cholesky factorization failed in precompute row " + std::to_string(host_min) +
+                                   " after jitter escalation up to 1e-6");
+  }
+  return FMGP_OK;
+}
+
 int fmgp_query_knn_device(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq, int32_t k,
                           int64_t self_offset, int32_t* idx_out, double* dist_sq_out, void* stream) {
   int rc;

@@ -61,6 +61,91 @@ def sharded_precompute(n: int, compute_shard: Callable[[int, int], tuple[torch.T
     return S, C
 
 
+class _Side:
+    """A side stream for collectives on CUDA tensors; a no-op on CPU (gloo tests)."""
+
+    def __init__(self, device: torch.device):
+        self.cuda = device.type == "cuda"
+        self.main = torch.cuda.current_stream(device) if self.cuda else None
+        self.side = torch.cuda.Stream(device) if self.cuda else None
+
+    def after_main(self):
+        """Context: work issued inside runs on the side stream, after everything issued so far on main."""
+        if not self.cuda:
+            return _Null()
+        self.side.wait_stream(self.main)
+        return torch.cuda.stream(self.side)
+
+    def join(self):
+        if self.cuda:
+            self.main.wait_stream(self.side)
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def overlapped_precompute(n: int, k: int, m: int, knn_rows: Callable[[int, int], torch.Tensor],
+                          solve_rows: Callable[[torch.Tensor, int, torch.Tensor], None], nchunks: int = 4,
+                          group=None, device: torch.device | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """sharded_precompute with the exchange overlapped: K1 for this rank's rows
+    (knn_rows(b, e) -> S rows), the S all-gather then runs on a side stream
+    while K2 solves the shard in `nchunks` chunks (solve_rows(S_rows, row_begin,
+    C_rows) writes C rows, stream-ordered); each chunk's C all-gather is issued
+    on the side stream as soon as the chunk is solved, so it overlaps the next
+    chunk's solve. Every rank returns the full S (n x k) and C (n x k x m),
+    bit-identical to sharded_precompute (rows are independent)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    b, e, per = shard_bounds(n, world, rank)
+    rows = e - b
+    S_loc = knn_rows(b, e)
+    dev = S_loc.device if device is None else device
+    if world == 1:
+        C_loc = torch.empty((rows, k, m), dtype=torch.float64, device=dev)
+        solve_rows(S_loc, b, C_loc)
+        return S_loc, C_loc
+    side = _Side(dev)
+    S_pad = torch.zeros((per, k), dtype=torch.int32, device=dev)
+    S_pad[:rows] = S_loc
+    S_all = torch.empty((world * per, k), dtype=torch.int32, device=dev)
+    with side.after_main():
+        _all_gather_into(S_all, S_pad, group)
+    C_pad = torch.zeros((per, k, m), dtype=torch.float64, device=dev)
+    C_all = torch.empty((world, per, k, m), dtype=torch.float64, device=dev)
+    pc = (per + nchunks - 1) // nchunks
+    staging = []
+    for lo in range(0, per, pc):
+        hi = min(per, lo + pc)
+        r_lo, r_hi = min(rows, lo), min(rows, hi)
+        if r_hi > r_lo:
+            solve_rows(S_loc[r_lo:r_hi], b + r_lo, C_pad[r_lo:r_hi])
+        g = torch.empty((world * (hi - lo), k, m), dtype=torch.float64, device=dev)
+        staging.append(g)
+        with side.after_main():
+            _all_gather_into(g, C_pad[lo:hi], group)
+            C_all[:, lo:hi].copy_(g.view(world, hi - lo, k, m))
+    side.join()
+    return S_all[:n], C_all.view(world * per, k, m)[:n]
+
+
+def _all_gather_into(out: torch.Tensor, local: torch.Tensor, group=None) -> None:
+    """out (world * rows, ...) <- the ranks' `local` (rows, ...) in rank order."""
+    local = local.contiguous()
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, local, group=group)
+    else:
+        parts = list(out.chunk(dist.get_world_size(group), 0))
+        tmp = [torch.empty_like(local) for _ in parts]
+        dist.all_gather(tmp, local, group=group)
+        for p_, t in zip(parts, tmp):
+            p_.copy_(t)
+
+
 def sharded_predict(nz: int, predict_shard: Callable[[int, int], torch.Tensor], gather: bool = False,
                     group=None) -> torch.Tensor:
     """Each rank predicts its contiguous test shard; optionally gather all means."""

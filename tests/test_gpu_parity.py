@@ -252,3 +252,61 @@ def test_fmgp_devices_split_is_bit_identical(fm, monkeypatch):
     with pytest.raises(fm.NumericError) as e3:
         fm.precompute(fm.TrainingSet(X, Y, 0.0), fm.FittedParams(p, fm.KernelKind.RBF), fm.NeighborIndex.build(X), 8)
     assert e1.value.failed_row == e3.value.failed_row and str(e1.value) == str(e3.value)
+
+
+def test_split_knn_and_chunked_async_solve_equal_precompute_device(fm):
+    # the entry points behind bench.py's overlapped multi-GPU step: K1 for a row
+    # range, then K2 in chunks with the asynchronous failure word
+    import ctypes as C
+    import torch
+    from paper_2205_10879_b200 import _native as N, datagen
+    ds = datagen.generate(5, 40000, 10)
+    i = ds.info
+    n, d, k = ds.X.shape[0], ds.X.shape[1], i.k
+    X = torch.from_numpy(ds.X).cuda()
+    Y = torch.from_numpy(ds.Y).cuda()
+    fit = fm.FittedParams(fm.KernelParams(i.sigma, i.rho, i.nu, i.tau), fm.KernelKind(i.kind))
+    kp = fit.theta_hat.c(fit.kind)
+    s = torch.cuda.current_stream()
+    b, e = 13000, 29001
+    S_ref = torch.empty((e - b, k), dtype=torch.int32, device="cuda")
+    C_ref = torch.empty((e - b, k, 1), dtype=torch.float64, device="cuda")
+    fm.precompute_device(X, Y, fit, k, b, e, S_ref, C_ref, s)
+    S = torch.empty_like(S_ref)
+    Cm = torch.full_like(C_ref, float("nan"))
+    N.check(N.LIB.fmgp_knn_rows_device(C.c_void_p(X.data_ptr()), n, d, k, b, e, C.c_void_p(S.data_ptr()),
+                                       C.c_void_p(s.cuda_stream)))
+    fail = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    for lo in range(0, e - b, 5000):
+        hi = min(e - b, lo + 5000)
+        N.check(N.LIB.fmgp_solve_rows_device(C.c_void_p(X.data_ptr()), C.c_void_p(Y.data_ptr()), n, d, 1,
+                                             C.byref(kp), k, C.c_void_p(S[lo:hi].data_ptr()), hi - lo, b + lo,
+                                             C.c_void_p(Cm[lo:hi].data_ptr()), C.c_void_p(fail.data_ptr()), None,
+                                             C.c_void_p(s.cuda_stream)))
+    torch.cuda.synchronize()
+    assert int(fail.item()) == -1
+    assert torch.equal(S, S_ref) and torch.equal(Cm, C_ref)
+    # failures: the word holds the lowest failing global row (exact duplicates, tau = 0, sigma = 1e6)
+    Xf = np.zeros((90, 2))
+    Xf[:, 0] = np.arange(90) * 10.0
+    Xf[71] = Xf[70]
+    Xf[21] = Xf[20]
+    Xt = torch.from_numpy(Xf).cuda()
+    Yt = torch.arange(90, dtype=torch.float64, device="cuda")
+    kpf = fm.KernelParams(1e6, 1.0, 2.5, 0.0).c(fm.KernelKind.RBF)
+    Sf = torch.empty((90, 8), dtype=torch.int32, device="cuda")
+    Cf = torch.empty((90, 8, 1), dtype=torch.float64, device="cuda")
+    N.check(N.LIB.fmgp_knn_rows_device(C.c_void_p(Xt.data_ptr()), 90, 2, 8, 0, 90, C.c_void_p(Sf.data_ptr()),
+                                       C.c_void_p(s.cuda_stream)))
+    fail.fill_(-1)
+    for lo in (60, 0, 30):  # out of order: the word keeps the minimum
+        N.check(N.LIB.fmgp_solve_rows_device(C.c_void_p(Xt.data_ptr()), C.c_void_p(Yt.data_ptr()), 90, 2, 1,
+                                             C.byref(kpf), 8, C.c_void_p(Sf[lo:lo + 30].data_ptr()), 30, lo,
+                                             C.c_void_p(Cf[lo:lo + 30].data_ptr()), C.c_void_p(fail.data_ptr()),
+                                             None, C.c_void_p(s.cuda_stream)))
+    torch.cuda.synchronize()
+    with pytest.raises(fm.NumericError) as ei:
+        fm.precompute(fm.TrainingSet(Xf, Yt.cpu().numpy(), 0.0),
+                      fm.FittedParams(fm.KernelParams(1e6, 1.0, 2.5, 0.0), fm.KernelKind.RBF),
+                      fm.NeighborIndex.build(Xf), 8)
+    assert int(fail.item()) == ei.value.failed_row

@@ -80,3 +80,55 @@ def test_two_rank_gloo_sharding_is_bit_identical_to_one_rank():
     S1, C1 = orc.precompute_rows(ds.X, ds.Y, i.kind, i.sigma, i.rho, i.nu, i.tau, 9)
     P1, _ = orc.predict(ds.X, S1, C1, i.kind, i.sigma, i.rho, i.nu, i.tau, ds.mean_offset, ds.Z)
     assert np.array_equal(S1, S2) and np.array_equal(C1, C2) and np.array_equal(P1, P2)
+
+
+def _overlap_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Port
+        from paper_2205_10879_b200 import datagen
+        from paper_2205_10879_b200.parallel import overlapped_precompute
+        orc = Port()
+        ds = datagen.generate(5, 301, 7)
+        i = ds.info
+        kp = (i.kind, i.sigma, i.rho, i.nu, i.tau)
+        k = 9
+
+        def knn_rows(b, e):  # K1 stand-in: the oracle's S rows
+            S, _ = orc.precompute_rows(ds.X, ds.Y, *kp, k, np.arange(b, e))
+            return torch.from_numpy(S)
+
+        def solve_rows(S_rows, row_begin, C_out):  # K2 stand-in: the oracle's C rows for those rows
+            rows = np.arange(row_begin, row_begin + S_rows.shape[0])
+            S, C = orc.precompute_rows(ds.X, ds.Y, *kp, k, rows)
+            assert np.array_equal(S, S_rows.numpy())  # the chunk got its own rows' S
+            C_out.copy_(torch.from_numpy(C))
+
+        S, C = overlapped_precompute(ds.X.shape[0], k, 1, knn_rows, solve_rows, nchunks=3)
+        if rank == 0:
+            q.put((S.numpy(), C.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_overlapped_gather_is_bit_identical_to_one_rank(world):
+    # K1 per shard, S gathered on a side stream, K2 in chunks with each chunk's C
+    # gathered while the next is solved: same tables as a single rank
+    from oracle.oracle import Port
+    from paper_2205_10879_b200 import datagen
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    S2, C2 = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ds = datagen.generate(5, 301, 7)
+    i = ds.info
+    S1, C1 = Port().precompute_rows(ds.X, ds.Y, i.kind, i.sigma, i.rho, i.nu, i.tau, 9)
+    assert np.array_equal(S1, S2) and np.array_equal(C1, C2)
