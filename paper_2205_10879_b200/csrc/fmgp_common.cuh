@@ -273,6 +273,100 @@ __device__ __forceinline__ double kernel_from_sq(double acc, const KParams& p) {
   return acc == 0.0 ? p.diag : v;
 }
 
+// Build-path arithmetic for the register solve (solve_reg.cu), branch-free:
+// the kernel-matrix entries only have to be accurate to a few ulps (the
+// coefficient tolerance is 1e-9 relative), so the special-case paths of the
+// libdevice sqrt/rsqrt are replaced by a MUFU seed plus Newton/Goldschmidt
+// refinement, and exp(-a) rounds with the 1.5*2^52 shift instead of
+// FRND/F2I and folds 2^-(m>>6) into the table value's exponent field.
+//
+// sqrt(x) for finite x >= 0: MUFU rsqrt seed (~2^-22), one Goldschmidt step
+// (~2^-43), one Newton correction of the root (< 1 ulp + rounding). x == 0
+// gives NaN (0 * inf); every caller replaces the d == 0 entry by the nugget.
+__device__ __forceinline__ double sqrt_build(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double r = x * y, h = 0.5 * y;
+  const double e = fma(-r, h, 0.5);
+  r = fma(r, e, r);
+  h = fma(h, e, h);
+  const double dd = fma(-r, r, x);
+  return fma(dd, h, r);
+}
+
+// 1/sqrt(x) for a Cholesky pivot x > 0: MUFU seed and two Newton steps
+// (quadratic: 2^-22 -> 2^-43 -> rounding). x <= 0 returns garbage; the
+// caller has already recorded the failed pivot.
+__device__ __forceinline__ double rsqrt_pivot(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double t = fma(-h * y, y, 0.5);
+  y = fma(y, t, y);
+  t = fma(-h * y, y, 0.5);
+  return fma(y, t, y);
+}
+
+// exp(-a) for a >= 0 (NaN-free): the exp_neg reduction (m = rint(64 a / ln2),
+// Cody-Waite r, degree-5 polynomial, 2^(-j/64) table) with the rounding done
+// by the 1.5*2^52 shift (m is the low word of the shifted value) and
+// 2^-(m>>6) applied as an exponent-field subtraction on the table value
+// (a <= 708 keeps the result normal). Within 2 ulp of exp(-a).
+__device__ __forceinline__ double exp_neg_build(double a) {
+  a = fmin(a, 708.0);
+  const double tm = fma(a, 92.33248261689366, 6755399441055744.0);
+  const int m = __double2loint(tm);
+  const double mf = tm - 6755399441055744.0;
+  double r = fma(mf, 0.01083042469326756, -a);
+  r = fma(mf, 2.9815858269852933e-12, r);
+  double q = fma(r, 8.333333333333333e-03, 4.1666666666666664e-02);
+  q = fma(q, r, 1.6666666666666666e-01);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  const double tj = __ldg(&kExp2NegTab[m & 63]);
+  const double sj = __hiloint2double(__double2hiint(tj) - ((m >> 6) << 20), __double2loint(tj));
+  return sj * q;
+}
+
+// Kernel value from the squared distance on the register-solve build path
+// (KF as in kernel_from_sq; `c` = the kind's distance scale: sqrt(3)/rho,
+// sqrt(5)/rho, 1/rho, or 0.5/rho^2 for RBF). d == 0 keeps the nugget.
+// General nu (GSL lnKnu path, no BASELINE config): out of line, so its
+// register demand does not set the register budget of the solve kernels.
+static __device__ __noinline__ double kernel_eval_general(double dist, const KParams& p);
+
+template <int KF>
+__device__ __forceinline__ double kernel_from_sq_build(double acc, double c, const KParams& p) {
+  double v;
+  if constexpr (KF == 0) {
+    v = p.s2 * exp_neg_build(acc * c);
+  } else if constexpr (KF == 1) {
+    v = p.s2 * exp_neg_build(sqrt_build(acc) * c);
+  } else if constexpr (KF == 2) {
+    const double a = sqrt_build(acc) * c;
+    const double e = exp_neg_build(a);
+    v = p.s2 * fma(a, e, e);
+  } else if constexpr (KF == 3) {
+    const double a = sqrt_build(acc) * c;
+    v = p.s2 * (fma(a, a * (1.0 / 3.0), 1.0 + a) * exp_neg_build(a));
+  } else {
+    v = kernel_eval_general(sqrt(acc), p);
+  }
+  return acc == 0.0 ? p.diag : v;
+}
+
+static __device__ __noinline__ double kernel_eval_general(double dist, const KParams& p) { return kernel_eval(dist, p); }
+
+template <int KF>
+__device__ __forceinline__ double kernel_scale_build(const KParams& p) {
+  if constexpr (KF == 0) return 0.5 * (p.inv_rho * p.inv_rho);
+  if constexpr (KF == 1) return p.inv_rho;
+  if constexpr (KF == 2) return 1.7320508075688772 * p.inv_rho;
+  if constexpr (KF == 3) return 2.2360679774997898 * p.inv_rho;
+  return 0.0;
+}
+
 // kernel_value for the neighbourhood matrices of the fused solve: the same
 // formulas with 1/rho multiplied instead of divided and contraction allowed.
 // The matrix entries differ from kernel_eval by at most a few ulps, far inside

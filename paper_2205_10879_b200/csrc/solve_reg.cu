@@ -4,14 +4,25 @@
 // linalg.cpp:10-36), one warp per neighbourhood.
 //
 // Why: the shared-memory left-looking kernel is bound by the LSU pipe (one
-// per-lane 64-bit load per FMA). Here lane l owns rows l and l+32 of the
-// augmented matrix [K ; Y^T] for the whole factorisation, in registers
-// (static indexing: K and M are template parameters and both loops are fully
-// unrolled). Column j needs only the pivot row L_j., which its owner writes to
-// shared memory as it is produced and every lane reads as a 128-bit
-// broadcast. The RHS rows (K .. K+M-1) ride along, so the column sweep also
-// performs the forward substitution; the backward solve then runs over the
-// shared-memory copy of L.
+// per-lane 64-bit load per FMA). Here each lane owns rows of the augmented
+// matrix [K ; Y^T] in registers (static indexing: K and M are template
+// parameters and the column loop is fully unrolled). Column j needs only the
+// pivot row L_j., which its owner writes to shared memory as it is produced
+// and every lane reads as a 128-bit broadcast. The RHS rows (K .. K+M-1) ride
+// along, so the column sweep also performs the forward substitution; the
+// backward solve then runs over the shared-memory copy of L.
+//
+// Row ownership (R = K + M rows): lane l owns row P + l (slot B) where
+// P = max(R - 32, 0), and for l < P also row l (slot A). Slot A rows finish
+// by column P - 1, so columns >= P run on one slot, and slot-B entries >= P
+// are only loaded (still the original values) when column P starts: the
+// live register set is at most max(2P, K) doubles per lane.
+//
+// Build (small d): the strict lower triangle is spread over the lanes by a
+// CTA-shared pair table; the entries use the branch-free build arithmetic of
+// fmgp_common.cuh (kernel_from_sq_build). The factorisation is branch-free:
+// a failed pivot is recorded in a flag and the jitter ladder retried after
+// the sweep (Eigen LLT semantics: success iff every pivot > 0).
 #include "fmgp_common.cuh"
 #include "fmgp_internal.h"
 
@@ -33,18 +44,16 @@ struct RegShape {
   static constexpr int kRows = K + M;
   static constexpr int kRw = (K + 1) & ~1;             // padded RHS row length
   static constexpr int kAug = ro_r(K) + M * kRw;       // augmented packed size (doubles)
-  static constexpr bool kTwo = kRows > 32;  // two row slots per lane?
-  // Rows are paired head-to-tail: lane l owns row l (slot 0) and row kRows-1-l
-  // (slot 1), so slot 0 (the short rows) is finished after column kN0 - 1 and
-  // both slots stay busy until then; one slot: lane l owns row l.
-  static constexpr int kN0 = kTwo ? (kRows + 1) / 2 : K;  // slot-0 rows 0 .. kN0-1 (their entries < kN0)
+  static constexpr bool kTwo = kRows > 32;            // two row slots on some lanes?
+  static_assert(kRows <= 64, "at most two row slots per lane");
+  // slot A: rows 0 .. kP-1 on lanes 0 .. kP-1; slot B: row kP + lane
+  static constexpr int kP = kTwo ? kRows - 32 : 0;
   static constexpr int kDch = 16;                      // coordinate slice width staged per pass
   static constexpr int kXsStride = kDch + 2;           // = 2 mod 4 doubles: conflict-light 128-bit row loads
-  static constexpr int kCol = (K + 2) & ~1;            // colbuf (even: 16-byte aligned pairs)
   // xs holds K x D coordinates for the small-d build (D > 0), K x kXsStride slices otherwise
   __host__ __device__ static constexpr int xs_doubles(int D) { return D > 0 ? ((K * D + 1) & ~1) : kXsStride * K; }
   __host__ __device__ static constexpr int per_warp(int D) {
-    return ((kAug + ((K + 1) & ~1) /*dinv*/ + kCol + xs_doubles(D) + (K + 1) / 2 + 2) + 1) & ~1;
+    return ((kAug + ((K + 1) & ~1) /*dinv*/ + xs_doubles(D) + (K + 1) / 2 + 2) + 1) & ~1;
   }
   static constexpr int kTabDoubles = ((K * (K - 1) / 2 + 3) / 4) * 2;  // pair table (uint32), 16 B granules
   __host__ __device__ static constexpr int row_off(int i) { return i < K ? ro_r(i) : ro_r(K) + (i - K) * kRw; }
@@ -70,18 +79,28 @@ template <int K, int D, int KF>
 __device__ __forceinline__ void pair_loop(const double* xs, const uint32_t* ptab, const KParams& kp, double* A,
                                           int lane) {
   constexpr int npairs = (K * (K - 1)) / 2;
+  const double c = kernel_scale_build<KF>(kp);
 #pragma unroll 2
   for (int e = lane; e < npairs; e += kWarp) {
     const uint32_t t = ptab[e];
     const double* xa = xs + ((t >> 8) & 0xffu) * D;
     const double* xb = xs + (t & 0xffu) * D;
-    double acc = 0.0;
+    double acc;
+    if constexpr (D == 2) {
+      const double2 u = *reinterpret_cast<const double2*>(xa);
+      const double2 w = *reinterpret_cast<const double2*>(xb);
+      const double d0 = u.x - w.x, d1 = u.y - w.y;
+      acc = fma(d1, d1, d0 * d0);
+    } else {
+      const double d0 = xa[0] - xb[0];
+      acc = d0 * d0;
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-      const double dd = __dsub_rn(xa[c], xb[c]);
-      acc = __dadd_rn(acc, __dmul_rn(dd, dd));
+      for (int cc = 1; cc < D; ++cc) {
+        const double dd = xa[cc] - xb[cc];
+        acc = fma(dd, dd, acc);
+      }
     }
-    A[t >> 16] = kernel_from_sq<KF>(acc, kp);
+    A[t >> 16] = kernel_from_sq_build<KF>(acc, c, kp);
   }
 }
 
@@ -198,105 +217,109 @@ __device__ void build_reg(const double* __restrict__ X, const double* __restrict
   __syncwarp();
 }
 
-// Register-resident left-looking factorisation of the augmented matrix:
-// column j of the lane's rows accumulates a_rj - sum_{p<j} a_rp L_jp from its
-// registers and the pivot row L_j. broadcast from shared memory (128-bit).
-// Returns false at the first pivot <= 0 (Eigen LLT semantics).
+// Register-resident left-looking factorisation of the augmented matrix
+// (ownership in the file header): column j of the lane's rows accumulates
+// a_rj - sum_{p<j} a_rp L_jp from its registers and the pivot row L_j.
+// broadcast from shared memory (128-bit). The owner of row j supplies the
+// pivot by a shuffle; every lane scales by the same 1/L_jj (the owner's own
+// entry becomes piv * (1/sqrt(piv)) = L_jj). Rows below the column are
+// inactive for it: their lanes compute and discard (stores are predicated).
+// Returns false iff some pivot was <= 0 (Eigen LLT semantics).
 template <int K, int M>
-__device__ bool factor_reg(double* A, double* dinv, double* colbuf, int lane) {
-  (void)colbuf;
+__device__ bool factor_reg(double* A, double* dinv, int lane) {
   using Sh = RegShape<K, M>;
-  constexpr int kRows = Sh::kRows;
-  const int r0 = lane, r1 = kRows - 1 - lane;
-  const bool has0 = Sh::kTwo ? r0 < Sh::kN0 : r0 < kRows;
-  const bool has1 = Sh::kTwo && lane < kRows - Sh::kN0;
-  double a0[Sh::kN0];
-  double a1[Sh::kTwo ? K : 1];
-  // Slot-1 entries p >= kN0 are loaded only when column kN0 starts (they are
-  // still the original values in shared memory then): their registers reuse
-  // the dead slot-0 rows, which keeps the peak register count down.
-  const double* R1 = A + Sh::row_off(has1 ? r1 : 0);
-  {
-    const double* R0 = A + Sh::row_off(has0 ? r0 : 0);
+  constexpr int kP = Sh::kP;
+  constexpr int kB0 = kP > 0 ? kP : K;  // slot-B entries loaded before the sweep
+  const int rB = kP + lane;
+  const bool hasB = rB < Sh::kRows;
+  const bool hasA = lane < kP;
+  double* RB = A + Sh::row_off(hasB ? rB : 0);
+  double* RA = A + Sh::row_off(hasA ? lane : 0);
+  double b[K];
+  double a[kP > 0 ? kP : 1];
+  // Entries beyond a row's length read the next packed row (in bounds, never
+  // used: a row r only ever reads its entries < j <= r).
 #pragma unroll
-    for (int p = 0; p < Sh::kN0; ++p) a0[p] = (has0 && (p <= r0 || r0 >= K)) ? R0[p] : 0.0;
-    if constexpr (Sh::kTwo) {
-#pragma unroll
-      for (int p = 0; p < Sh::kN0; ++p) a1[p] = (has1 && (p <= r1 || r1 >= K)) ? R1[p] : 0.0;
-    }
+  for (int p = 0; p + 1 < kB0; p += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(RB + p);
+    b[p] = v.x;
+    b[p + 1] = v.y;
   }
+  if constexpr (kB0 & 1) b[kB0 - 1] = RB[kB0 - 1];
+  if constexpr (kP > 0) {
+#pragma unroll
+    for (int p = 0; p + 1 < kP; p += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(RA + p);
+      a[p] = v.x;
+      a[p + 1] = v.y;
+    }
+    if constexpr (kP & 1) a[kP - 1] = RA[kP - 1];
+  }
+  bool bad = false;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    if constexpr (Sh::kTwo) {
-      if (j == Sh::kN0) {
+    if constexpr (kP > 0) {
+      if (j == kP) {  // slot A is finished: bring in the rest of slot B (still original values)
 #pragma unroll
-        for (int p = Sh::kN0; p < K; ++p) a1[p] = (has1 && (p <= r1 || r1 >= K)) ? R1[p] : 0.0;
+        for (int p = kP; p < K; ++p) b[p] = RB[p];
       }
     }
+    const bool twoA = kP > 0 && j < kP;
     const double* Lj = A + ro_r(j);  // pivot row j (entries < j are final)
-    // four independent accumulators per row slot (DFMA latency chains of j/4)
-    double s0a = 0.0, s0b = 0.0, s0c = 0.0, s0d = 0.0, s1a = 0.0, s1b = 0.0, s1c = 0.0, s1d = 0.0;
-    if (j < Sh::kN0) s0a = a0[j < Sh::kN0 ? j : 0];
-    if constexpr (Sh::kTwo) s1a = a1[j];
+    // four independent accumulators per slot (DFMA latency chains of j/4)
+    double b0 = b[j], b1 = 0.0, b2 = 0.0, b3 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (twoA) a0 = a[j < kP ? j : 0];
 #pragma unroll
     for (int p = 0; p + 3 < j; p += 4) {
       const double2 l = *reinterpret_cast<const double2*>(Lj + p);
       const double2 m = *reinterpret_cast<const double2*>(Lj + p + 2);
-      if (j < Sh::kN0) {
-        s0a = fma(-a0[p], l.x, s0a);
-        s0b = fma(-a0[p + 1], l.y, s0b);
-        s0c = fma(-a0[p + 2], m.x, s0c);
-        s0d = fma(-a0[p + 3], m.y, s0d);
-      }
-      if constexpr (Sh::kTwo) {
-        s1a = fma(-a1[p], l.x, s1a);
-        s1b = fma(-a1[p + 1], l.y, s1b);
-        s1c = fma(-a1[p + 2], m.x, s1c);
-        s1d = fma(-a1[p + 3], m.y, s1d);
+      b0 = fma(-b[p], l.x, b0);
+      b1 = fma(-b[p + 1], l.y, b1);
+      b2 = fma(-b[p + 2], m.x, b2);
+      b3 = fma(-b[p + 3], m.y, b3);
+      if (twoA) {
+        a0 = fma(-a[p < kP ? p : 0], l.x, a0);
+        a1 = fma(-a[p + 1 < kP ? p + 1 : 0], l.y, a1);
+        a2 = fma(-a[p + 2 < kP ? p + 2 : 0], m.x, a2);
+        a3 = fma(-a[p + 3 < kP ? p + 3 : 0], m.y, a3);
       }
     }
     {  // up to three leftover columns (j is a compile-time constant here)
       const int p0 = j & ~3;
-      if ((j & 3) >= 1) {
-        const double l = Lj[p0];
-        if (j < Sh::kN0) s0a = fma(-a0[p0 < Sh::kN0 ? p0 : 0], l, s0a);
-        if constexpr (Sh::kTwo) s1a = fma(-a1[p0], l, s1a);
-      }
       if ((j & 3) >= 2) {
-        const double l = Lj[p0 + 1];
-        if (j < Sh::kN0) s0b = fma(-a0[(p0 + 1) < Sh::kN0 ? p0 + 1 : 0], l, s0b);
-        if constexpr (Sh::kTwo) s1b = fma(-a1[p0 + 1], l, s1b);
+        const double2 l = *reinterpret_cast<const double2*>(Lj + p0);
+        b0 = fma(-b[p0], l.x, b0);
+        b1 = fma(-b[p0 + 1], l.y, b1);
+        if (twoA) {
+          a0 = fma(-a[p0 < kP ? p0 : 0], l.x, a0);
+          a1 = fma(-a[p0 + 1 < kP ? p0 + 1 : 0], l.y, a1);
+        }
       }
-      if ((j & 3) >= 3) {
-        const double l = Lj[p0 + 2];
-        if (j < Sh::kN0) s0c = fma(-a0[(p0 + 2) < Sh::kN0 ? p0 + 2 : 0], l, s0c);
-        if constexpr (Sh::kTwo) s1c = fma(-a1[p0 + 2], l, s1c);
-      }
-    }
-    const double s0 = (s0a + s0b) + (s0c + s0d), s1 = (s1a + s1b) + (s1c + s1d);
-    const double mine = j < Sh::kN0 ? s0 : s1;
-    const double piv = __shfl_sync(0xffffffffu, mine, j < Sh::kN0 ? j : kRows - 1 - j);
-    if (!(piv > 0.0)) return false;
-    const double inv = rsqrt(piv);  // 1/L_jj and L_jj = piv/L_jj from one reciprocal square root
-    const double ljj = piv * inv;
-    if (j < Sh::kN0) {
-      if (has0 && r0 >= j) {
-        const double v = r0 == j ? ljj : s0 * inv;
-        a0[j < Sh::kN0 ? j : 0] = v;
-        A[Sh::row_off(r0) + j] = v;
+      if ((j & 1) == 1) {
+        const int q = j - 1;
+        const double l = Lj[q];
+        b2 = fma(-b[q], l, b2);
+        if (twoA) a2 = fma(-a[q < kP ? q : 0], l, a2);
       }
     }
-    if constexpr (Sh::kTwo) {
-      if (has1 && r1 >= j) {
-        const double v = r1 == j ? ljj : s1 * inv;
-        a1[j] = v;
-        A[Sh::row_off(r1) + j] = v;
-      }
+    const double sB = (b0 + b1) + (b2 + b3);
+    const double sA = (a0 + a1) + (a2 + a3);
+    const double piv = __shfl_sync(0xffffffffu, twoA ? sA : sB, twoA ? j : j - kP);
+    bad |= !(piv > 0.0);
+    const double inv = rsqrt_pivot(piv);
+    const double vB = sB * inv;
+    b[j] = vB;
+    if (hasB && rB >= j) RB[j] = vB;
+    if (twoA) {
+      const double vA = sA * inv;
+      a[j < kP ? j : 0] = vA;
+      if (hasA && lane >= j) RA[j] = vA;
     }
     if (lane == 0) dinv[j] = inv;
     __syncwarp();
   }
-  return true;
+  return !bad;
 }
 
 // Backward solve L^T x = z, z = the forward-substituted RHS rows. Lane l keeps
@@ -331,8 +354,16 @@ __device__ void back_solve_reg(const double* A, const double* dinv, double* __re
   }
 }
 
+// CTA shape: 4 warps (one pair table per 4 neighbourhoods in flight), 4-5
+// CTAs per SM: <= 128 registers per thread for two-slot shapes.
+template <int K, int M>
+struct RegLaunch {
+  static constexpr int kWarps = 4;
+  static constexpr int kMinBlocks = K + M <= 32 ? 5 : 4;
+};
+
 template <int K, int M, int D>
-__global__ void __launch_bounds__(64, K <= 32 ? 8 : 6)
+__global__ void __launch_bounds__(RegLaunch<K, M>::kWarps * kWarp, RegLaunch<K, M>::kMinBlocks)
 solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
                  int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
                  unsigned long long* __restrict__ fail_min) {
@@ -348,8 +379,7 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
   }
   double* A = smem + (D > 0 ? Sh::kTabDoubles : 0) + warp * Sh::per_warp(D);
   double* dinv = A + Sh::kAug;
-  double* colbuf = dinv + ((K + 1) & ~1);
-  double* xs = colbuf + Sh::kCol;
+  double* xs = dinv + ((K + 1) & ~1);
   int32_t* sr = reinterpret_cast<int32_t*>(xs + Sh::xs_doubles(D));
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * warps + warp; r < nrows;
        r += static_cast<int64_t>(gridDim.x) * warps) {
@@ -361,7 +391,7 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
         build_small<K, M, D>(X, Y, sr, kp, attempt, A, xs, ptab, lane);
       else
         build_reg<K, M>(X, Y, d, sr, kp, attempt, A, xs, lane);
-      ok = factor_reg<K, M>(A, dinv, colbuf, lane);
+      ok = factor_reg<K, M>(A, dinv, lane);
       __syncwarp();
     }
     if (!ok) {
@@ -378,7 +408,7 @@ template <int K, int M, int D>
 cudaError_t launch_reg(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows, int64_t row_begin,
                        const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
   using Sh = RegShape<K, M>;
-  constexpr int kWarps = 2;
+  constexpr int kWarps = RegLaunch<K, M>::kWarps;
   const size_t smem = sizeof(double) * ((D > 0 ? Sh::kTabDoubles : 0) + Sh::per_warp(D) * kWarps);
   cudaError_t err = cudaFuncSetAttribute(solve_reg_kernel<K, M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
