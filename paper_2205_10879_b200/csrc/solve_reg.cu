@@ -75,32 +75,55 @@ __device__ void fill_pair_table(uint32_t* ptab) {
   }
 }
 
+template <int D>
+__device__ __forceinline__ void load_pair(const double* xs, uint32_t t, double (&u)[D], double (&w)[D]) {
+  const double* xa = xs + ((t >> 8) & 0xffu) * D;
+  const double* xb = xs + (t & 0xffu) * D;
+  if constexpr (D == 2) {
+    const double2 a2 = *reinterpret_cast<const double2*>(xa);
+    const double2 b2 = *reinterpret_cast<const double2*>(xb);
+    u[0] = a2.x; u[1] = a2.y; w[0] = b2.x; w[1] = b2.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      u[c] = xa[c];
+      w[c] = xb[c];
+    }
+  }
+}
+
+// One pair per lane per step; the next step's table entry and coordinates are
+// loaded before the current entry is evaluated (the loop is latency-bound on
+// the table -> coordinate shared-memory chain otherwise).
 template <int K, int D, int KF>
 __device__ __forceinline__ void pair_loop(const double* xs, const uint32_t* ptab, const KParams& kp, double* A,
                                           int lane) {
   constexpr int npairs = (K * (K - 1)) / 2;
+  static_assert(npairs >= kWarp, "first step loads one entry per lane");
   const double c = kernel_scale_build<KF>(kp);
-#pragma unroll 2
+  uint32_t t = ptab[lane];
+  double u[D], w[D];
+  load_pair<D>(xs, t, u, w);
+#pragma unroll 1
   for (int e = lane; e < npairs; e += kWarp) {
-    const uint32_t t = ptab[e];
-    const double* xa = xs + ((t >> 8) & 0xffu) * D;
-    const double* xb = xs + (t & 0xffu) * D;
-    double acc;
-    if constexpr (D == 2) {
-      const double2 u = *reinterpret_cast<const double2*>(xa);
-      const double2 w = *reinterpret_cast<const double2*>(xb);
-      const double d0 = u.x - w.x, d1 = u.y - w.y;
-      acc = fma(d1, d1, d0 * d0);
-    } else {
-      const double d0 = xa[0] - xb[0];
-      acc = d0 * d0;
+    const int en = e + kWarp;
+    const uint32_t tn = ptab[en < npairs ? en : e];
+    double un[D], wn[D];
+    load_pair<D>(xs, tn, un, wn);
+    const double d0 = u[0] - w[0];
+    double acc = d0 * d0;
 #pragma unroll
-      for (int cc = 1; cc < D; ++cc) {
-        const double dd = xa[cc] - xb[cc];
-        acc = fma(dd, dd, acc);
-      }
+    for (int cc = 1; cc < D; ++cc) {
+      const double dd = u[cc] - w[cc];
+      acc = fma(dd, dd, acc);
     }
     A[t >> 16] = kernel_from_sq_build<KF>(acc, c, kp);
+    t = tn;
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) {
+      u[cc] = un[cc];
+      w[cc] = wn[cc];
+    }
   }
 }
 
@@ -354,12 +377,12 @@ __device__ void back_solve_reg(const double* A, const double* dinv, double* __re
   }
 }
 
-// CTA shape: 4 warps (one pair table per 4 neighbourhoods in flight), 4-5
-// CTAs per SM: <= 128 registers per thread for two-slot shapes.
+// CTA shape: 4 warps (one pair table per 4 neighbourhoods in flight), 4 CTAs
+// per SM: <= 128 registers per thread, 16 warps per SM.
 template <int K, int M>
 struct RegLaunch {
   static constexpr int kWarps = 4;
-  static constexpr int kMinBlocks = K + M <= 32 ? 5 : 4;
+  static constexpr int kMinBlocks = 4;
 };
 
 template <int K, int M, int D>
