@@ -44,14 +44,30 @@ def _stale(out: Path, deps: list[Path]) -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build_cuda(force: bool = False) -> Path:
-    out = LIB / "libfmgp_b200.so"
-    deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
-    deps += [REPO / "include" / "fmgp_b200.h", Path(__file__)]
-    if force or _stale(out, deps):
-        LIB.mkdir(exist_ok=True)
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-              "-Xptxas", "-O3", "-o", str(out), *[str(CSRC / s) for s in CUDA_SOURCES]])
+def build_cuda(force: bool = False, defines: list[str] | None = None, out: Path | None = None) -> Path:
+    """Compile each CUDA TU to an object in parallel (build/obj), then link the
+    shared library. `defines` (-DNAME=V) and `out` are for kernel A/B variants."""
+    out = out or LIB / "libfmgp_b200.so"
+    defines = defines or []
+    headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [REPO / "include" / "fmgp_b200.h", Path(__file__)]
+    deps = [CSRC / s for s in CUDA_SOURCES] + headers
+    if not (force or _stale(out, deps)):
+        return out
+    LIB.mkdir(exist_ok=True)
+    out.parent.mkdir(parents=True, exist_ok=True)
+    tag = "_".join(d.lstrip("-D").replace("=", "") for d in defines) or "default"
+    objdir = REPO / "build" / "obj" / tag
+    objdir.mkdir(parents=True, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-O3", *defines]
+    jobs = []
+    for s in CUDA_SOURCES:
+        obj = objdir / (Path(s).stem + ".o")
+        if force or _stale(obj, [CSRC / s] + headers):
+            jobs.append([NVCC, *flags, "-c", "-o", str(obj), str(CSRC / s)])
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4) or 1) as ex:
+        list(ex.map(_run, jobs))
+    _run([NVCC, *ARCH, "-shared", "-o", str(out), *[str(objdir / (Path(s).stem + ".o")) for s in CUDA_SOURCES]])
     return out
 
 
