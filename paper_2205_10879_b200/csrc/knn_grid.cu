@@ -28,6 +28,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
+#include <string>
 
 #include "fmgp_common.cuh"
 #include "fmgp_internal.h"
@@ -338,10 +339,81 @@ __device__ __forceinline__ double outside_lb_sq(const GridParams& g, const doubl
 constexpr int kQueryThreads = 256;
 constexpr int kSlots = 64;  // ranges per chunk: 2 per lane (one cell-row per lane)
 
+// Static cell visiting order for the warp kernel: every offset o of Chebyshev
+// radius <= R sorted by its static lower bound sb(o) = sum_t max(|o_t| - 1, 0)^2
+// (in h^2: no point of cell c + o is closer than h sqrt(sb) to any point of
+// cell c), the sb = 0 block (3^D cells) first. Packed (o_x + 128) |
+// (o_y + 128) << 8 | (o_z + 128) << 16 | sb << 24. Generated at compile time.
+template <int D>
+struct OrdR {
+  static constexpr int R = D == 3 ? 3 : 4;
+  static constexpr int N = D == 3 ? 343 : (D == 2 ? 81 : 9);
+};
+template <int D>
+struct OrdTable {
+  int32_t e[OrdR<D>::N];
+};
+template <int D>
+constexpr OrdTable<D> make_ord() {
+  constexpr int R = OrdR<D>::R, N = OrdR<D>::N, W = 2 * R + 1;
+  OrdTable<D> t{};
+  int sb[N] = {}, l1[N] = {};
+  for (int i = 0; i < N; ++i) {
+    int o[3] = {0, 0, 0};
+    int v = i;
+    for (int a = 0; a < D; ++a) {
+      o[a] = v % W - R;
+      v /= W;
+    }
+    int s2 = 0, n1 = 0;
+    for (int a = 0; a < D; ++a) {
+      const int m = (o[a] < 0 ? -o[a] : o[a]) - 1;
+      s2 += m > 0 ? m * m : 0;
+      n1 += o[a] < 0 ? -o[a] : o[a];
+    }
+    t.e[i] = (o[0] + 128) | ((o[1] + 128) << 8) | ((o[2] + 128) << 16) | (s2 << 24);
+    sb[i] = s2;
+    l1[i] = n1;
+  }
+  for (int i = 1; i < N; ++i) {  // insertion sort by (sb, |o|_1), stable
+    const int e = t.e[i], s0 = sb[i], n0 = l1[i];
+    int j = i - 1;
+    while (j >= 0 && (sb[j] > s0 || (sb[j] == s0 && l1[j] > n0))) {
+      t.e[j + 1] = t.e[j];
+      sb[j + 1] = sb[j];
+      l1[j + 1] = l1[j];
+      --j;
+    }
+    t.e[j + 1] = e;
+    sb[j + 1] = s0;
+    l1[j + 1] = n0;
+  }
+  return t;
+}
+__constant__ OrdTable<2> kOrd2 = make_ord<2>();
+__constant__ OrdTable<3> kOrd3 = make_ord<3>();
+template <int D>
+__device__ __forceinline__ int32_t ord_entry(int i) {
+  if constexpr (D == 3) return kOrd3.e[i];
+  else return kOrd2.e[i];
+}
+
 // One warp per query. Query w is: sorted position qpos[w] (self mode,
 // exclusion by original index), or sorted position w when qpos == nullptr
 // and Q == nullptr, or external coordinates Q[w] (no exclusion). Output row
 // index: original index - row_offset (self modes) or qout[w] / w.
+//
+// Walk (d = 2, 3): the cells of Chebyshev radius <= R in the static order
+// above, one chunk of up to 32 cells at a time (the 3^D block first); a cell
+// whose exact box distance to q (each axis gap shrunk by the 1e-7 h margin)
+// exceeds the current kk-th key is skipped, and the walk stops before a chunk
+// whose static bound h sqrt(min(sb, R^2)) - slack - 1e-7 h (slack = distance
+// of q outside its own cell's box, 0 for points of the set) already exceeds
+// the kk-th key (cells beyond radius R have sb >= R^2). If the list runs out
+// the Chebyshev-ring walk continues from radius R + 1 with the
+// outside-the-block stop test. With cells of ~kk/6 (2-D) or ~kk/16 (3-D)
+// points this examines ~2x (2-D) to ~3x (3-D) fewer candidates than a radius-1
+// block of ~kk/2 points per cell, and returns the same rows.
 template <int D, int E>
 __global__ void __launch_bounds__(kQueryThreads, 3)
 grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
@@ -382,7 +454,106 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
     Cand thr{INFINITY, INT_MAX};
     const int tl = (kk - 1) & 31, te = (kk - 1) >> 5;
 
-    for (int r = 1;; ++r) {
+    // Scan up to 64 ranges (two per lane) of cell-ordered points: candidates
+    // 32 at a time, ballot skip, bitonic sort + merge into the top-KP list.
+    auto scan_ranges = [&](int32_t b0, int32_t l0, int32_t b1, int32_t l1) {
+      int32_t incl = l0 + l1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int32_t excl = incl - (l0 + l1);
+      rb[2 * lane] = b0;
+      rb[2 * lane + 1] = b1;
+      rp[2 * lane] = excl;
+      rp[2 * lane + 1] = excl + l0;
+      const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 31) rp[kSlots] = total;
+      __syncwarp();
+      for (int32_t base = 0; base < total; base += 32) {
+        const int32_t want = base + lane;
+        Cand cd{INFINITY, INT_MAX};
+        if (want < total) {
+          int j = 0;  // largest slot j with rp[j] <= want (skips empty slots)
+#pragma unroll
+          for (int step = kSlots / 2; step > 0; step >>= 1)
+            if (rp[j + step] <= want) j += step;
+          const int64_t p = static_cast<int64_t>(rb[j]) + (want - rp[j]);
+          const int32_t id = pid[p];
+          double x[D];
+#pragma unroll
+          for (int t = 0; t < D; ++t) x[t] = pts[p * D + t];
+          const double sd = dist_sq_fixed<D>(q, x);
+          if (id != self) cd = Cand{sd, id};
+        }
+        const bool pass = cless(cd, thr);
+        if (__ballot_sync(0xffffffffu, pass) != 0) {
+          if (!pass) cd = Cand{INFINITY, INT_MAX};
+          merge_batch_chain<E>(L, cd, lane);
+          Cand t{0, 0};
+#pragma unroll
+          for (int e = 0; e < E; ++e)
+            if (e == te) t = L[e];
+          thr = shfl_c(t, tl);
+        }
+      }
+      __syncwarp();
+    };
+
+    int r0 = 1;  // first Chebyshev ring of the fallback walk
+    bool done = false;
+    if constexpr (D >= 2) {
+      constexpr int R = OrdR<D>::R, N = OrdR<D>::N, N0 = D == 3 ? 27 : 9;
+      double slack2 = 0.0, lo_c[D];
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        lo_c[t] = g.lo[t] + c[t] * g.h;
+        const double gap = fmax(fmax(lo_c[t] - q[t], q[t] - (lo_c[t] + g.h)), 0.0);
+        slack2 += gap * gap;
+      }
+      const double slack = sqrt(slack2), margin = 1e-7 * g.h;
+      for (int base = 0; base < N;) {
+        const int len = base == 0 ? N0 : min(32, N - base);
+        if (base > 0) {
+          const int sbv = min(static_cast<int>(static_cast<uint32_t>(ord_entry<D>(base)) >> 24), R * R);
+          const double lb = g.h * sqrt(static_cast<double>(sbv)) - slack - margin;
+          if (lb > 0.0 && thr.d < lb * lb * (1.0 - 1e-12)) {
+            done = true;
+            break;
+          }
+        }
+        int32_t b0 = 0, l0 = 0;
+        if (lane < len) {
+          const int32_t e = ord_entry<D>(base + lane);
+          int cc[3] = {c[0] + ((e & 0xff) - 128), c[1] + (((e >> 8) & 0xff) - 128), D == 3 ? c[2] + (((e >> 16) & 0xff) - 128) : 0};
+          bool in = true;
+          double lb2 = 0.0;
+#pragma unroll
+          for (int t = 0; t < D; ++t) {
+            in = in && cc[t] >= 0 && cc[t] < g.G[t];
+            const double lo = g.lo[t] + cc[t] * g.h;
+            const double gap = fmax(fmax(lo - q[t], q[t] - (lo + g.h)) - margin, 0.0);
+            lb2 += gap * gap;
+          }
+          if (in && !(lb2 * (1.0 - 1e-12) > thr.d)) {
+            const int64_t key = D == 3 ? (static_cast<int64_t>(cc[2]) * g.G[1] + cc[1]) * g.G[0] + cc[0]
+                                       : static_cast<int64_t>(cc[1]) * g.G[0] + cc[0];
+            b0 = cstart[key];
+            l0 = cstart[key + 1] - b0;
+          }
+        }
+        scan_ranges(b0, l0, 0, 0);
+        base += len;
+      }
+      if (!done) {
+        const double lb2 = outside_lb_sq<D>(g, q, c, R);
+        done = lb2 == INFINITY || thr.d < lb2;
+      }
+      r0 = R + 1;
+    }
+
+    for (int r = r0; !done; ++r) {
       const bool block = (r == 1);
       const int z0 = D >= 3 ? max(0, c[2] - r) : 0, z1 = D >= 3 ? min(g.G[2] - 1, c[2] + r) : 0;
       const int y0 = D >= 2 ? max(0, c[1] - r) : 0, y1 = D >= 2 ? min(g.G[1] - 1, c[1] + r) : 0;
@@ -413,48 +584,7 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
             }
           }
         }
-        int32_t incl = l0 + l1;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int32_t excl = incl - (l0 + l1);
-        rb[2 * lane] = b0;
-        rb[2 * lane + 1] = b1;
-        rp[2 * lane] = excl;
-        rp[2 * lane + 1] = excl + l0;
-        const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        if (lane == 31) rp[kSlots] = total;
-        __syncwarp();
-        for (int32_t base = 0; base < total; base += 32) {
-          const int32_t want = base + lane;
-          Cand cd{INFINITY, INT_MAX};
-          if (want < total) {
-            int j = 0;  // largest slot j with rp[j] <= want (skips empty slots)
-#pragma unroll
-            for (int step = kSlots / 2; step > 0; step >>= 1)
-              if (rp[j + step] <= want) j += step;
-            const int64_t p = static_cast<int64_t>(rb[j]) + (want - rp[j]);
-            const int32_t id = pid[p];
-            double x[D];
-#pragma unroll
-            for (int t = 0; t < D; ++t) x[t] = pts[p * D + t];
-            const double s = dist_sq_fixed<D>(q, x);
-            if (id != self) cd = Cand{s, id};
-          }
-          const bool pass = cless(cd, thr);
-          if (__ballot_sync(0xffffffffu, pass) != 0) {
-            if (!pass) cd = Cand{INFINITY, INT_MAX};
-            merge_batch_chain<E>(L, cd, lane);
-            Cand t{0, 0};
-#pragma unroll
-            for (int e = 0; e < E; ++e)
-              if (e == te) t = L[e];
-            thr = shfl_c(t, tl);
-          }
-        }
-        __syncwarp();
+        scan_ranges(b0, l0, b1, l1);
       }
       const double lb2 = outside_lb_sq<D>(g, q, c, r);
       if (lb2 == INFINITY) break;  // the block covers every cell
@@ -472,6 +602,173 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
         row[o + t] = L[e].i;
         if (out_d) out_d[orow * kk + t] = L[e].d;
       }
+    }
+  }
+}
+
+// Thread-per-query variant (A/B only, FMGP_KNN_GRID=thread; walks the
+// Chebyshev rings from radius 1, measured no faster than the warp kernel:
+// the per-thread heap sifts diverge across the warp and the heaps' shared
+// memory leaves little L1 for the candidate loads): each thread
+// owns one query, walks the same block/rings with its own loop and keeps its
+// top-kk in a max-heap on (key, index) in shared memory (slot-major, so the
+// heap accesses of a warp are bank-conflict-free), root cached in registers.
+// With ~4-5 k candidates per query at cfg2 the warp kernel spends most of its
+// instructions in 32-wide bitonic sorts and merges; here a rejected
+// candidate costs one compare and an admitted one a heap sift (<= log2 kk
+// levels), and consecutive threads hold queries of the same or neighbouring
+// cells (cell order), so their candidate loads are mostly the same address.
+// Same walk, stop test and (key, index) order as grid_query_kernel: the
+// rows are identical.
+constexpr int kThreadMaxK = 64;
+constexpr int kThreadQueryThreads = 64;
+
+template <int D>
+__global__ void __launch_bounds__(kThreadQueryThreads)
+grid_query_thread_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts,
+                         const int32_t* __restrict__ pid, const int32_t* __restrict__ cstart, int64_t nq,
+                         const int32_t* __restrict__ qpos, const double* __restrict__ Q,
+                         const int32_t* __restrict__ qout, const int32_t* __restrict__ excl_arr, int kk,
+                         int with_self, int64_t row_offset, int32_t* __restrict__ out, double* __restrict__ out_d) {
+  extern __shared__ double hsm[];
+  const int T = blockDim.x;
+  double* hd = hsm + threadIdx.x;                                                  // hd[s * T]
+  int32_t* hi = reinterpret_cast<int32_t*>(hsm + static_cast<size_t>(kk) * T) + threadIdx.x;  // hi[s * T]
+  const GridParams g = *gpp;
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * T + threadIdx.x; w < nq;
+       w += static_cast<int64_t>(gridDim.x) * T) {
+    double q[D];
+    int32_t self = -1;
+    int64_t orow;
+    if (Q == nullptr) {
+      const int64_t p = qpos != nullptr ? qpos[w] : w;
+#pragma unroll
+      for (int t = 0; t < D; ++t) q[t] = pts[p * D + t];
+      self = pid[p];
+      orow = static_cast<int64_t>(self) - row_offset;
+    } else {
+#pragma unroll
+      for (int t = 0; t < D; ++t) q[t] = Q[w * D + t];
+      orow = qout != nullptr ? qout[w] : w;
+      if (excl_arr != nullptr) self = excl_arr[orow];
+    }
+    int c[3];
+    cell_key<D>(q, g, c);
+    int cnt = 0;
+    double rd = INFINITY;  // heap root (the kk-th best once full)
+    int32_t ri = INT_MAX;
+
+    auto consider = [&](int32_t b, int32_t e) {
+      for (int32_t p = b; p < e; ++p) {
+        const int32_t id = pid[p];
+        double x[D];
+#pragma unroll
+        for (int t = 0; t < D; ++t) x[t] = pts[static_cast<int64_t>(p) * D + t];
+        const double sd = dist_sq_fixed<D>(q, x);
+        if (id == self) continue;
+        if (cnt < kk) {  // push + sift up
+          int pos = cnt++;
+          while (pos > 0) {
+            const int par = (pos - 1) >> 1;
+            const double pd = hd[par * T];
+            const int32_t pi = hi[par * T];
+            if (!pair_less(pd, pi, sd, id)) break;
+            hd[pos * T] = pd;
+            hi[pos * T] = pi;
+            pos = par;
+          }
+          hd[pos * T] = sd;
+          hi[pos * T] = id;
+          rd = hd[0];
+          ri = hi[0];
+        } else if (pair_less(sd, id, rd, ri)) {  // replace the root + sift down
+          int pos = 0;
+          for (;;) {
+            int ch = 2 * pos + 1;
+            if (ch >= kk) break;
+            double cd = hd[ch * T];
+            int32_t ci = hi[ch * T];
+            if (ch + 1 < kk) {
+              const double d2 = hd[(ch + 1) * T];
+              const int32_t i2 = hi[(ch + 1) * T];
+              if (pair_less(cd, ci, d2, i2)) {
+                cd = d2;
+                ci = i2;
+                ++ch;
+              }
+            }
+            if (!pair_less(sd, id, cd, ci)) break;
+            hd[pos * T] = cd;
+            hi[pos * T] = ci;
+            pos = ch;
+          }
+          hd[pos * T] = sd;
+          hi[pos * T] = id;
+          rd = hd[0];
+          ri = hi[0];
+        }
+      }
+    };
+
+    for (int r = 1;; ++r) {
+      const bool block = (r == 1);
+      const int z0 = D >= 3 ? max(0, c[2] - r) : 0, z1 = D >= 3 ? min(g.G[2] - 1, c[2] + r) : 0;
+      const int y0 = D >= 2 ? max(0, c[1] - r) : 0, y1 = D >= 2 ? min(g.G[1] - 1, c[1] + r) : 0;
+      const int xl = c[0] - r, xr = c[0] + r;
+      const int x0 = max(0, xl), x1 = min(g.G[0] - 1, xr);
+      for (int z = z0; z <= z1; ++z) {
+        for (int y = y0; y <= y1; ++y) {
+          const bool edge = block || (D >= 3 && (z == c[2] - r || z == c[2] + r)) ||
+                            (D >= 2 && (y == c[1] - r || y == c[1] + r));
+          const int64_t rowkey = (static_cast<int64_t>(z) * g.G[1] + y) * g.G[0];
+          if (edge) {
+            consider(cstart[rowkey + x0], cstart[rowkey + x1 + 1]);
+          } else {
+            if (xl >= 0) consider(cstart[rowkey + xl], cstart[rowkey + xl + 1]);
+            if (xr < g.G[0]) consider(cstart[rowkey + xr], cstart[rowkey + xr + 1]);
+          }
+        }
+      }
+      const double lb2 = outside_lb_sq<D>(g, q, c, r);
+      if (lb2 == INFINITY) break;             // the block covers every cell
+      if (cnt == kk && rd < lb2) break;       // nothing outside can enter the top-kk
+    }
+    // heap sort in place: ascending (key, index) in slots 0 .. cnt-1
+    for (int end = cnt - 1; end > 0; --end) {
+      const double td = hd[end * T];
+      const int32_t ti = hi[end * T];
+      hd[end * T] = hd[0];
+      hi[end * T] = hi[0];
+      int pos = 0;
+      for (;;) {
+        int ch = 2 * pos + 1;
+        if (ch >= end) break;
+        double cd = hd[ch * T];
+        int32_t ci = hi[ch * T];
+        if (ch + 1 < end) {
+          const double d2 = hd[(ch + 1) * T];
+          const int32_t i2 = hi[(ch + 1) * T];
+          if (pair_less(cd, ci, d2, i2)) {
+            cd = d2;
+            ci = i2;
+            ++ch;
+          }
+        }
+        if (!pair_less(td, ti, cd, ci)) break;
+        hd[pos * T] = cd;
+        hi[pos * T] = ci;
+        pos = ch;
+      }
+      hd[pos * T] = td;
+      hi[pos * T] = ti;
+    }
+    const int width = kk + (with_self ? 1 : 0);
+    int32_t* row = out + orow * width;
+    const int o = with_self ? 1 : 0;
+    if (with_self) row[0] = self;
+    for (int t = 0; t < kk; ++t) {
+      row[o + t] = t < cnt ? hi[t * T] : INT_MAX;
+      if (out_d) out_d[orow * kk + t] = t < cnt ? hd[t * T] : INFINITY;
     }
   }
 }
@@ -673,6 +970,26 @@ void launch_query_e(int E, const GridParams* gp, const double* pts, const int32_
                     int64_t nq, const int32_t* qpos, const double* Q, const int32_t* qout, const int32_t* excl_arr,
                     int kk, int with_self, int64_t row_offset, int32_t* out, double* out_d, int num_sms,
                     cudaStream_t s) {
+  // FMGP_KNN_GRID=thread selects the thread-per-query kernel (A/B checks)
+  static const bool thread_mode = [] {
+    const char* e = std::getenv("FMGP_KNN_GRID");
+    return e != nullptr && std::string(e) == "thread";
+  }();
+  if (thread_mode && kk <= kThreadMaxK) {
+    const size_t smem = static_cast<size_t>(kk) * kThreadQueryThreads * (sizeof(double) + sizeof(int32_t));
+    cudaFuncSetAttribute(grid_query_thread_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_query_thread_kernel<D>, kThreadQueryThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = (nq + kThreadQueryThreads - 1) / kThreadQueryThreads;
+    const int64_t cap = static_cast<int64_t>(num_sms) * per_sm;
+    if (blocks > cap) blocks = cap;
+    grid_query_thread_kernel<D><<<static_cast<unsigned>(blocks), kThreadQueryThreads, smem, s>>>(
+        gp, pts, pid, cstart, nq, qpos, Q, qout, excl_arr, kk, with_self, row_offset, out, out_d);
+    note_launches(1);
+    return;
+  }
   if (E == 1)
     launch_query<D, 1>(gp, pts, pid, cstart, nq, qpos, Q, qout, excl_arr, kk, with_self, row_offset, out, out_d,
                           num_sms, s);
@@ -690,7 +1007,10 @@ cudaError_t knn_grid_d(const double* Q, int64_t nq, const double* P, int64_t np,
                        cudaStream_t s) {
   const int E = kk <= 32 ? 1 : (kk <= 64 ? 2 : 4);
   // Points per cell: enough that the radius-1 block usually holds the kk-th neighbour.
-  const double per_cell = (D == 1) ? fmax(4.0, 0.6 * kk) : (D == 2 ? fmax(4.0, 0.5 * kk) : fmax(3.0, 0.37 * kk));
+  // Points per cell. d = 1: enough that the radius-1 block usually holds the
+  // kk-th neighbour; d = 2, 3: smaller cells for the distance-ordered walk
+  // (the 3^D block holds ~1.5 kk, later cells are skipped by their distance).
+  const double per_cell = (D == 1) ? fmax(4.0, 0.6 * kk) : (D == 2 ? fmax(4.0, kk / 6.0) : fmax(2.0, kk / 16.0));
   const int64_t ncap = np;  // cells never exceed the point count
   GridParams* gp = nullptr;
   unsigned long long* mm = nullptr;
