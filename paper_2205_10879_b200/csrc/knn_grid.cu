@@ -774,11 +774,17 @@ grid_query_thread_kernel(const GridParams* __restrict__ gpp, const double* __res
 }
 
 // Fused predict for d <= 3 (fast_predict_one, fast_predict.cpp:132-144): one
-// warp per test point finds the nearest training point with the same ring
-// search (an argmin over (key, index) instead of a top-k list), then
-// evaluates the k cross-covariances and the dot with C_j in the reference's
-// sequential order, without writing the 1-NN index out in between.
-template <int D>
+// warp per test point finds the nearest training point (argmin over
+// (key, index), the reference's std::min over pairs) with the same
+// distance-ordered cell walk as grid_query_kernel (cells of ~1.5 points in
+// 2-D, ~1 in 3-D: the 3^D block almost always holds the answer and the next
+// chunk's static bound stops the walk), then evaluates the k
+// cross-covariances (kernel_from_sq_build, KF = kernel kind) against C_j and
+// reduces the dot over the warp by a shuffle tree, without writing the 1-NN
+// index out in between. The sum order differs from the reference's
+// sequential loop by rounding only (posterior means within 1e-15 relative of
+// the sequential sum here, tolerance 1e-9).
+template <int D, int KF>
 __global__ void __launch_bounds__(kQueryThreads, 4)
 grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
                     const int32_t* __restrict__ cstart, int64_t nq, const double* __restrict__ Qs,
@@ -792,6 +798,7 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
   const int wib = threadIdx.x >> 5;
   int32_t* rb = s_beg[wib];
   int32_t* rp = s_pre[wib];
+  const double kc = kernel_scale_build<KF>(kp);
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t w = warp0; w < nq; w += nwarps) {
@@ -802,7 +809,99 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
     int c[3];
     cell_key<D>(q, g, c);
     Cand best{INFINITY, INT_MAX};
-    for (int r = 1;; ++r) {
+
+    // argmin over up to 64 ranges (two per lane), then over the warp
+    auto scan_ranges = [&](int32_t b0, int32_t l0, int32_t b1, int32_t l1) {
+      int32_t incl = l0 + l1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int32_t excl = incl - (l0 + l1);
+      rb[2 * lane] = b0;
+      rb[2 * lane + 1] = b1;
+      rp[2 * lane] = excl;
+      rp[2 * lane + 1] = excl + l0;
+      const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 31) rp[kSlots] = total;
+      __syncwarp();
+      for (int32_t base = 0; base < total; base += 32) {
+        const int32_t want = base + lane;
+        if (want < total) {
+          int j = 0;
+#pragma unroll
+          for (int step = kSlots / 2; step > 0; step >>= 1)
+            if (rp[j + step] <= want) j += step;
+          const int64_t p = static_cast<int64_t>(rb[j]) + (want - rp[j]);
+          double x[D];
+#pragma unroll
+          for (int t = 0; t < D; ++t) x[t] = pts[p * D + t];
+          const Cand cd{dist_sq_fixed<D>(q, x), pid[p]};
+          if (cless(cd, best)) best = cd;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const Cand other = shfl_xor_c(best, o);
+        if (cless(other, best)) best = other;
+      }
+    };
+
+    int r0 = 1;
+    bool done = false;
+    if constexpr (D >= 2) {
+      constexpr int R = OrdR<D>::R, N = OrdR<D>::N, N0 = D == 3 ? 27 : 9;
+      double slack2 = 0.0;
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        const double lo = g.lo[t] + c[t] * g.h;
+        const double gap = fmax(fmax(lo - q[t], q[t] - (lo + g.h)), 0.0);
+        slack2 += gap * gap;
+      }
+      const double slack = sqrt(slack2), margin = 1e-7 * g.h;
+      for (int base = 0; base < N;) {
+        const int len = base == 0 ? N0 : min(32, N - base);
+        if (base > 0) {
+          const int sbv = min(static_cast<int>(static_cast<uint32_t>(ord_entry<D>(base)) >> 24), R * R);
+          const double lb = g.h * sqrt(static_cast<double>(sbv)) - slack - margin;
+          if (lb > 0.0 && best.d < lb * lb * (1.0 - 1e-12)) {
+            done = true;
+            break;
+          }
+        }
+        int32_t b0 = 0, l0 = 0;
+        if (lane < len) {
+          const int32_t e = ord_entry<D>(base + lane);
+          int cc[3] = {c[0] + ((e & 0xff) - 128), c[1] + (((e >> 8) & 0xff) - 128),
+                       D == 3 ? c[2] + (((e >> 16) & 0xff) - 128) : 0};
+          bool in = true;
+          double lb2 = 0.0;
+#pragma unroll
+          for (int t = 0; t < D; ++t) {
+            in = in && cc[t] >= 0 && cc[t] < g.G[t];
+            const double lo = g.lo[t] + cc[t] * g.h;
+            const double gap = fmax(fmax(lo - q[t], q[t] - (lo + g.h)) - margin, 0.0);
+            lb2 += gap * gap;
+          }
+          if (in && !(lb2 * (1.0 - 1e-12) > best.d)) {
+            const int64_t key = D == 3 ? (static_cast<int64_t>(cc[2]) * g.G[1] + cc[1]) * g.G[0] + cc[0]
+                                       : static_cast<int64_t>(cc[1]) * g.G[0] + cc[0];
+            b0 = cstart[key];
+            l0 = cstart[key + 1] - b0;
+          }
+        }
+        scan_ranges(b0, l0, 0, 0);
+        base += len;
+      }
+      if (!done) {
+        const double lb2 = outside_lb_sq<D>(g, q, c, R);
+        done = lb2 == INFINITY || best.d < lb2;
+      }
+      r0 = R + 1;
+    }
+    for (int r = r0; !done; ++r) {
       const bool block = (r == 1);
       const int z0 = D >= 3 ? max(0, c[2] - r) : 0, z1 = D >= 3 ? min(g.G[2] - 1, c[2] + r) : 0;
       const int y0 = D >= 2 ? max(0, c[1] - r) : 0, y1 = D >= 2 ? min(g.G[1] - 1, c[1] + r) : 0;
@@ -832,42 +931,7 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
             }
           }
         }
-        int32_t incl = l0 + l1;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int32_t excl = incl - (l0 + l1);
-        rb[2 * lane] = b0;
-        rb[2 * lane + 1] = b1;
-        rp[2 * lane] = excl;
-        rp[2 * lane + 1] = excl + l0;
-        const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        if (lane == 31) rp[kSlots] = total;
-        __syncwarp();
-        for (int32_t base = 0; base < total; base += 32) {
-          const int32_t want = base + lane;
-          if (want < total) {
-            int j = 0;
-#pragma unroll
-            for (int step = kSlots / 2; step > 0; step >>= 1)
-              if (rp[j + step] <= want) j += step;
-            const int64_t p = static_cast<int64_t>(rb[j]) + (want - rp[j]);
-            double x[D];
-#pragma unroll
-            for (int t = 0; t < D; ++t) x[t] = pts[p * D + t];
-            const Cand cd{dist_sq_fixed<D>(q, x), pid[p]};
-            if (cless(cd, best)) best = cd;
-          }
-        }
-        __syncwarp();
-      }
-      // warp argmin over (key, index)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const Cand other = shfl_xor_c(best, o);
-        if (cless(other, best)) best = other;
+        scan_ranges(b0, l0, b1, l1);
       }
       const double lb2 = outside_lb_sq<D>(g, q, c, r);
       if (lb2 == INFINITY) break;
@@ -877,18 +941,21 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
     if (nn_out != nullptr && lane == 0) nn_out[orow] = static_cast<int32_t>(j);
     for (int cc = 0; cc < m; ++cc) {
       double acc = 0.0;
-      for (int t0 = 0; t0 < k; t0 += kWarp) {
-        const int t = t0 + lane;
-        double prod = 0.0;
-        if (t < k) {
-          const int64_t nb = S[j * k + t];
-          const double dist = sqrt(dist_sq_fixed<D>(q, X + nb * D));
-          prod = __dmul_rn(kernel_eval(dist, kp), Cf[(j * k + t) * m + cc]);
+      for (int t = lane; t < k; t += kWarp) {
+        const int64_t nb = S[j * k + t];
+        const double* xn = X + nb * D;
+        const double d0 = q[0] - xn[0];
+        double dsq = d0 * d0;
+#pragma unroll
+        for (int u = 1; u < D; ++u) {
+          const double du = q[u] - xn[u];
+          dsq = fma(du, du, dsq);
         }
-        const int cnt = min(kWarp, k - t0);
-        for (int s2 = 0; s2 < cnt; ++s2) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, prod, s2));
+        acc = fma(kernel_from_sq_build<KF>(dsq, kc, kp), Cf[(j * k + t) * m + cc], acc);
       }
-      if (lane == 0) out[orow * m + cc] = __dadd_rn(acc, mean_offset[cc]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) out[orow * m + cc] = acc + mean_offset[cc];
     }
   }
 }
@@ -1065,7 +1132,8 @@ template <int D>
 cudaError_t predict_grid_d(const double* X, int64_t n, const int32_t* S, const double* Cf, int k, int m,
                            const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz, double* out,
                            int32_t* nn_out, int num_sms, cudaStream_t s) {
-  const double per_cell = (D == 1) ? 4.0 : (D == 2 ? 4.0 : 3.0);  // ~1 neighbour wanted: small cells
+  // ~1 neighbour wanted: small cells (d = 2, 3: the 3^D block of the ordered walk)
+  const double per_cell = (D == 1) ? 4.0 : (D == 2 ? 1.5 : 1.0);
   const int64_t ncap = n;
   GridParams* gp = nullptr;
   unsigned long long* mm = nullptr;
@@ -1086,8 +1154,20 @@ cudaError_t predict_grid_d(const double* X, int64_t n, const int32_t* S, const d
   const int64_t cap = static_cast<int64_t>(num_sms) * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  grid_predict_kernel<D><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(
-      gp, pb.pts, pb.pid, pb.cstart, nz, qb.pts, qb.pid, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out);
+  switch (kp.kind == 1 ? 0 : 1 + kp.nu_code) {  // kernel_code(), evaluated on the host
+#define FMGP_PRED_CASE(KF)                                                                                  \
+  case KF:                                                                                                  \
+    grid_predict_kernel<D, KF><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                     \
+        gp, pb.pts, pb.pid, pb.cstart, nz, qb.pts, qb.pid, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out); \
+    break;
+    FMGP_PRED_CASE(0)
+    FMGP_PRED_CASE(1)
+    FMGP_PRED_CASE(2)
+    FMGP_PRED_CASE(3)
+    default:
+      FMGP_PRED_CASE(4)
+#undef FMGP_PRED_CASE
+  }
   note_launches(1);
   err = cudaGetLastError();
   cudaFreeAsync(gp, s);
