@@ -23,6 +23,8 @@
 // fmgp_common.cuh (kernel_from_sq_build). The factorisation is branch-free:
 // a failed pivot is recorded in a flag and the jitter ladder retried after
 // the sweep (Eigen LLT semantics: success iff every pivot > 0).
+#include <cstdlib>
+
 #include "fmgp_common.cuh"
 #include "fmgp_internal.h"
 
@@ -95,18 +97,18 @@ __device__ __forceinline__ void load_pair(const double* xs, uint32_t t, double (
 // One pair per lane per step; the next step's table entry and coordinates are
 // loaded before the current entry is evaluated (the loop is latency-bound on
 // the table -> coordinate shared-memory chain otherwise).
-template <int K, int D, int KF>
+template <int K, int D, int KF, int NL = kWarp>
 __device__ __forceinline__ void pair_loop(const double* xs, const uint32_t* ptab, const KParams& kp, double* A,
                                           int lane) {
   constexpr int npairs = (K * (K - 1)) / 2;
-  static_assert(npairs >= kWarp, "first step loads one entry per lane");
+  static_assert(npairs >= NL, "first step loads one entry per lane");
   const double c = kernel_scale_build<KF>(kp);
   uint32_t t = ptab[lane];
   double u[D], w[D];
   load_pair<D>(xs, t, u, w);
 #pragma unroll 1
-  for (int e = lane; e < npairs; e += kWarp) {
-    const int en = e + kWarp;
+  for (int e = lane; e < npairs; e += NL) {
+    const int en = e + NL;
     const uint32_t tn = ptab[en < npairs ? en : e];
     double un[D], wn[D];
     load_pair<D>(xs, tn, un, wn);
@@ -377,6 +379,273 @@ __device__ void back_solve_reg(const double* A, const double* dinv, double* __re
   }
 }
 
+// ---------------------------------------------------------------- K2-pair
+// (A/B variant, FMGP_SOLVE_PAIR=1; profiles/r01/ab_pair_solve.txt.)
+// Two neighbourhoods per warp, one per half-warp (lanes 0-15 / 16-31), for
+// the small-d shapes. Why: the register sweep above is bound by the
+// shared-memory data pipe, and its largest consumer is the pivot-row
+// broadcast (every lane reads L_j. for its one or two rows; a broadcast
+// 128-bit load costs two wavefronts per 16 bytes). With 16 lanes per
+// neighbourhood each lane owns up to four rows, so one broadcast feeds up to
+// four FMAs per lane, and a single load instruction serves both halves
+// (each half-warp is one wavefront anyway): half the pivot traffic, half the
+// per-column pivot/rsqrt/shuffle overhead and fewer idle FMA lanes per
+// neighbourhood, at the cost of half as many warps (the shared memory per
+// neighbourhood, not registers, caps the neighbourhoods in flight).
+//
+// Ownership within a half (hl = lane & 15, R = k + m rows, NS = ceil(R/16)
+// slots): slot s holds row base(s) + hl, base(s) = R - 16 (NS - s) (rows < 0
+// absent). Slot s finishes at column base(s) + 15, so its entries are loaded
+// in stages: at column end(t-1) every slot s >= t loads its (still original)
+// entries end(t-1) .. end(t)-1, end(s) = min(base(s) + 16, k).
+template <int K, int M>
+struct PairShape {
+  static constexpr int kRows = K + M;
+  static constexpr int kNS = (kRows + 15) / 16;
+  static_assert(kNS <= 4, "at most four row slots per lane");
+  __host__ __device__ static constexpr int base(int s) { return kRows - 16 * (kNS - s); }
+  __host__ __device__ static constexpr int end(int s) { return base(s) + 16 < K ? base(s) + 16 : K; }
+  __host__ __device__ static constexpr int start(int t) { return t == 0 ? 0 : end(t - 1); }
+  __host__ __device__ static constexpr int owner_slot(int j) { return (j - base(0)) / 16; }
+};
+
+template <int K, int M>
+__device__ bool factor_pair(double* A, double* dinv, int lane) {
+  using Ps = PairShape<K, M>;
+  using Sh = RegShape<K, M>;
+  constexpr int NS = Ps::kNS;
+  const int hl = lane & 15;
+  const int hbase = lane & 16;
+  double x[NS][K];
+  double* Rs[NS];
+  int rs[NS];
+  bool vs[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    rs[s] = Ps::base(s) + hl;
+    vs[s] = rs[s] >= 0 && rs[s] < Sh::kRows;
+    Rs[s] = A + Sh::row_off(vs[s] ? rs[s] : 0);
+  }
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      if (j == Ps::start(t) && Ps::start(t) < Ps::end(t)) {
+        // stage t: slots >= t load entries start(t) .. end(t)-1 (original values; entries
+        // beyond a row's length read the next packed row and are never used)
+#pragma unroll
+        for (int s = t; s < NS; ++s) {
+          int p = Ps::start(t);
+          if (p & 1) {
+            x[s][p] = Rs[s][p];
+            ++p;
+          }
+#pragma unroll
+          for (; p + 1 < Ps::end(t); p += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(Rs[s] + p);
+            x[s][p] = v.x;
+            x[s][p + 1] = v.y;
+          }
+          if (p < Ps::end(t)) x[s][p] = Rs[s][p];
+        }
+      }
+    }
+    const double* Lj = A + ro_r(j);  // pivot row j (entries < j are final)
+    double acc[NS][4];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const bool act = Ps::base(s) + 15 >= j;
+      acc[s][0] = act ? x[s][act ? j : 0] : 0.0;
+      acc[s][1] = acc[s][2] = acc[s][3] = 0.0;
+    }
+#pragma unroll
+    for (int p = 0; p + 3 < j; p += 4) {
+      const double2 l = *reinterpret_cast<const double2*>(Lj + p);
+      const double2 m = *reinterpret_cast<const double2*>(Lj + p + 2);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (Ps::base(s) + 15 >= j) {
+          acc[s][0] = fma(-x[s][p], l.x, acc[s][0]);
+          acc[s][1] = fma(-x[s][p + 1], l.y, acc[s][1]);
+          acc[s][2] = fma(-x[s][p + 2], m.x, acc[s][2]);
+          acc[s][3] = fma(-x[s][p + 3], m.y, acc[s][3]);
+        }
+      }
+    }
+    {
+      const int p0 = j & ~3;
+      if ((j & 3) >= 2) {
+        const double2 l = *reinterpret_cast<const double2*>(Lj + p0);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          if (Ps::base(s) + 15 >= j) {
+            acc[s][0] = fma(-x[s][p0], l.x, acc[s][0]);
+            acc[s][1] = fma(-x[s][p0 + 1], l.y, acc[s][1]);
+          }
+        }
+      }
+      if ((j & 1) == 1) {
+        const int q = j - 1;
+        const double l = Lj[q];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (Ps::base(s) + 15 >= j) acc[s][2] = fma(-x[s][q], l, acc[s][2]);
+      }
+    }
+    double sum[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) sum[s] = (acc[s][0] + acc[s][1]) + (acc[s][2] + acc[s][3]);
+    const int so = Ps::owner_slot(j);
+    const double piv = __shfl_sync(0xffffffffu, sum[so], hbase | (j - Ps::base(so)));
+    bad |= !(piv > 0.0);
+    const double inv = rsqrt_pivot(piv);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (Ps::base(s) + 15 >= j) {
+        const double v = sum[s] * inv;
+        x[s][j] = v;
+        if (vs[s] && rs[s] >= j) Rs[s][j] = v;
+      }
+    }
+    if (hl == 0) dinv[j] = inv;
+    __syncwarp();
+  }
+  return !bad;
+}
+
+// Backward solve L^T x = z per half: lane hl keeps x_p for p = hl, hl+16,
+// hl+32, ... in registers; x_j is broadcast within the half by a shuffle and
+// row j of L is read contiguously (16 lanes x 8 bytes per half).
+template <int K, int M>
+__device__ void back_solve_pair(const double* A, const double* dinv, double* __restrict__ Crow, bool store, int lane) {
+  using Sh = RegShape<K, M>;
+  constexpr int NY = (K + 15) / 16;
+  const int hl = lane & 15;
+  const int hbase = lane & 16;
+#pragma unroll 1
+  for (int c = 0; c < M; ++c) {
+    const double* z = A + Sh::row_off(K + c);
+    double y[NY];
+#pragma unroll
+    for (int t = 0; t < NY; ++t) y[t] = 16 * t + hl < K ? z[16 * t + hl < K ? 16 * t + hl : 0] : 0.0;
+#pragma unroll
+    for (int j = K - 1; j >= 0; --j) {
+      const double yj = __shfl_sync(0xffffffffu, y[j / 16], hbase | (j & 15));
+      const double xj = yj * dinv[j];
+      const double* Lj = A + ro_r(j);
+#pragma unroll
+      for (int t = 0; t < NY; ++t) {
+        if (16 * t > j) continue;
+        const int p = 16 * t + hl;
+        if (16 * t + 15 < j) {
+          y[t] = fma(-Lj[p], xj, y[t]);
+        } else {
+          if (p < j) y[t] = fma(-Lj[p < j ? p : 0], xj, y[t]);
+          if (p == j) y[t] = xj;
+        }
+      }
+    }
+    if (store) {
+#pragma unroll
+      for (int t = 0; t < NY; ++t)
+        if (16 * t + hl < K) Crow[(16 * t + hl) * M + c] = y[t];
+    }
+  }
+}
+
+// Small-d build of one half's neighbourhood with its 16 lanes.
+template <int K, int M, int D>
+__device__ void build_small_half(const double* __restrict__ X, const double* __restrict__ Y, const int32_t* sr,
+                                 const KParams& kp, int rung, double* A, double* xs, const uint32_t* ptab, int hl) {
+  using Sh = RegShape<K, M>;
+  for (int e = hl; e < K * D; e += 16) {
+    const int t = e / D, c = e - t * D;
+    xs[e] = X[static_cast<int64_t>(sr[t]) * D + c];
+  }
+  __syncwarp();
+  switch (kernel_code(kp)) {
+    case 0: pair_loop<K, D, 0, 16>(xs, ptab, kp, A, hl); break;
+    case 1: pair_loop<K, D, 1, 16>(xs, ptab, kp, A, hl); break;
+    case 2: pair_loop<K, D, 2, 16>(xs, ptab, kp, A, hl); break;
+    case 3: pair_loop<K, D, 3, 16>(xs, ptab, kp, A, hl); break;
+    default: pair_loop<K, D, 4, 16>(xs, ptab, kp, A, hl); break;
+  }
+  const double dg = jitter_r(kp.diag, rung);
+  for (int i = hl; i < K; i += 16) A[ro_r(i) + i] = dg;
+  for (int e = hl; e < K * M; e += 16) {
+    const int t = e / M, c = e - t * M;
+    A[Sh::row_off(K + c) + t] = Y[static_cast<int64_t>(sr[t]) * M + c];
+  }
+  __syncwarp();
+}
+
+constexpr int kPairWarps = 4;
+
+template <int K, int M, int D>
+__global__ void __launch_bounds__(kPairWarps * kWarp, 2)
+solve_pair_kernel(const double* __restrict__ X, const double* __restrict__ Y, const int32_t* __restrict__ S,
+                  int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
+                  unsigned long long* __restrict__ fail_min) {
+  using Sh = RegShape<K, M>;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x % kWarp;
+  const int warp = threadIdx.x / kWarp;
+  const int warps = blockDim.x / kWarp;
+  const int h = lane >> 4, hl = lane & 15;
+  uint32_t* ptab = reinterpret_cast<uint32_t*>(smem);
+  fill_pair_table<K>(ptab);
+  __syncthreads();
+  double* A = smem + Sh::kTabDoubles + (2 * warp + h) * Sh::per_warp(D);
+  double* dinv = A + Sh::kAug;
+  double* xs = dinv + ((K + 1) & ~1);
+  int32_t* sr = reinterpret_cast<int32_t*>(xs + Sh::xs_doubles(D));
+  for (int64_t pr = static_cast<int64_t>(blockIdx.x) * warps + warp; 2 * pr < nrows;
+       pr += static_cast<int64_t>(gridDim.x) * warps) {
+    const int64_t r = 2 * pr + h;
+    const bool has = r < nrows;
+    const int64_t rr = has ? r : 2 * pr;  // a missing second row repeats the first (never stored)
+    for (int t = hl; t < K; t += 16) sr[t] = S[rr * K + t];
+    __syncwarp();
+    int rung = 0;
+    bool ok = false;
+    for (int it = 0; it < 4; ++it) {
+      build_small_half<K, M, D>(X, Y, sr, kp, rung, A, xs, ptab, hl);
+      ok = factor_pair<K, M>(A, dinv, lane);
+      __syncwarp();
+      // a half that failed moves to the next jitter rung; a half that succeeded
+      // repeats its rung (same arithmetic, same result) while the other retries
+      const bool retry = !ok && rung < 3;
+      if (!__any_sync(0xffffffffu, retry)) break;
+      if (retry) ++rung;
+    }
+    if (!ok && has && hl == 0) atomicMin(fail_min, static_cast<unsigned long long>(row_begin + r));
+    back_solve_pair<K, M>(A, dinv, C + r * K * M, ok && has, lane);
+    __syncwarp();
+  }
+}
+
+template <int K, int M, int D>
+cudaError_t launch_pair(const double* X, const double* Y, const int32_t* S, int64_t nrows, int64_t row_begin,
+                        const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
+  using Sh = RegShape<K, M>;
+  const size_t smem = sizeof(double) * (Sh::kTabDoubles + 2 * Sh::per_warp(D) * kPairWarps);
+  cudaError_t err = cudaFuncSetAttribute(solve_pair_kernel<K, M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  int per_sm = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_pair_kernel<K, M, D>, kPairWarps * kWarp, smem);
+  if (err != cudaSuccess) return err;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t pairs = (nrows + 1) / 2;
+  const int64_t need = (pairs + kPairWarps - 1) / kPairWarps;
+  const int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(num_sms) * per_sm);
+  solve_pair_kernel<K, M, D><<<static_cast<unsigned>(grid), kPairWarps * kWarp, smem, stream>>>(
+      X, Y, S, nrows, row_begin, kp, C, fail_min);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
 // CTA shape: 4 warps (one pair table per 4 neighbourhoods in flight), 4 CTAs
 // per SM: <= 128 registers per thread, 16 warps per SM.
 template <int K, int M>
@@ -461,6 +730,19 @@ cudaError_t fused_solve_reg(const double* X, const double* Y, int d, int m, cons
   if (nrows <= 0) return cudaSuccess;
 #define FMGP_REG_CASE(KK, MM, DD) \
   return launch_reg<KK, MM, DD>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream)
+  // FMGP_SOLVE_PAIR=1 selects two neighbourhoods per warp for small d (A/B:
+  // fewer instructions and shared wavefronts per row, but only 8 warps/SM fit
+  // and it is latency-bound: cfg2 solve 14.2 ms vs 13.9 ms for the default)
+  static const bool pair = [] {
+    const char* e = std::getenv("FMGP_SOLVE_PAIR");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (pair && m == 1 && (d == 2 || d == 3) && (k == 50 || k == 30)) {
+    if (k == 50) return d == 2 ? launch_pair<50, 1, 2>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream)
+                               : launch_pair<50, 1, 3>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+    return d == 2 ? launch_pair<30, 1, 2>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream)
+                  : launch_pair<30, 1, 3>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+  }
   if (k == 50 && m == 1) {
     if (d == 2) FMGP_REG_CASE(50, 1, 2);
     if (d == 3) FMGP_REG_CASE(50, 1, 3);
