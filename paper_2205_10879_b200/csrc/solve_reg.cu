@@ -23,6 +23,7 @@
 // fmgp_common.cuh (kernel_from_sq_build). The factorisation is branch-free:
 // a failed pivot is recorded in a flag and the jitter ladder retried after
 // the sweep (Eigen LLT semantics: success iff every pivot > 0).
+#include <climits>
 #include <cstdlib>
 
 #include "fmgp_common.cuh"
@@ -33,6 +34,10 @@ namespace fmgp {
 namespace {
 
 __constant__ double kJitR[4] = {0.0, 1e-10, 1e-8, 1e-6};
+
+// The Gram build replaces the direct difference loop from this dimension on
+// (FMGP_SOLVE_GRAM=0 turns it off for A/B checks).
+constexpr int kGramMinD = 32;
 
 __host__ __device__ constexpr int ro_r(int i) { return ((i * (i + 1)) >> 1) + ((i + 1) >> 1); }
 
@@ -53,7 +58,13 @@ struct RegShape {
   static constexpr int kDch = 16;                      // coordinate slice width staged per pass
   static constexpr int kXsStride = kDch + 2;           // = 2 mod 4 doubles: conflict-light 128-bit row loads
   // xs holds K x D coordinates for the small-d build (D > 0), K x kXsStride slices otherwise
-  __host__ __device__ static constexpr int xs_doubles(int D) { return D > 0 ? ((K * D + 1) & ~1) : kXsStride * K; }
+  // Gram build (d >= kGramMinD, K <= 32): 32 rows x kGramS doubles of one
+  // 16-dimension chunk plus the 32 Gram diagonal entries
+  static constexpr int kGramS = 20;  // row stride = 4 mod 16 doubles: conflict-free fragment loads
+  static constexpr int kGramXs = 32 * kGramS + 32;
+  __host__ __device__ static constexpr int xs_doubles(int D) {
+    return D > 0 ? ((K * D + 1) & ~1) : (K <= 32 && kGramXs > kXsStride * K ? kGramXs : kXsStride * K);
+  }
   __host__ __device__ static constexpr int per_warp(int D) {
     return ((kAug + ((K + 1) & ~1) /*dinv*/ + xs_doubles(D) + (K + 1) / 2 + 2) + 1) & ~1;
   }
@@ -238,6 +249,110 @@ __device__ void build_reg(const double* __restrict__ X, const double* __restrict
   for (int e = lane; e < K * M; e += kWarp) {
     const int t = e / M, c = e - t * M;
     A[Sh::row_off(K + c) + t] = Y[static_cast<int64_t>(sr[t]) * M + c];
+  }
+  __syncwarp();
+}
+
+// Large-d build (D = 0, K <= 32) on the FP64 tensor cores: the Gram matrix
+// G = X_N X_N^T of the neighbourhood's coordinates (rows padded to 32) is
+// accumulated with DMMA m8n8k4 over 16-dimension chunks staged in shared
+// memory (lane (g, t) holds X[8I + g][c + t], which is both the A fragment of
+// row block I and the B fragment of column block I, so one 64-bit load per
+// block and k-step feeds the 10 lower-triangle tiles), then
+// d^2 = G_ii + G_jj - 2 G_ij (clamped at 0) feeds the kernel. Cost per pair
+// ~2d/16 DMMA-thread ops instead of 2d scalar ops with two shared loads; the
+// distance differs from the reference's sum of squared differences by
+// rounding relative to |x|^2 (1e-15 at cfg3), far inside the coefficient
+// tolerance. A pair with d^2 <= 1e-12 (G_ii + G_jj) is recomputed exactly
+// from X (sum of squared differences), so exact duplicates keep the nugget
+// (kernel.cpp:106-119) bit for bit. The next chunk's coordinates are loaded
+// from global memory while the current chunk's MMAs run.
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int K, int M>
+__device__ void build_gram(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* sr,
+                           const KParams& kp, int attempt, double* A, double* xs, int lane) {
+  using Sh = RegShape<K, M>;
+  static_assert(K <= 32, "one 32-row Gram block");
+  constexpr int S = Sh::kGramS;
+  double* gd = xs + 32 * S;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int I = 0; I < 4; ++I)
+#pragma unroll
+    for (int J = 0; J < 4; ++J) acc[I][J][0] = acc[I][J][1] = 0.0;
+  // gather slots: element e = lane + 32 u of a 32 x 16 chunk is (row e >> 4, dim e & 15)
+  const int64_t rowoff0 = static_cast<int64_t>(sr[lane >> 4 < K ? lane >> 4 : 0]) * d;
+  double pre[16];
+  auto gather = [&](int c0) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int row = (lane >> 4) + 2 * u, dim = lane & 15;
+      const bool ok = row < K && c0 + dim < d;
+      pre[u] = ok ? X[static_cast<int64_t>(sr[row < K ? row : 0]) * d + c0 + dim] : 0.0;
+    }
+  };
+  (void)rowoff0;
+  gather(0);
+  for (int c0 = 0; c0 < d; c0 += 16) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) xs[((lane >> 4) + 2 * u) * S + (lane & 15)] = pre[u];
+    __syncwarp();
+    if (c0 + 16 < d) gather(c0 + 16);
+#pragma unroll
+    for (int kq = 0; kq < 16; kq += 4) {
+      double f[4];
+#pragma unroll
+      for (int I = 0; I < 4; ++I) f[I] = xs[(8 * I + g) * S + kq + t];
+#pragma unroll
+      for (int I = 0; I < 4; ++I)
+#pragma unroll
+        for (int J = 0; J <= I; ++J) dmma_884(acc[I][J], f[I], f[J]);
+    }
+    __syncwarp();
+  }
+  // Gram diagonal -> shared memory
+#pragma unroll
+  for (int I = 0; I < 4; ++I) {
+    if (g == 2 * t) gd[8 * I + g] = acc[I][I][0];
+    if (g == 2 * t + 1) gd[8 * I + g] = acc[I][I][1];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int I = 0; I < 4; ++I) {
+#pragma unroll
+    for (int J = 0; J <= I; ++J) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+        if (r < K && c < r) {
+          const double gr = gd[r], gc = gd[c];
+          double d2 = fmax(gr + gc - 2.0 * acc[I][J][e], 0.0);
+          if (d2 <= 1e-12 * (gr + gc)) {  // near or exact duplicate: the exact key decides
+            const double* xa = X + static_cast<int64_t>(sr[r]) * d;
+            const double* xb = X + static_cast<int64_t>(sr[c]) * d;
+            double ex = 0.0;
+            for (int q = 0; q < d; ++q) {
+              const double df = xa[q] - xb[q];
+              ex = fma(df, df, ex);
+            }
+            d2 = ex;
+          }
+          A[ro_r(r) + c] = kernel_eval_fast(sqrt(d2), kp);
+        }
+      }
+    }
+  }
+  const double dg = jitter_r(kp.diag, attempt);
+  for (int i = lane; i < K; i += kWarp) A[ro_r(i) + i] = dg;
+  for (int e = lane; e < K * M; e += kWarp) {
+    const int tt = e / M, cc = e - tt * M;
+    A[Sh::row_off(K + cc) + tt] = Y[static_cast<int64_t>(sr[tt]) * M + cc];
   }
   __syncwarp();
 }
@@ -658,7 +773,7 @@ template <int K, int M, int D>
 __global__ void __launch_bounds__(RegLaunch<K, M>::kWarps * kWarp, RegLaunch<K, M>::kMinBlocks)
 solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
                  int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
-                 unsigned long long* __restrict__ fail_min) {
+                 unsigned long long* __restrict__ fail_min, int gram_min_d) {
   using Sh = RegShape<K, M>;
   extern __shared__ double smem[];
   const int lane = threadIdx.x % kWarp;
@@ -682,7 +797,17 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
       if constexpr (D > 0)
         build_small<K, M, D>(X, Y, sr, kp, attempt, A, xs, ptab, lane);
       else
-        build_reg<K, M>(X, Y, d, sr, kp, attempt, A, xs, lane);
+      {
+        if constexpr (K <= 32) {
+          if (d >= gram_min_d) {
+            build_gram<K, M>(X, Y, d, sr, kp, attempt, A, xs, lane);
+          } else {
+            build_reg<K, M>(X, Y, d, sr, kp, attempt, A, xs, lane);
+          }
+        } else {
+          build_reg<K, M>(X, Y, d, sr, kp, attempt, A, xs, lane);
+        }
+      }
       ok = factor_reg<K, M>(A, dinv, lane);
       __syncwarp();
     }
@@ -711,8 +836,12 @@ cudaError_t launch_reg(const double* X, const double* Y, int d, const int32_t* S
   if (per_sm < 1) per_sm = 1;
   const int64_t need = (nrows + kWarps - 1) / kWarps;
   const int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(num_sms) * per_sm);
-  solve_reg_kernel<K, M, D><<<static_cast<unsigned>(grid), kWarps * kWarp, smem, stream>>>(X, Y, d, S, nrows, row_begin,
-                                                                                        kp, C, fail_min);
+  static const int gram_min_d = [] {
+    const char* e = std::getenv("FMGP_SOLVE_GRAM");
+    return (e != nullptr && e[0] == '0') ? INT_MAX : kGramMinD;
+  }();
+  solve_reg_kernel<K, M, D><<<static_cast<unsigned>(grid), kWarps * kWarp, smem, stream>>>(
+      X, Y, d, S, nrows, row_begin, kp, C, fail_min, gram_min_d);
   note_launches(1);
   return cudaGetLastError();
 }
