@@ -159,7 +159,7 @@ def test_linear_in_y_and_sigma_invariant(fm):
     assert np.abs(s - a).max() <= 1e-10
 
 
-@pytest.mark.parametrize("k,d", [(8, 2), (30, 2), (50, 2), (50, 3), (100, 2), (100, 40)])
+@pytest.mark.parametrize("k,d", [(8, 2), (30, 2), (50, 2), (50, 3), (100, 2), (100, 40), (30, 40)])
 def test_numeric_error_names_lowest_failing_row(fm, port, k, d):
     # Exact duplicates with tau = 0 give an exactly singular block; with sigma = 1e6
     # the jitter rungs (<= 1e-6) are below one ulp of the diagonal, so the ladder
@@ -310,3 +310,25 @@ def test_split_knn_and_chunked_async_solve_equal_precompute_device(fm):
                       fm.FittedParams(fm.KernelParams(1e6, 1.0, 2.5, 0.0), fm.KernelKind.RBF),
                       fm.NeighborIndex.build(Xf), 8)
     assert int(fail.item()) == ei.value.failed_row
+
+
+@pytest.mark.parametrize("m", [1, 10])
+@pytest.mark.parametrize("d", [32, 100, 784])
+def test_gram_build_matches_oracle(fm, port, d, m):
+    # k = 30 at d >= 32 builds the neighbourhood matrices from a DMMA Gram
+    # matrix (solve_reg.cu build_gram), on sparse cfg3-like rows. Exact
+    # duplicates (d^2 = 0 -> nugget, an exactly singular block) are covered by
+    # test_numeric_error_names_lowest_failing_row[30-40]: the ladder is only
+    # exhausted there if the Gram path detects the zero distance exactly.
+    rng = np.random.default_rng(7 * d + m)
+    n, k = 600, 30
+    X = rng.random((n, d)) * (rng.random((n, d)) < 0.2)
+    Y = rng.standard_normal((n, m))
+    p = fm.KernelParams(1.0, 10.0, 0.5, 0.1)
+    model = fm.precompute(fm.TrainingSet(X, Y if m > 1 else Y[:, 0], 0.0),
+                          fm.FittedParams(p, fm.KernelKind.Matern), fm.NeighborIndex.build(X), k)
+    rows = np.arange(0, n, 9)
+    S_o, C_o = port.precompute_rows(X, Y, 0, 1.0, 10.0, 0.5, 0.1, k, rows)
+    assert np.array_equal(model.S[rows], S_o)
+    err = row_rel_err(model.C.reshape(n, k, -1)[rows], C_o)
+    assert err.max() <= C_TOL, err.max()
