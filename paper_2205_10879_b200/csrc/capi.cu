@@ -1,3 +1,4 @@
+#include <chrono>
 // The C ABI (include/fmgp_b200.h): argument checks with the reference's
 // error conventions, device memory and streams, and the stage launchers.
 // There is no CPU compute path: without a usable CUDA device every compute
@@ -144,14 +145,32 @@ static int precompute_host_rows(const double* X, const double* Y, int64_t n, int
   int rc;
   if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
   if (k < 1 || k > n) return fail(FMGP_EINVAL, "precompute: k out of range");
-  if ((rc = check_points(X, n, d)) != FMGP_OK) return rc;
+  // shape checks now; the finiteness scan of X runs below, while X and Y copy
+  if ((rc = check_points(nullptr, n, d)) != FMGP_OK) return rc;
   if ((rc = check_solve_shape(k, d, m)) != FMGP_OK) return rc;
   if (row_begin < 0 || row_end > n || row_begin > row_end) return fail(FMGP_EINVAL, "precompute: bad row range");
-  if ((rc = require_device()) != FMGP_OK) return rc;
+  if ((rc = require_device()) != FMGP_OK) {  // argument errors still take precedence
+    if (!all_finite(X, n * d)) return fail(FMGP_EINVAL, "NeighborIndex: non-finite coordinates");
+    return rc;
+  }
   const int64_t rows = row_end - row_begin;
-  if (rows == 0) return FMGP_OK;
+  if (rows == 0) return all_finite(X, n * d) ? FMGP_OK : fail(FMGP_EINVAL, "NeighborIndex: non-finite coordinates");
   Stream st;
   FMGP_CUDA(st.create());
+  // FMGP_TRACE=1: stage timeline of this call on stderr (CUDA events on the
+  // work and read-back streams, host issue time), for the e2e breakdown
+  static const bool trace = [] {
+    const char* e = std::getenv("FMGP_TRACE");
+    return e != nullptr && e[0] == '1';
+  }();
+  const auto host_t0 = std::chrono::steady_clock::now();
+  cudaEvent_t tev[6] = {};
+  if (trace)
+    for (auto& e : tev) cudaEventCreate(&e);
+  auto mark = [&](int i, cudaStream_t s) {
+    if (trace) cudaEventRecord(tev[i], s);
+  };
+  mark(0, st.s);
   DevBuf<double> dX, dY, dC;
   DevBuf<int32_t> dS;
   FMGP_CUDA(dX.alloc(static_cast<size_t>(n) * d, st.s));
@@ -160,13 +179,19 @@ static int precompute_host_rows(const double* X, const double* Y, int64_t n, int
   FMGP_CUDA(dC.alloc(static_cast<size_t>(rows) * k * m, st.s));
   FMGP_CUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * n * d, cudaMemcpyHostToDevice, st.s));
   FMGP_CUDA(cudaMemcpyAsync(dY.p, Y, sizeof(double) * n * m, cudaMemcpyHostToDevice, st.s));
+  if (!all_finite(X, n * d)) {  // overlaps the copies; nothing has been launched on X yet
+    cudaStreamSynchronize(st.s);
+    return fail(FMGP_EINVAL, "NeighborIndex: non-finite coordinates");
+  }
   const int sms = num_sms_current();
+  mark(1, st.s);
   if (k > 1) {
     FMGP_CUDA(fmgp::knn_exact(dX.p + static_cast<size_t>(row_begin) * d, rows, dX.p, n, d, k - 1, row_begin, nullptr,
                               1, dS.p, nullptr, sms, st.s));
   } else {
     FMGP_CUDA(fmgp::self_rows_launch(dS.p, rows, row_begin, st.s));
   }
+  mark(2, st.s);
   Stream rb_st;
   FMGP_CUDA(rb_st.create());
   std::vector<cudaEvent_t> evs;
@@ -198,10 +223,25 @@ static int precompute_host_rows(const double* X, const double* Y, int64_t n, int
     FMGP_CUDA(handoff());
     FMGP_CUDA(cudaMemcpyAsync(C_out + c0, dC.p + c0, sizeof(double) * cn, cudaMemcpyDeviceToHost, rb_st.s));
   }
+  mark(3, st.s);
+  mark(4, rb_st.s);
+  const double host_issue_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
   unsigned long long host_min = ~0ull;
   FMGP_CUDA(cudaMemcpyAsync(&host_min, fmin.p, sizeof(host_min), cudaMemcpyDeviceToHost, st.s));
   FMGP_CUDA(cudaStreamSynchronize(st.s));
   FMGP_CUDA(cudaStreamSynchronize(rb_st.s));
+  if (trace) {
+    float t[5] = {};
+    for (int i = 1; i < 5; ++i) cudaEventElapsedTime(&t[i], tev[0], tev[i]);
+    const double host_total_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    std::fprintf(stderr,
+                 "[fmgp trace] precompute rows %lld: h2d done %.3f ms, kNN done %.3f, solve done %.3f, "
+                 "read-back done %.3f (device, from call start); host issue %.3f ms, host total %.3f ms\n",
+                 static_cast<long long>(rows), t[1], t[2], t[3], t[4], host_issue_ms, host_total_ms);
+    for (auto e : tev) cudaEventDestroy(e);
+  }
   if (host_min != ~0ull) {
     if (failed_row) *failed_row = static_cast<int64_t>(host_min);
     return fail(FMGP_ENUMERIC, "Cholesky factorization failed in precompute row " + std::to_string(host_min) +
