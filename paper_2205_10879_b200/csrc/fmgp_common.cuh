@@ -313,7 +313,10 @@ __device__ __forceinline__ double rsqrt_pivot(double x) {
 // 2^-(m>>6) applied as an exponent-field subtraction on the table value
 // (a <= 708 keeps the result normal). Within 2 ulp of exp(-a).
 __device__ __forceinline__ double exp_neg_build(double a) {
-  a = a < 708.0 ? a : 708.0;  // also maps NaN (an overflowed distance) to the clamp
+  // a >= 0: clamp at 708 (0x40862000'00000000) by the high word, an integer
+  // compare + two selects (a double compare compiles to fmin with NaN fix-ups);
+  // NaN (an overflowed distance) also maps to the clamp
+  a = __double2hiint(a) < 0x40862000 ? a : 708.0;
   const double tm = fma(a, 92.33248261689366, 6755399441055744.0);
   const int m = __double2loint(tm);
   const double mf = tm - 6755399441055744.0;
