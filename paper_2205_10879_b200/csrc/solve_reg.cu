@@ -105,53 +105,60 @@ __device__ __forceinline__ void load_pair(const double* xs, uint32_t t, double (
   }
 }
 
-// Two pairs per lane per step (e and e + NL, independent: their sqrt/exp
+// PP pairs per lane per step (e, e + NL, ..., independent: their sqrt/exp
 // chains interleave); the next step's table words and coordinates are loaded
 // at the top of the step, so the shared-memory chain table -> coordinates
 // has a whole step of arithmetic to complete behind.
+#ifndef FMGP_BUILD_PP
+#define FMGP_BUILD_PP 4
+#endif
 template <int K, int D, int KF, int NL = kWarp>
 __device__ __forceinline__ void pair_loop(const double* xs, const uint32_t* ptab, const KParams& kp, double* A,
                                           int lane) {
+  constexpr int PP = FMGP_BUILD_PP;
   constexpr int npairs = (K * (K - 1)) / 2;
-  static_assert(npairs >= 2 * NL, "first step loads two entries per lane");
+  static_assert(npairs >= PP * NL, "first step loads PP entries per lane");
   const double c = kernel_scale_build<KF>(kp);
-  uint32_t t0 = ptab[lane], t1 = ptab[lane + NL];
-  double u0[D], w0[D], u1[D], w1[D];
-  load_pair<D>(xs, t0, u0, w0);
-  load_pair<D>(xs, t1, u1, w1);
+  uint32_t t[PP];
+  double u[PP][D], w[PP][D];
+#pragma unroll
+  for (int i = 0; i < PP; ++i) {
+    t[i] = ptab[lane + i * NL];
+    load_pair<D>(xs, t[i], u[i], w[i]);
+  }
 #pragma unroll 1
-  for (int e = lane; e < npairs; e += 2 * NL) {
-    const bool has1 = e + NL < npairs;
-    const int f0 = e + 2 * NL, f1 = e + 3 * NL;
-    const uint32_t n0 = ptab[f0 < npairs ? f0 : e];
-    const uint32_t n1 = ptab[f1 < npairs ? f1 : e];
-    double un0[D], wn0[D], un1[D], wn1[D];
-    load_pair<D>(xs, n0, un0, wn0);
-    load_pair<D>(xs, n1, un1, wn1);
-    double acc0, acc1;
-    {
-      const double d0 = u0[0] - w0[0], d1 = u1[0] - w1[0];
-      acc0 = d0 * d0;
-      acc1 = d1 * d1;
+  for (int e = lane; e < npairs; e += PP * NL) {
+    uint32_t tn[PP];
+    double un[PP][D], wn[PP][D];
+#pragma unroll
+    for (int i = 0; i < PP; ++i) {
+      const int f = e + (PP + i) * NL;
+      tn[i] = ptab[f < npairs ? f : e];
+      load_pair<D>(xs, tn[i], un[i], wn[i]);
+    }
+    double v[PP];
+#pragma unroll
+    for (int i = 0; i < PP; ++i) {
+      const double d0 = u[i][0] - w[i][0];
+      double acc = d0 * d0;
 #pragma unroll
       for (int cc = 1; cc < D; ++cc) {
-        const double a0 = u0[cc] - w0[cc], a1 = u1[cc] - w1[cc];
-        acc0 = fma(a0, a0, acc0);
-        acc1 = fma(a1, a1, acc1);
+        const double dd = u[i][cc] - w[i][cc];
+        acc = fma(dd, dd, acc);
       }
+      v[i] = kernel_from_sq_build<KF>(acc, c, kp);
     }
-    const double v0 = kernel_from_sq_build<KF>(acc0, c, kp);
-    const double v1 = kernel_from_sq_build<KF>(acc1, c, kp);
-    A[t0 >> 16] = v0;
-    if (has1) A[t1 >> 16] = v1;
-    t0 = n0;
-    t1 = n1;
 #pragma unroll
-    for (int cc = 0; cc < D; ++cc) {
-      u0[cc] = un0[cc];
-      w0[cc] = wn0[cc];
-      u1[cc] = un1[cc];
-      w1[cc] = wn1[cc];
+    for (int i = 0; i < PP; ++i)
+      if (i == 0 || e + i * NL < npairs) A[t[i] >> 16] = v[i];
+#pragma unroll
+    for (int i = 0; i < PP; ++i) {
+      t[i] = tn[i];
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) {
+        u[i][cc] = un[i][cc];
+        w[i][cc] = wn[i][cc];
+      }
     }
   }
 }
