@@ -423,8 +423,15 @@ __device__ bool factor_reg(double* A, double* dinv, int lane) {
   for (int j = 0; j < K; ++j) {
     if constexpr (kP > 0) {
       if (j == kP) {  // slot A is finished: bring in the rest of slot B (still original values)
+        constexpr int p0 = (kP + 1) & ~1;  // 128-bit loads from the first even entry
+        if constexpr (kP & 1) b[kP] = RB[kP];
 #pragma unroll
-        for (int p = kP; p < K; ++p) b[p] = RB[p];
+        for (int p = p0; p + 1 < K; p += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(RB + p);
+          b[p] = v.x;
+          b[p + 1] = v.y;
+        }
+        if constexpr ((K - p0) & 1) b[K - 1] = RB[K - 1];
       }
     }
     const bool twoA = kP > 0 && j < kP;
