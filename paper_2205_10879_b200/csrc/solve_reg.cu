@@ -112,10 +112,13 @@ __device__ __forceinline__ void load_pair(const double* xs, uint32_t t, double (
 #ifndef FMGP_BUILD_PP
 #define FMGP_BUILD_PP 4
 #endif
+#ifndef FMGP_BUILD_PP3
+#define FMGP_BUILD_PP3 2
+#endif
 template <int K, int D, int KF, int NL = kWarp>
 __device__ __forceinline__ void pair_loop(const double* xs, const uint32_t* ptab, const KParams& kp, double* A,
                                           int lane) {
-  constexpr int PP = FMGP_BUILD_PP;
+  constexpr int PP = D <= 2 ? FMGP_BUILD_PP : FMGP_BUILD_PP3;  // fewer in flight for d = 3 (registers)
   constexpr int npairs = (K * (K - 1)) / 2;
   static_assert(npairs >= PP * NL, "first step loads PP entries per lane");
   const double c = kernel_scale_build<KF>(kp);
