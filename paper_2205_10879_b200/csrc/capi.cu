@@ -177,13 +177,33 @@ static int precompute_host_rows(const double* X, const double* Y, int64_t n, int
   FMGP_CUDA(dY.alloc(static_cast<size_t>(n) * m, st.s));
   FMGP_CUDA(dS.alloc(static_cast<size_t>(rows) * k, st.s));
   FMGP_CUDA(dC.alloc(static_cast<size_t>(rows) * k * m, st.s));
+  // X goes first on the work stream (the kNN needs it); Y only feeds the solve,
+  // so it is copied on the read-back stream while the kNN runs
+  Stream rb_st;
+  FMGP_CUDA(rb_st.create());
   FMGP_CUDA(cudaMemcpyAsync(dX.p, X, sizeof(double) * n * d, cudaMemcpyHostToDevice, st.s));
-  FMGP_CUDA(cudaMemcpyAsync(dY.p, Y, sizeof(double) * n * m, cudaMemcpyHostToDevice, st.s));
-  if (!all_finite(X, n * d)) {  // overlaps the copies; nothing has been launched on X yet
-    cudaStreamSynchronize(st.s);
-    return fail(FMGP_EINVAL, "NeighborIndex: non-finite coordinates");
-  }
+  FMGP_CUDA(cudaMemcpyAsync(dY.p, Y, sizeof(double) * n * m, cudaMemcpyHostToDevice, rb_st.s));
+  cudaEvent_t y_ready;
+  FMGP_CUDA(cudaEventCreateWithFlags(&y_ready, cudaEventDisableTiming));
+  struct EvOne {
+    cudaEvent_t e;
+    ~EvOne() { cudaEventDestroy(e); }
+  } y_guard{y_ready};
+  FMGP_CUDA(cudaEventRecord(y_ready, rb_st.s));
   const int sms = num_sms_current();
+  {  // NeighborIndex::build's finiteness check, on the device copy of X (a 16 MB
+     // host scan costs ~1 ms of host time the kNN launch would wait for)
+    DevBuf<unsigned int> nbad;
+    FMGP_CUDA(nbad.alloc(1, st.s));
+    FMGP_CUDA(fmgp::nonfinite_count_launch(dX.p, n * d, nbad.p, sms, st.s));
+    unsigned int host_bad = 0;
+    FMGP_CUDA(cudaMemcpyAsync(&host_bad, nbad.p, sizeof(host_bad), cudaMemcpyDeviceToHost, st.s));
+    FMGP_CUDA(cudaStreamSynchronize(st.s));
+    if (host_bad != 0) {
+      cudaStreamSynchronize(rb_st.s);
+      return fail(FMGP_EINVAL, "NeighborIndex: non-finite coordinates");
+    }
+  }
   mark(1, st.s);
   if (k > 1) {
     FMGP_CUDA(fmgp::knn_exact(dX.p + static_cast<size_t>(row_begin) * d, rows, dX.p, n, d, k - 1, row_begin, nullptr,
@@ -192,8 +212,7 @@ static int precompute_host_rows(const double* X, const double* Y, int64_t n, int
     FMGP_CUDA(fmgp::self_rows_launch(dS.p, rows, row_begin, st.s));
   }
   mark(2, st.s);
-  Stream rb_st;
-  FMGP_CUDA(rb_st.create());
+  FMGP_CUDA(cudaStreamWaitEvent(st.s, y_ready, 0));  // the solve reads Y
   std::vector<cudaEvent_t> evs;
   struct EvGuard {
     std::vector<cudaEvent_t>& v;
@@ -214,14 +233,19 @@ static int precompute_host_rows(const double* X, const double* Y, int64_t n, int
   DevBuf<unsigned long long> fmin;
   FMGP_CUDA(fmin.alloc(1, st.s));
   FMGP_CUDA(cudaMemsetAsync(fmin.p, 0xFF, sizeof(unsigned long long), st.s));
-  const int64_t chunk = std::max<int64_t>(int64_t(1) << 15, (rows + 15) / 16);
-  for (int64_t rb = 0; rb < rows; rb += chunk) {
-    const int64_t re = std::min(rows, rb + chunk);
+  // chunks of rows/16, halving once fewer than two remain (down to 8192
+  // rows), so the read-back of the last chunk, which nothing hides, is short
+  const int64_t base = std::max<int64_t>(int64_t(1) << 15, (rows + 15) / 16);
+  for (int64_t rb = 0; rb < rows;) {
+    const int64_t left = rows - rb;
+    const int64_t chunk = left <= 8192 ? left : std::max<int64_t>(8192, std::min(base, (left + 1) / 2));
+    const int64_t re = rb + chunk;
     const size_t c0 = static_cast<size_t>(rb) * k * m, cn = static_cast<size_t>(re - rb) * k * m;
     FMGP_CUDA(fmgp::fused_solve(dX.p, dY.p, d, m, dS.p + static_cast<size_t>(rb) * k, re - rb, row_begin + rb, k, kp,
                                 dC.p + c0, nullptr, fmin.p, sms, st.s));
     FMGP_CUDA(handoff());
     FMGP_CUDA(cudaMemcpyAsync(C_out + c0, dC.p + c0, sizeof(double) * cn, cudaMemcpyDeviceToHost, rb_st.s));
+    rb = re;
   }
   mark(3, st.s);
   mark(4, rb_st.s);

@@ -45,6 +45,17 @@ __global__ void sqrt_kernel(double* __restrict__ v, int64_t n) {
     v[e] = sqrt(v[e]);
 }
 
+// Count of non-finite values (exponent field all ones), the device half of
+// NeighborIndex::build's finiteness check on the host-buffer path.
+__global__ void nonfinite_kernel(const double* __restrict__ v, int64_t n, unsigned int* __restrict__ count) {
+  unsigned int bad = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad += (__double2hiint(v[i]) & 0x7ff00000) == 0x7ff00000 ? 1u : 0u;
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(count, bad);
+}
+
 __global__ void self_rows_kernel(int32_t* __restrict__ S, int64_t nrows, int64_t row_begin) {
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nrows;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -95,6 +106,17 @@ cudaError_t distances_launch(const double* P, int d, const double* q, const int3
                              cudaStream_t stream) {
   if (cnt == 0) return cudaSuccess;
   distances_kernel<<<grid_for(cnt), 256, 0, stream>>>(P, d, q, idx, cnt, out);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t nonfinite_count_launch(const double* v, int64_t n, unsigned int* count, int num_sms,
+                                   cudaStream_t stream) {
+  cudaError_t err = cudaMemsetAsync(count, 0, sizeof(unsigned int), stream);
+  if (err != cudaSuccess || n <= 0) return err;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > static_cast<int64_t>(num_sms) * 8) blocks = static_cast<int64_t>(num_sms) * 8;
+  nonfinite_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(v, n, count);
   note_launches(1);
   return cudaGetLastError();
 }
