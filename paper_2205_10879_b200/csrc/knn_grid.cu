@@ -414,8 +414,14 @@ __device__ __forceinline__ int32_t ord_entry(int i) {
 // outside-the-block stop test. With cells of ~kk/6 (2-D) or ~kk/16 (3-D)
 // points this examines ~2x (2-D) to ~3x (3-D) fewer candidates than a radius-1
 // block of ~kk/2 points per cell, and returns the same rows.
+#ifndef FMGP_GQ_MINB
+#define FMGP_GQ_MINB 4
+#endif
+#ifndef FMGP_GP_MINB
+#define FMGP_GP_MINB 4
+#endif
 template <int D, int E>
-__global__ void __launch_bounds__(kQueryThreads, 3)
+__global__ void __launch_bounds__(kQueryThreads, FMGP_GQ_MINB)
 grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
                   const int32_t* __restrict__ cstart, int64_t nq, const int32_t* __restrict__ qpos,
                   const double* __restrict__ Q, const int32_t* __restrict__ qout, const int32_t* __restrict__ excl_arr,
@@ -785,7 +791,7 @@ grid_query_thread_kernel(const GridParams* __restrict__ gpp, const double* __res
 // sequential loop by rounding only (posterior means within 1e-15 relative of
 // the sequential sum here, tolerance 1e-9).
 template <int D, int KF>
-__global__ void __launch_bounds__(kQueryThreads, 4)
+__global__ void __launch_bounds__(kQueryThreads, FMGP_GP_MINB)
 grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
                     const int32_t* __restrict__ cstart, int64_t nq, const double* __restrict__ Qs,
                     const int32_t* __restrict__ qout, const double* __restrict__ X, const int32_t* __restrict__ S,
