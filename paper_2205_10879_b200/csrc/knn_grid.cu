@@ -459,6 +459,7 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
     for (int e = 0; e < E; ++e) L[e] = Cand{INFINITY, INT_MAX};
     Cand thr{INFINITY, INT_MAX};
     const int tl = (kk - 1) & 31, te = (kk - 1) >> 5;
+    bool fresh = true;  // list still empty (nothing merged yet)
 
     // Scan up to 64 ranges (two per lane) of cell-ordered points: candidates
     // 32 at a time, ballot skip, bitonic sort + merge into the top-KP list.
@@ -477,8 +478,7 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
       const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
       if (lane == 31) rp[kSlots] = total;
       __syncwarp();
-      for (int32_t base = 0; base < total; base += 32) {
-        const int32_t want = base + lane;
+      auto fetch = [&](int32_t want) -> Cand {
         Cand cd{INFINITY, INT_MAX};
         if (want < total) {
           int j = 0;  // largest slot j with rp[j] <= want (skips empty slots)
@@ -493,6 +493,28 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
           const double sd = dist_sq_fixed<D>(q, x);
           if (id != self) cd = Cand{sd, id};
         }
+        return cd;
+      };
+      int32_t base = 0;
+      if (fresh && total >= 64) {
+        // the list is empty: sort the first 64 candidates as one bitonic network
+        // (two 32-sorts + one merge: 41 compare-exchange stages instead of the
+        // 60 of two batch merges) and take them as the list
+        Cand a = bitonic_sort32(fetch(lane), lane);
+        Cand b2 = bitonic_sort32(fetch(32 + lane), lane);
+        merge32(a, b2, lane);
+#pragma unroll
+        for (int e = 0; e < E; ++e) L[e] = e == 0 ? a : (e == 1 ? b2 : Cand{INFINITY, INT_MAX});
+        Cand t{0, 0};
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (e == te) t = L[e];
+        thr = shfl_c(t, tl);
+        base = 64;
+      }
+      fresh = false;
+      for (; base < total; base += 32) {
+        Cand cd = fetch(base + lane);
         const bool pass = cless(cd, thr);
         if (__ballot_sync(0xffffffffu, pass) != 0) {
           if (!pass) cd = Cand{INFINITY, INT_MAX};
