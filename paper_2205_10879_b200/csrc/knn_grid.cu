@@ -338,6 +338,7 @@ __device__ __forceinline__ double outside_lb_sq(const GridParams& g, const doubl
 
 constexpr int kQueryThreads = 256;
 constexpr int kSlots = 64;  // ranges per chunk: 2 per lane (one cell-row per lane)
+constexpr int kInsertMax = 4;  // batches with at most this many admissions are inserted one by one
 
 // Static cell visiting order for the warp kernel: every offset o of Chebyshev
 // radius <= R sorted by its static lower bound sb(o) = sum_t max(|o_t| - 1, 0)^2
@@ -516,15 +517,46 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
       for (; base < total; base += 32) {
         Cand cd = fetch(base + lane);
         const bool pass = cless(cd, thr);
-        if (__ballot_sync(0xffffffffu, pass) != 0) {
-          if (!pass) cd = Cand{INFINITY, INT_MAX};
-          merge_batch_chain<E>(L, cd, lane);
-          Cand t{0, 0};
+        const unsigned bal = __ballot_sync(0xffffffffu, pass);
+        if (bal == 0) continue;
+        if (__popc(bal) <= kInsertMax) {
+          // few candidates: insert each into the sorted list (rank by ballots,
+          // shift the tail up one slot) instead of a 30-stage sort + merge
+          unsigned mleft = bal;
+          while (mleft != 0) {
+            const int src = __ffs(mleft) - 1;
+            mleft &= mleft - 1;
+            const Cand c = shfl_c(cd, src);
+            if (!cless(c, thr)) continue;  // the threshold fell since the ballot
+            int rank = 0;
 #pragma unroll
-          for (int e = 0; e < E; ++e)
-            if (e == te) t = L[e];
-          thr = shfl_c(t, tl);
+            for (int e = 0; e < E; ++e) rank += __popc(__ballot_sync(0xffffffffu, cless(L[e], c)));
+#pragma unroll
+            for (int e = E - 1; e >= 0; --e) {  // descending: L[e-1] is still the old segment
+              Cand up = Cand{__shfl_up_sync(0xffffffffu, L[e].d, 1), __shfl_up_sync(0xffffffffu, L[e].i, 1)};
+              if (e > 0) {
+                const Cand last = shfl_c(L[e > 0 ? e - 1 : 0], 31);
+                if (lane == 0) up = last;
+              }
+              const int g = 32 * e + lane;
+              if (g == rank) L[e] = c;
+              else if (g > rank) L[e] = up;
+            }
+            Cand t{0, 0};
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+              if (e == te) t = L[e];
+            thr = shfl_c(t, tl);
+          }
+          continue;
         }
+        if (!pass) cd = Cand{INFINITY, INT_MAX};
+        merge_batch_chain<E>(L, cd, lane);
+        Cand t{0, 0};
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (e == te) t = L[e];
+        thr = shfl_c(t, tl);
       }
       __syncwarp();
     };
