@@ -338,7 +338,10 @@ __device__ __forceinline__ double outside_lb_sq(const GridParams& g, const doubl
 
 constexpr int kQueryThreads = 256;
 constexpr int kSlots = 64;  // ranges per chunk: 2 per lane (one cell-row per lane)
-constexpr int kInsertMax = 4;  // batches with at most this many admissions are inserted one by one
+#ifndef FMGP_INSERT_MAX
+#define FMGP_INSERT_MAX 4
+#endif
+constexpr int kInsertMax = FMGP_INSERT_MAX;  // batches with at most this many admissions are inserted one by one
 
 // Static cell visiting order for the warp kernel: every offset o of Chebyshev
 // radius <= R sorted by its static lower bound sb(o) = sum_t max(|o_t| - 1, 0)^2
