@@ -55,8 +55,10 @@ namespace {
 constexpr int kBM = 128;  // queries per tile (TMEM lanes)
 constexpr int kBN = 128;  // reference points per tile (TMEM columns per buffer)
 constexpr int kBK = 64;   // fp16 dims per k-block (one 128 B swizzle row)
-constexpr int kStages = 2;       // A+B stages when the query tile streams (KB > 1)
+constexpr int kStages = 2;       // A+B stages when the query tile streams (KB > 1), minimum
+constexpr int kStagesMax = 4;    // ... and maximum (as many as shared memory leaves room for)
 constexpr int kBStagesRes = 3;   // B-only stages when the query tile is resident (KB == 1)
+constexpr int kBars = kStagesMax > kBStagesRes ? kStagesMax : kBStagesRes;  // stage barriers
 constexpr int kTBufs = 4;        // TMEM accumulator buffers (4 x 128 columns)
 constexpr int kCapMax = 128;  // candidate-list capacity per query (kk <= kCapMax - 29)
 constexpr int kMaxThreads = 320;  // TMA + MMA + 4 or 8 epilogue warps (8: two column halves, lists fit twice)
@@ -269,6 +271,8 @@ struct TcArgs {
   int with_self;
   int wait_mode;         // producer-side wait (see mbar_wait_sleep)
   int halves;            // 1: 4 epilogue warps; 2: 8 (each tile's columns split, separate lists)
+  int stages;            // A+B pipeline stages in streaming mode (KB > 1): kStages .. kStagesMax
+  int nslots;            // 16 KB operand slots: 1 + kBStagesRes (resident) or 2 * stages
   int32_t* out;          // nq x (kk + with_self)
   double* out_d;         // nq x kk (nullable)
   int32_t* cand;         // [cap][nq] candidate ids, column-major (coalesced stores)
@@ -292,18 +296,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   // 1024-byte alignment (SWIZZLE_128B operands) by offsetting the __shared__ pointer itself,
   // so the compiler keeps the shared address space (LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-  // 4 x 16 KB operand slots: streaming mode (KB > 1) stage s = (A slot s, B slot 2 + s);
+  // 16 KB operand slots: streaming mode (KB > 1) stage s = (A slot s, B slot stages + s);
   // resident mode (KB == 1) A = slot 0 (loaded once per query tile), B stages = slots 1..3
   uint8_t* slots = smem;
   const bool ares = a.KB == 1;
-  const int nst = ares ? kBStagesRes : kStages;
+  const int nst = ares ? kBStagesRes : a.stages;
   const int halves = a.halves;
-  float* lk = reinterpret_cast<float*>(slots + 4 * kABytes);  // [halves][cap][128] candidate v (column = query)
+  float* lk = reinterpret_cast<float*>(slots + a.nslots * kABytes);  // [halves][cap][128] candidate v (column = query)
   int32_t* li = reinterpret_cast<int32_t*>(lk + halves * a.cap * kBM);  // [halves][cap][128] candidate index
   float* scratch = reinterpret_cast<float*>(li + halves * a.cap * kBM);   // [4*halves warps][32][kScrStride]
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 4 * halves * 32 * kScrStride);
-  uint64_t* empty = full + kBStagesRes;
-  uint64_t* tfull = empty + kBStagesRes;  // kTBufs TMEM buffers
+  uint64_t* empty = full + kBars;
+  uint64_t* tfull = empty + kBars;  // kTBufs TMEM buffers
   uint64_t* tempty = tfull + kTBufs;
   uint64_t* afull = tempty + kTBufs;      // resident query tile
   uint64_t* aempty = afull + 1;
@@ -315,7 +319,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   const int64_t npt = (a.np + kBN - 1) / kBN;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kBStagesRes; ++s) {
+    for (int s = 0; s < kBars; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -359,7 +363,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             } else {
               mbar_expect_tx(&full[stage], kStageBytes);
               tma_load_2d(slots + stage * kABytes, &tmQ, &full[stage], kb * kBK, static_cast<int>(qt * kBM));
-              tma_load_2d(slots + (2 + stage) * kABytes, &tmP, &full[stage], kb * kBK, static_cast<int>(pt * kBN));
+              tma_load_2d(slots + (nst + stage) * kABytes, &tmP, &full[stage], kb * kBK, static_cast<int>(pt * kBN));
             }
             if (++stage == nst) {
               stage = 0;
@@ -390,7 +394,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           tc_fence_after();
           if (lane == 0) {
             const uint64_t ad = sdesc_sw128(su32(ares ? slots : slots + stage * kABytes));
-            const uint64_t bd = sdesc_sw128(su32(slots + (ares ? 1 + stage : 2 + stage) * kABytes));
+            const uint64_t bd = sdesc_sw128(su32(slots + (ares ? 1 + stage : nst + stage) * kABytes));
 #pragma unroll
             for (int k16 = 0; k16 < kBK / 16; ++k16)
               tc_mma_f16(d_tmem, ad + 2 * k16, bd + 2 * k16, kIdesc, (kb > 0 || k16 > 0) ? 1u : 0u);
@@ -778,13 +782,27 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   const int cap = std::min(kCapMax, ((kk + 29 + 3) / 4) * 4);
   // 8 epilogue warps (two column halves with separate candidate lists) when both
   // lists fit next to the operand slots and the recheck's 128-candidate warp
-  auto smem_for = [&](int hv) {
-    return static_cast<size_t>(1024) + kStages * kStageBytes + static_cast<size_t>(hv) * cap * kBM * 8 +
-           sizeof(float) * 4 * hv * 32 * kScrStride + 256;
+  auto smem_for = [&](int hv, int nslots) {
+    return static_cast<size_t>(1024) + static_cast<size_t>(nslots) * kABytes +
+           static_cast<size_t>(hv) * cap * kBM * 8 + sizeof(float) * 4 * hv * 32 * kScrStride + 256;
   };
   // Only when the epilogue is the bound (DP == 64: resident query tile, cheap
   // recheck); for wide rows (KB > 1) the GEMM/TMA side and the doubled recheck dominate.
-  const int halves = (KB == 1 && 2 * cap <= 128 && smem_for(2) <= 232448) ? 2 : 1;
+  const int halves = (KB == 1 && 2 * cap <= 128 && smem_for(2, 1 + kBStagesRes) <= 232448) ? 2 : 1;
+  // Wide rows stream (A, B) k-block pairs: as many stages in flight as the
+  // candidate lists leave room for (the TMA round trip from L2 is several MMA
+  // k-blocks long; FMGP_TC_STAGES overrides, for A/B checks)
+  int stages = kStages;
+  if (KB > 1) {
+    const char* e = std::getenv("FMGP_TC_STAGES");
+    const int want = e != nullptr ? std::atoi(e) : kStagesMax;
+    for (int st = std::min(std::max(want, kStages), kStagesMax); st >= kStages; --st)
+      if (smem_for(halves, 2 * st) <= 232448) {
+        stages = st;
+        break;
+      }
+  }
+  const int nslots = KB > 1 ? 2 * stages : 1 + kBStagesRes;
   __half *Qh = nullptr, *Ph = nullptr;
   float* qn = nullptr;
   double* sums = nullptr;
@@ -824,6 +842,8 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.kk = kk;
   a.cap = cap;
   a.halves = halves;
+  a.stages = stages;
+  a.nslots = nslots;
   a.self_offset = self_offset;
   a.excl = excl_arr;
   a.with_self = with_self;
@@ -843,7 +863,7 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.maxabs_bits = bits;
   a.pmax_bits = bits + 1;
   a.debug_G = debug_G;
-  const size_t smem = smem_for(halves);
+  const size_t smem = smem_for(halves, nslots);
   err = cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   const int64_t nqt = (nq + kBM - 1) / kBM;
