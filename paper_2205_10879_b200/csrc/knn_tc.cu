@@ -57,8 +57,9 @@ constexpr int kBN = 128;  // reference points per tile (TMEM columns per buffer)
 constexpr int kBK = 64;   // fp16 dims per k-block (one 128 B swizzle row)
 constexpr int kStages = 2;       // A+B stages when the query tile streams (KB > 1), minimum
 constexpr int kStagesMax = 4;    // ... and maximum (as many as shared memory leaves room for)
-constexpr int kBStagesRes = 3;   // B-only stages when the query tile is resident (KB == 1)
-constexpr int kBars = kStagesMax > kBStagesRes ? kStagesMax : kBStagesRes;  // stage barriers
+constexpr int kBStagesRes = 3;   // B-only stages when the query tile is resident (KB == 1), minimum
+constexpr int kBStagesResMax = 6;  // ... and maximum
+constexpr int kBars = kStagesMax > kBStagesResMax ? kStagesMax : kBStagesResMax;  // stage barriers
 constexpr int kTBufs = 4;        // TMEM accumulator buffers (4 x 128 columns)
 constexpr int kCapMax = 128;  // candidate-list capacity per query (kk <= kCapMax - 29)
 constexpr int kMaxThreads = 320;  // TMA + MMA + 4 or 8 epilogue warps (8: two column halves, lists fit twice)
@@ -271,8 +272,9 @@ struct TcArgs {
   int with_self;
   int wait_mode;         // producer-side wait (see mbar_wait_sleep)
   int halves;            // 1: 4 epilogue warps; 2: 8 (each tile's columns split, separate lists)
-  int stages;            // A+B pipeline stages in streaming mode (KB > 1): kStages .. kStagesMax
-  int nslots;            // 16 KB operand slots: 1 + kBStagesRes (resident) or 2 * stages
+  int stages;            // pipeline stages: A+B pairs (KB > 1, kStages .. kStagesMax) or B tiles
+                         // (KB == 1, kBStagesRes .. kBStagesResMax)
+  int nslots;            // 16 KB operand slots: 1 + stages (resident) or 2 * stages
   int32_t* out;          // nq x (kk + with_self)
   double* out_d;         // nq x kk (nullable)
   int32_t* cand;         // [cap][nq] candidate ids, column-major (coalesced stores)
@@ -300,7 +302,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   // resident mode (KB == 1) A = slot 0 (loaded once per query tile), B stages = slots 1..3
   uint8_t* slots = smem;
   const bool ares = a.KB == 1;
-  const int nst = ares ? kBStagesRes : a.stages;
+  const int nst = a.stages;
   const int halves = a.halves;
   float* lk = reinterpret_cast<float*>(slots + a.nslots * kABytes);  // [halves][cap][128] candidate v (column = query)
   int32_t* li = reinterpret_cast<int32_t*>(lk + halves * a.cap * kBM);  // [halves][cap][128] candidate index
@@ -789,20 +791,20 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   // Only when the epilogue is the bound (DP == 64: resident query tile, cheap
   // recheck); for wide rows (KB > 1) the GEMM/TMA side and the doubled recheck dominate.
   const int halves = (KB == 1 && 2 * cap <= 128 && smem_for(2, 1 + kBStagesRes) <= 232448) ? 2 : 1;
-  // Wide rows stream (A, B) k-block pairs: as many stages in flight as the
-  // candidate lists leave room for (the TMA round trip from L2 is several MMA
-  // k-blocks long; FMGP_TC_STAGES overrides, for A/B checks)
-  int stages = kStages;
-  if (KB > 1) {
-    const char* e = std::getenv("FMGP_TC_STAGES");
-    const int want = e != nullptr ? std::atoi(e) : kStagesMax;
-    for (int st = std::min(std::max(want, kStages), kStagesMax); st >= kStages; --st)
-      if (smem_for(halves, 2 * st) <= 232448) {
-        stages = st;
-        break;
-      }
-  }
-  const int nslots = KB > 1 ? 2 * stages : 1 + kBStagesRes;
+  // As many operand stages in flight as the candidate lists leave room for
+  // (the TMA round trip from L2 is several MMA k-blocks long): (A, B) k-block
+  // pairs for wide rows, B tiles when the query tile is resident.
+  // FMGP_TC_STAGES overrides (A/B checks).
+  const char* st_env = std::getenv("FMGP_TC_STAGES");
+  const int smin = KB > 1 ? kStages : kBStagesRes, smax = KB > 1 ? kStagesMax : kBStagesResMax;
+  const int want = st_env != nullptr ? std::atoi(st_env) : smax;
+  int stages = smin;
+  for (int st = std::min(std::max(want, smin), smax); st >= smin; --st)
+    if (smem_for(halves, KB > 1 ? 2 * st : 1 + st) <= 232448) {
+      stages = st;
+      break;
+    }
+  const int nslots = KB > 1 ? 2 * stages : 1 + stages;
   __half *Qh = nullptr, *Ph = nullptr;
   float* qn = nullptr;
   double* sums = nullptr;
