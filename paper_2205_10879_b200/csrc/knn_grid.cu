@@ -1002,6 +1002,36 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
     }
     const int64_t j = best.i;
     if (nn_out != nullptr && lane == 0) nn_out[orow] = static_cast<int32_t>(j);
+    if (m == 1 && k <= 2 * kWarp) {
+      // the common shape: both 32-neighbour rounds' loads (S, C, then the X
+      // gathers) are issued before any arithmetic, so the dependent gather
+      // chain is paid once per test point, not once per round
+      const int t0 = lane, t1 = lane + kWarp;
+      const bool h0 = t0 < k, h1 = t1 < k;
+      const int64_t nb0 = h0 ? S[j * k + t0] : 0, nb1 = h1 ? S[j * k + t1] : 0;
+      const double c0 = h0 ? Cf[j * k + t0] : 0.0, c1 = h1 ? Cf[j * k + t1] : 0.0;
+      double x0[D], x1[D];
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        x0[u] = X[nb0 * D + u];
+        x1[u] = X[nb1 * D + u];
+      }
+      double dq0 = q[0] - x0[0], dq1 = q[0] - x1[0];
+      double s0 = dq0 * dq0, s1 = dq1 * dq1;
+#pragma unroll
+      for (int u = 1; u < D; ++u) {
+        dq0 = q[u] - x0[u];
+        dq1 = q[u] - x1[u];
+        s0 = fma(dq0, dq0, s0);
+        s1 = fma(dq1, dq1, s1);
+      }
+      double acc = h0 ? kernel_from_sq_build<KF>(s0, kc, kp) * c0 : 0.0;
+      if (h1) acc = fma(kernel_from_sq_build<KF>(s1, kc, kp), c1, acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) out[orow] = acc + mean_offset[0];
+      continue;
+    }
     for (int cc = 0; cc < m; ++cc) {
       double acc = 0.0;
       for (int t = lane; t < k; t += kWarp) {
