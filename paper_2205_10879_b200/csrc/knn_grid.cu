@@ -57,6 +57,9 @@ __device__ __forceinline__ double ord_val(unsigned long long k) {
 }
 
 __global__ void bbox_kernel(const double* __restrict__ X, int64_t n, int d, unsigned long long* __restrict__ mm) {
+  // per-thread min/max -> warp shuffles -> CTA (shared memory) -> one atomic pair
+  // per dimension per CTA (per-warp atomics on six words serialise in L2)
+  __shared__ unsigned long long slo[3][32], shi[3][32];
   unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -66,6 +69,7 @@ __global__ void bbox_kernel(const double* __restrict__ X, int64_t n, int d, unsi
       hi[t] = k > hi[t] ? k : hi[t];
     }
   }
+  const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int t = 0; t < d; ++t) {
     for (int o = 16; o > 0; o >>= 1) {
       unsigned long long a = __shfl_xor_sync(0xffffffffu, lo[t], o);
@@ -74,8 +78,25 @@ __global__ void bbox_kernel(const double* __restrict__ X, int64_t n, int d, unsi
       hi[t] = b > hi[t] ? b : hi[t];
     }
     if ((threadIdx.x & 31) == 0) {
-      atomicMin(&mm[2 * t], lo[t]);
-      atomicMax(&mm[2 * t + 1], hi[t]);
+      slo[t][wid] = lo[t];
+      shi[t][wid] = hi[t];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    for (int t = 0; t < d; ++t) {
+      unsigned long long a = threadIdx.x < nw ? slo[t][threadIdx.x] : ~0ull;
+      unsigned long long b = threadIdx.x < nw ? shi[t][threadIdx.x] : 0ull;
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, a, o);
+        const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, b, o);
+        a = a2 < a ? a2 : a;
+        b = b2 > b ? b2 : b;
+      }
+      if (threadIdx.x == 0) {
+        atomicMin(&mm[2 * t], a);
+        atomicMax(&mm[2 * t + 1], b);
+      }
     }
   }
 }
