@@ -801,9 +801,12 @@ cudaError_t launch_pair(const double* X, const double* Y, const int32_t* S, int6
 
 // CTA shape: 4 warps (one pair table per 4 neighbourhoods in flight), 4 CTAs
 // per SM: <= 128 registers per thread, 16 warps per SM.
+#ifndef FMGP_REG_WARPS
+#define FMGP_REG_WARPS 4
+#endif
 template <int K, int M>
 struct RegLaunch {
-  static constexpr int kWarps = 4;
+  static constexpr int kWarps = FMGP_REG_WARPS;
   static constexpr int kMinBlocks = 4;
 };
 
