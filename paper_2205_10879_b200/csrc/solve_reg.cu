@@ -503,10 +503,6 @@ template <int K, int M>
 __device__ void back_solve_reg(const double* A, const double* dinv, double* __restrict__ Crow, int lane) {
   using Sh = RegShape<K, M>;
   static_assert(K <= 64, "two register slots per lane");
-  // 1/L_jj of the lane's own rows in registers: the owner scales before the
-  // shuffle, so x_j arrives ready (no broadcast load of dinv[j] per column)
-  const double dl0 = lane < K ? dinv[lane] : 0.0;
-  const double dl1 = lane + 32 < K ? dinv[lane + 32] : 0.0;
 #pragma unroll 1
   for (int c = 0; c < M; ++c) {
     const double* z = A + Sh::row_off(K + c);
@@ -514,17 +510,16 @@ __device__ void back_solve_reg(const double* A, const double* dinv, double* __re
     double y1 = lane + 32 < K ? z[lane + 32] : 0.0;
 #pragma unroll
     for (int j = K - 1; j >= 0; --j) {
+      const double yj = __shfl_sync(0xffffffffu, j < 32 ? y0 : y1, j & 31);
+      const double xj = yj * dinv[j];
       const double* Lj = A + ro_r(j);
-      const double l0 = Lj[lane];  // entries past j belong to the next row: never used below
-      const double l1 = j >= 32 ? Lj[(lane + 32 < j) ? lane + 32 : 0] : 0.0;
-      const double xj = __shfl_sync(0xffffffffu, j < 32 ? y0 * dl0 : y1 * dl1, j & 31);
       if (j < 32) {
         if (lane == j) y0 = xj;
-        if (lane < j) y0 = fma(-l0, xj, y0);
+        if (lane < j) y0 = fma(-Lj[lane], xj, y0);
       } else {
         if (lane == j - 32) y1 = xj;
-        y0 = fma(-l0, xj, y0);
-        if (lane + 32 < j) y1 = fma(-l1, xj, y1);
+        if (lane < 32) y0 = fma(-Lj[lane], xj, y0);
+        if (lane + 32 < j) y1 = fma(-Lj[lane + 32], xj, y1);
       }
     }
     if (lane < K) Crow[lane * M + c] = y0;
