@@ -83,17 +83,25 @@ int check_solve_shape(int32_t k, int32_t d, int32_t m) {
   return FMGP_OK;
 }
 
-int predict_device_impl(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d, int32_t k,
-                        int32_t m, const fmgp::KParams& kp, const double* mean_offset_dev, const double* Z,
-                        int64_t nz, double* out, int32_t* nn_out, cudaStream_t stream) {
-  if (nz <= 0) return FMGP_OK;
-  const int sms = num_sms_current();
+bool knn_force_brute() {
   static const bool force_brute = [] {
     const char* e = std::getenv("FMGP_KNN");
     return e != nullptr && std::string(e) == "brute";
   }();
-  if (!force_brute && d <= 3) {
-    FMGP_CUDA(fmgp::predict_grid(X, n, d, S, C, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, sms, stream));
+  return force_brute;
+}
+
+// `grid`: a model handle's prebuilt predict grid (d <= 3), or null to build one for this call.
+int predict_device_impl(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d, int32_t k,
+                        int32_t m, const fmgp::KParams& kp, const double* mean_offset_dev, const double* Z,
+                        int64_t nz, double* out, int32_t* nn_out, cudaStream_t stream, const void* grid = nullptr) {
+  if (nz <= 0) return FMGP_OK;
+  const int sms = num_sms_current();
+  if (!knn_force_brute() && d <= 3) {
+    if (grid != nullptr)
+      FMGP_CUDA(fmgp::predict_grid_cached(grid, X, S, C, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, sms, stream));
+    else
+      FMGP_CUDA(fmgp::predict_grid(X, n, d, S, C, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, sms, stream));
     return FMGP_OK;
   }
   DevBuf<int32_t> nn_tmp;
@@ -130,6 +138,7 @@ struct fmgp_model {
   int32_t* S = nullptr;
   double* C = nullptr;
   double* mo = nullptr;
+  void* grid = nullptr;  // predict-walk grid of X (d <= 3), built once at create
 };
 
 // Host-buffer precompute of rows [row_begin, row_end) (X, Y full; S_out and
@@ -672,6 +681,9 @@ int fmgp_model_create(const double* X, const int32_t* S, const double* C, int64_
   if (e == cudaSuccess) e = cudaMemcpy(mdl->S, S, sizeof(int32_t) * n * k, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(mdl->C, C, sizeof(double) * n * k * m, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(mdl->mo, mean_offset, sizeof(double) * m, cudaMemcpyHostToDevice);
+  // the reference's model owns its NeighborIndex (fast_predict.cpp:127-129);
+  // here that is the predict walk's cell grid of X, built once per handle
+  if (e == cudaSuccess && d <= 3 && !knn_force_brute()) mdl->grid = fmgp::predict_grid_cache_build(mdl->X, n, d, 0, &e);
   if (e != cudaSuccess) {
     fmgp_model_destroy(mdl);
     return cuda_fail(e, "fmgp_model_create");
@@ -693,7 +705,7 @@ int fmgp_model_predict(const fmgp_model* mdl, const double* Z, int64_t nz, doubl
   FMGP_CUDA(dN.alloc(static_cast<size_t>(nz), st.s));
   FMGP_CUDA(cudaMemcpyAsync(dZ.p, Z, sizeof(double) * nz * mdl->d, cudaMemcpyHostToDevice, st.s));
   int rc = predict_device_impl(mdl->X, mdl->S, mdl->C, mdl->n, mdl->d, mdl->k, mdl->m, mdl->kp, mdl->mo, dZ.p, nz,
-                               dO.p, dN.p, st.s);
+                               dO.p, dN.p, st.s, mdl->grid);
   if (rc != FMGP_OK) return rc;
   FMGP_CUDA(cudaMemcpyAsync(out, dO.p, sizeof(double) * nz * mdl->m, cudaMemcpyDeviceToHost, st.s));
   if (nn_out) FMGP_CUDA(cudaMemcpyAsync(nn_out, dN.p, sizeof(int32_t) * nz, cudaMemcpyDeviceToHost, st.s));
@@ -704,6 +716,7 @@ int fmgp_model_predict(const fmgp_model* mdl, const double* Z, int64_t nz, doubl
 void fmgp_model_destroy(fmgp_model* mdl) {
   if (mdl == nullptr) return;
   cudaSetDevice(mdl->device);
+  if (mdl->grid) fmgp::predict_grid_cache_free(mdl->grid);
   if (mdl->X) cudaFree(mdl->X);
   if (mdl->S) cudaFree(mdl->S);
   if (mdl->C) cudaFree(mdl->C);

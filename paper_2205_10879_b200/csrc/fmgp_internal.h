@@ -57,6 +57,12 @@ namespace fmgp {
 
 // Exact kNN through a uniform cell grid (d <= 3, kk <= 128); same contract as
 // knn_bruteforce (excl_arr only with external queries).
+// Predict-walk grid of the training points, built once per model handle (d <= 3).
+void* predict_grid_cache_build(const double* X, int64_t n, int d, cudaStream_t stream, cudaError_t* err);
+void predict_grid_cache_free(void* cache);
+cudaError_t predict_grid_cached(const void* cache, const double* X, const int32_t* S, const double* Cf, int k, int m,
+                                const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz,
+                                double* out, int32_t* nn_out, int num_sms, cudaStream_t stream);
 bool knn_grid_supported(int d, int kk);
 cudaError_t knn_grid(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
                      const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,

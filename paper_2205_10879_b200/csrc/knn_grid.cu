@@ -889,7 +889,7 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
     double q[D];
 #pragma unroll
     for (int t = 0; t < D; ++t) q[t] = Qs[w * D + t];
-    const int64_t orow = qout[w];
+    const int64_t orow = qout != nullptr ? qout[w] : w;  // unsorted small batches: identity
     int c[3];
     cell_key<D>(q, g, c);
     Cand best{INFINITY, INT_MAX};
@@ -1242,37 +1242,74 @@ cudaError_t knn_grid_d(const double* Q, int64_t nq, const double* P, int64_t np,
   return err;
 }
 
+// The training-point grid of the predict walk (bbox -> cubic cells of ~1.5
+// points in 2-D, ~1 in 3-D -> counting sort): built per call, or once per
+// model handle (PredictGridCache) and reused by every predict on it.
+constexpr int64_t kPredictSortMin = 4096;  // test batches at least this large are cell-sorted first
+
+struct PredictGridCache {
+  int d = 0;
+  int64_t n = 0;
+  GridParams* gp = nullptr;
+  SortBufs pb;
+};
+
 template <int D>
-cudaError_t predict_grid_d(const double* X, int64_t n, const int32_t* S, const double* Cf, int k, int m,
-                           const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz, double* out,
-                           int32_t* nn_out, int num_sms, cudaStream_t s) {
-  // ~1 neighbour wanted: small cells (d = 2, 3: the 3^D block of the ordered walk)
+cudaError_t build_predict_grid(const double* X, int64_t n, PredictGridCache& g, cudaStream_t s) {
   const double per_cell = (D == 1) ? 4.0 : (D == 2 ? 1.5 : 1.0);
   const int64_t ncap = n;
-  GridParams* gp = nullptr;
   unsigned long long* mm = nullptr;
-  SortBufs pb, qb;
-  cudaError_t err = cudaMallocAsync(&gp, sizeof(GridParams), s);
+  g.d = D;
+  g.n = n;
+  cudaError_t err = cudaMallocAsync(&g.gp, sizeof(GridParams), s);
   if (err == cudaSuccess) err = cudaMallocAsync(&mm, sizeof(unsigned long long) * 6, s);
-  if (err == cudaSuccess) err = pb.alloc(n, ncap, D, s);
-  if (err == cudaSuccess) err = qb.alloc(nz, ncap, D, s);
+  if (err == cudaSuccess) err = g.pb.alloc(n, ncap, D, s);
   if (err != cudaSuccess) return err;
   cudaMemsetAsync(mm, 0, sizeof(unsigned long long) * 6, s);
   for (int t = 0; t < D; ++t) cudaMemsetAsync(mm + 2 * t, 0xFF, sizeof(unsigned long long), s);
   bbox_kernel<<<grid1d(n), 256, 0, s>>>(X, n, D, mm);
-  grid_params_kernel<<<1, 1, 0, s>>>(mm, n, D, per_cell, ncap, gp);
+  grid_params_kernel<<<1, 1, 0, s>>>(mm, n, D, per_cell, ncap, g.gp);
   note_launches(2);
-  cell_sort<D>(X, n, gp, ncap, pb, s);
-  cell_sort<D>(Z, nz, gp, ncap, qb, s);
+  cell_sort<D>(X, n, g.gp, ncap, g.pb, s);
+  cudaFreeAsync(mm, s);
+  return cudaGetLastError();
+}
+
+void release_predict_grid(PredictGridCache& g, cudaStream_t s) {
+  if (g.gp) cudaFreeAsync(g.gp, s);
+  g.gp = nullptr;
+  g.pb.release(s);
+  g.pb = SortBufs{};
+}
+
+// Test points sorted by the same cells (locality), then the fused kernel.
+template <int D>
+cudaError_t run_predict_grid(const PredictGridCache& g, const double* X, const int32_t* S, const double* Cf, int k,
+                             int m, const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz,
+                             double* out, int32_t* nn_out, int num_sms, cudaStream_t s) {
+  // Large batches are sorted by cell for locality; a small one (a few warps'
+  // worth, e.g. fast_predict_one) goes in input order: the sort's cell-count
+  // scan is O(cells), which would dominate its latency.
+  SortBufs qb;
+  const double* Qs = Z;
+  const int32_t* qo = nullptr;
+  cudaError_t err = cudaSuccess;
+  if (nz >= kPredictSortMin) {
+    err = qb.alloc(nz, g.n, D, s);
+    if (err != cudaSuccess) return err;
+    cell_sort<D>(Z, nz, g.gp, g.n, qb, s);
+    Qs = qb.pts;
+    qo = qb.pid;
+  }
   int64_t blocks = (nz * 32 + kQueryThreads - 1) / kQueryThreads;
   const int64_t cap = static_cast<int64_t>(num_sms) * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   switch (kp.kind == 1 ? 0 : 1 + kp.nu_code) {  // kernel_code(), evaluated on the host
-#define FMGP_PRED_CASE(KF)                                                                                  \
-  case KF:                                                                                                  \
-    grid_predict_kernel<D, KF><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                     \
-        gp, pb.pts, pb.pid, pb.cstart, nz, qb.pts, qb.pid, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out); \
+#define FMGP_PRED_CASE(KF)                                                                                      \
+  case KF:                                                                                                      \
+    grid_predict_kernel<D, KF><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                         \
+        g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out);     \
     break;
     FMGP_PRED_CASE(0)
     FMGP_PRED_CASE(1)
@@ -1284,10 +1321,18 @@ cudaError_t predict_grid_d(const double* X, int64_t n, const int32_t* S, const d
   }
   note_launches(1);
   err = cudaGetLastError();
-  cudaFreeAsync(gp, s);
-  cudaFreeAsync(mm, s);
-  pb.release(s);
   qb.release(s);
+  return err;
+}
+
+template <int D>
+cudaError_t predict_grid_d(const double* X, int64_t n, const int32_t* S, const double* Cf, int k, int m,
+                           const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz, double* out,
+                           int32_t* nn_out, int num_sms, cudaStream_t s) {
+  PredictGridCache g;
+  cudaError_t err = build_predict_grid<D>(X, n, g, s);
+  if (err == cudaSuccess) err = run_predict_grid<D>(g, X, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, s);
+  release_predict_grid(g, s);
   return err;
 }
 
@@ -1302,6 +1347,43 @@ cudaError_t predict_grid(const double* X, int64_t n, int d, const int32_t* S, co
     case 2: return predict_grid_d<2>(X, n, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
     case 3: return predict_grid_d<3>(X, n, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
     default: return cudaErrorInvalidValue;
+  }
+}
+
+void* predict_grid_cache_build(const double* X, int64_t n, int d, cudaStream_t stream, cudaError_t* err) {
+  *err = cudaErrorInvalidValue;
+  if (d < 1 || d > 3 || n < 1) return nullptr;
+  auto* g = new PredictGridCache();
+  switch (d) {
+    case 1: *err = build_predict_grid<1>(X, n, *g, stream); break;
+    case 2: *err = build_predict_grid<2>(X, n, *g, stream); break;
+    default: *err = build_predict_grid<3>(X, n, *g, stream); break;
+  }
+  if (*err == cudaSuccess) *err = cudaStreamSynchronize(stream);  // the handle is used from other streams
+  if (*err != cudaSuccess) {
+    predict_grid_cache_free(g);
+    return nullptr;
+  }
+  return g;
+}
+
+void predict_grid_cache_free(void* cache) {
+  auto* g = static_cast<PredictGridCache*>(cache);
+  if (g == nullptr) return;
+  release_predict_grid(*g, 0);
+  cudaStreamSynchronize(0);
+  delete g;
+}
+
+cudaError_t predict_grid_cached(const void* cache, const double* X, const int32_t* S, const double* Cf, int k, int m,
+                                const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz,
+                                double* out, int32_t* nn_out, int num_sms, cudaStream_t stream) {
+  const auto* g = static_cast<const PredictGridCache*>(cache);
+  if (nz <= 0) return cudaSuccess;
+  switch (g->d) {
+    case 1: return run_predict_grid<1>(*g, X, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
+    case 2: return run_predict_grid<2>(*g, X, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
+    default: return run_predict_grid<3>(*g, X, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
   }
 }
 
