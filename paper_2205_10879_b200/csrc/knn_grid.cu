@@ -1190,8 +1190,19 @@ cudaError_t knn_grid_d(const double* Q, int64_t nq, const double* P, int64_t np,
   // Points per cell: enough that the radius-1 block usually holds the kk-th neighbour.
   // Points per cell. d = 1: enough that the radius-1 block usually holds the
   // kk-th neighbour; d = 2, 3: smaller cells for the distance-ordered walk
-  // (the 3^D block holds ~1.5 kk, later cells are skipped by their distance).
-  const double per_cell = (D == 1) ? fmax(4.0, 0.6 * kk) : (D == 2 ? fmax(4.0, kk / 6.0) : fmax(2.0, kk / 16.0));
+  // (the 3^D block holds ~1.8 kk in 2-D, ~2.2 kk in 3-D; later cells are
+  // skipped by their distance). A/B at cfg2: kk/4 2.54, kk/5 2.40, kk/6 2.44,
+  // kk/7 2.58, kk/8 2.85 ms; cfg5: kk/10 29.6, kk/13 29.6, kk/16 29.9,
+  // kk/20 31.7 ms.
+  static const double div2 = [] {  // FMGP_GRID_DIV2 / FMGP_GRID_DIV3: A/B of the cell size
+    const char* e = std::getenv("FMGP_GRID_DIV2");
+    return e != nullptr ? std::atof(e) : 5.0;
+  }();
+  static const double div3 = [] {
+    const char* e = std::getenv("FMGP_GRID_DIV3");
+    return e != nullptr ? std::atof(e) : 12.0;
+  }();
+  const double per_cell = (D == 1) ? fmax(4.0, 0.6 * kk) : (D == 2 ? fmax(4.0, kk / div2) : fmax(2.0, kk / div3));
   const int64_t ncap = np;  // cells never exceed the point count
   GridParams* gp = nullptr;
   unsigned long long* mm = nullptr;
