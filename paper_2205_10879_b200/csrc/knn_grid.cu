@@ -1267,7 +1267,15 @@ struct PredictGridCache {
 
 template <int D>
 cudaError_t build_predict_grid(const double* X, int64_t n, PredictGridCache& g, cudaStream_t s) {
-  const double per_cell = (D == 1) ? 4.0 : (D == 2 ? 1.5 : 1.0);
+  static const double pc2 = [] {  // FMGP_PGRID_PC2 / FMGP_PGRID_PC3: A/B of the cell size
+    const char* e = std::getenv("FMGP_PGRID_PC2");
+    return e != nullptr ? std::atof(e) : 1.5;
+  }();
+  static const double pc3 = [] {
+    const char* e = std::getenv("FMGP_PGRID_PC3");
+    return e != nullptr ? std::atof(e) : 1.0;
+  }();
+  const double per_cell = (D == 1) ? 4.0 : (D == 2 ? pc2 : pc3);
   const int64_t ncap = n;
   unsigned long long* mm = nullptr;
   g.d = D;
