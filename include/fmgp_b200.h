@@ -150,6 +150,8 @@ int fmgp_nearest_device(const double* P, int64_t np, int32_t d, const double* Q,
  * to cnt stored points idx[], i.e. sqrt(dist_sq); idx out of range ->
  * FMGP_EINVAL ("distance_to: bad query or index"). */
 typedef struct fmgp_index fmgp_index;
+/* device < 0: the calling thread's current device (also for fmgp_model_create).
+ * Entry points that switch devices restore the caller's current device. */
 int fmgp_index_create(const double* P, int64_t np, int32_t d, int32_t device, fmgp_index** out);
 int fmgp_index_query_knn(const fmgp_index* index, const double* Q, int64_t nq, int32_t k,
                          const int32_t* exclude, int32_t* idx_out, double* dist_out);
@@ -180,6 +182,56 @@ int fmgp_model_create(const double* X, const int32_t* S, const double* C, int64_
 int fmgp_model_predict(const fmgp_model* model, const double* Z, int64_t nz, double* out,
                        int32_t* nn_out);
 void fmgp_model_destroy(fmgp_model* model);
+/* A model over caller-owned DEVICE buffers X (n*d), S (n*k), C (n*k*m) on the
+ * current device (not copied; they must outlive the handle); mean_offset is a
+ * host array of m. Builds the predict-walk grid once. */
+int fmgp_model_wrap_device(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d, int32_t k,
+                           int32_t m, const fmgp_kernel_params* params, const double* mean_offset, fmgp_model** out);
+/* Stream-ordered predict with Z, out, nn_out (nullable) in HBM on the current
+ * device, through the handle's replica on that device and its cached grid. */
+int fmgp_model_predict_device(const fmgp_model* model, const double* Z, int64_t nz, double* out, int32_t* nn_out,
+                              void* stream);
+/* Number of device replicas (1, or the members of the group that built it). */
+int fmgp_model_replicas(const fmgp_model* model);
+
+/* ---- device groups: multi-GPU precompute (the reference's
+ * thread split, fast_predict.cpp:110-125) ------------------------------------
+ * The training set is replicated on every member GPU; training rows are dealt
+ * block-cyclically (fmgp_group_rows lists a member's [begin, end) blocks); S
+ * and C are all-gathered in place over NVLink (NCCL, loaded at run time), each
+ * round's exchange overlapped with the next round's solve. Results are
+ * bit-identical to fmgp_precompute for any group.
+ *  - rank group: one process per GPU. Rank 0 calls fmgp_group_unique_id and
+ *    the caller distributes the 128 bytes (e.g. torch.distributed); every
+ *    rank then calls fmgp_group_create_rank (collective).
+ *  - device group: one process, several devices, one host thread each; NCCL
+ *    when the devices are distinct, peer copies otherwise (a device may be
+ *    listed twice to exercise the layout on one GPU). */
+typedef struct fmgp_group fmgp_group;
+int fmgp_group_unique_id(uint8_t* id_out /* 128 bytes */);
+int fmgp_group_create_rank(const uint8_t* id, int32_t nranks, int32_t rank, int32_t device, fmgp_group** out);
+int fmgp_group_create_devices(const int32_t* devices, int32_t ndev, fmgp_group** out);
+/* backend: 0 none (one member), 1 NCCL, 2 peer copies */
+int fmgp_group_info(const fmgp_group* group, int32_t* nranks, int32_t* local_members, int32_t* backend);
+/* The row layout (no device needed): member `member` of `nranks` owns
+ * *nblocks blocks, ranges[2*b], ranges[2*b+1] = [begin, end) (nullable).
+ * Blocks of pc = ceil(n / (nranks * R)) rows, R = FMGP_GROUP_CHUNKS (4). */
+int fmgp_group_rows(int64_t n, int32_t nranks, int32_t member, int64_t* nblocks, int64_t* ranges);
+void fmgp_group_destroy(fmgp_group* group);
+/* Host buffers: X (n*d), Y (n*m) in; S_out (n*k) and C_out (n*k*m) receive
+ * the rows this process's members computed (every row for a device group,
+ * the rank's blocks for a rank group). model_out (nullable; needs
+ * mean_offset, m values): a model whose replicas are the members' full,
+ * all-gathered device results (no copy). Collective over the group. */
+int fmgp_group_precompute(fmgp_group* group, const double* X, const double* Y, int64_t n, int32_t d, int32_t m,
+                          const fmgp_kernel_params* params, int32_t k, const double* mean_offset, int32_t* S_out,
+                          double* C_out, int64_t* failed_row, fmgp_model** model_out);
+/* Rank groups: X, Y full replicas in HBM; S_out (n*k) and C_out (n*k*m) are
+ * full-size device buffers that end holding every row on every rank. Work is
+ * issued on `stream`; returns after the failure word is read back. */
+int fmgp_group_precompute_device(fmgp_group* group, const double* X, const double* Y, int64_t n, int32_t d,
+                                 int32_t m, const fmgp_kernel_params* params, int32_t k, int32_t* S_out,
+                                 double* C_out, int64_t* failed_row, void* stream);
 
 /* ---- kernel arithmetic on device (kernel.cpp:88-119) ----------------------
  * K_out (na*nb row-major) = kernel(||A_i - B_j||); with B == NULL computes
@@ -264,6 +316,10 @@ int fmgp_muygps_predict(const double* X, const double* Y, int64_t n, int32_t d, 
  * summed kernel-stage times (ms) and the number of calls since the last read. */
 void fmgp_set_stage_timing(int on);
 int fmgp_stage_times(double* knn_ms, double* solve_ms, int64_t* calls);
+
+/* FP64 roofline denominators measured on the current device now: DFMA and
+ * DMMA (m8n8k4) TFLOP/s over the whole chip (best of three ~1 ms runs). */
+int fmgp_diag_fp64_peak(double* dfma_tflops, double* dmma_tflops);
 
 /* ---- diagnostics (tensor-core kNN) ----------------------------------------
  * D~ (the tensor-core filter value n^_q + n^_p - 2 q^.p^ in the scaled fp16

@@ -15,6 +15,11 @@
 //   fmgp_ref_loocv_loss      -> loocv_loss                       (muygps.cpp:64-78)
 //   fmgp_ref_train           -> BatchSpec::sample + train        (muygps.cpp:15-30, :214-270)
 //   fmgp_ref_muygps_predict  -> muygps_predict                   (muygps.cpp:272-295)
+//   fmgp_ref_predict_session / _run / _free -> a PrecomputedModel built once,
+//                               then fast_predict_batch (threads <= 1) or
+//                               fast_predict_one per row (threads > 1), for timing
+//   fmgp_ref_save_model / fmgp_ref_load_model -> save_model / load_model
+//                               (fast_predict.cpp:158-280), for cross-build file tests
 // Multi-output (BASELINE cfg3, m > 1): the reference is single-output
 // (dataset.hpp:14); the harness shares S and passes the k x m right-hand
 // sides to the reference's own solve_spd (linalg.hpp:19-20), which solves
@@ -306,6 +311,110 @@ int fmgp_ref_muygps_predict(const double* X_rm, const double* Y, int64_t n, int 
     Eigen::VectorXd r = muygps_predict(ts, from_rm(Z_rm, nz, d), f, index, k);
     for (int64_t t = 0; t < nz; ++t) out[t] = r(t);
   });
+}
+
+// A reference PrecomputedModel per output column, built once (the copies
+// and the index build are outside whatever the caller times).
+struct RefPredictSession {
+  std::vector<PrecomputedModel> models;
+  int d = 0, m = 0;
+};
+
+void* fmgp_ref_predict_session(const double* X_rm, const int32_t* S, const double* C, int64_t n, int d, int k, int m,
+                               int kind, double sigma, double rho, double nu, double tau, double mean_offset) {
+  RefPredictSession* out = nullptr;
+  const int rc = guard([&] {
+    auto* ss = new RefPredictSession();
+    ss->d = d;
+    ss->m = m;
+    Eigen::MatrixXd X = from_rm(X_rm, n, d);
+    NeighborIndex index = NeighborIndex::build(X, IndexMode::Exact);
+    NeighborTable table;
+    table.S.resize(n, k);
+    std::memcpy(table.S.data(), S, sizeof(int32_t) * n * k);
+    for (int c = 0; c < m; ++c) {
+      Eigen::Matrix<double, Eigen::Dynamic, Eigen::Dynamic, Eigen::RowMajor> Cc(n, k);
+      for (int64_t i = 0; i < n * k; ++i) Cc.data()[i] = C[i * m + c];
+      ss->models.push_back(PrecomputedModel{X, table, std::move(Cc), KernelParams(sigma, rho, nu, tau),
+                                            kind_of(kind), mean_offset, index});
+    }
+    out = ss;
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+int fmgp_ref_predict_run(void* session, const double* Z_rm, int64_t nz, int threads, double* out) {
+  return guard([&] {
+    auto* ss = static_cast<RefPredictSession*>(session);
+    const int m = ss->m;
+    Eigen::MatrixXd Z = from_rm(Z_rm, nz, ss->d);
+    if (threads <= 1) {
+      for (int c = 0; c < m; ++c) {
+        Eigen::VectorXd v = fast_predict_batch(ss->models[c], Z);
+        for (int64_t t = 0; t < nz; ++t) out[t * m + c] = v(t);
+      }
+      return;
+    }
+    std::vector<std::thread> ws;
+    const int64_t chunk = (nz + threads - 1) / threads;
+    for (int w = 0; w < threads; ++w) {
+      const int64_t b = w * chunk, e = std::min<int64_t>(nz, b + chunk);
+      if (b >= e) continue;
+      ws.emplace_back([&, b, e] {
+        for (int64_t t = b; t < e; ++t) {
+          Eigen::VectorXd z = Z.row(t).transpose();
+          for (int c = 0; c < m; ++c) out[t * m + c] = fast_predict_one(ss->models[c], z);
+        }
+      });
+    }
+    for (auto& t : ws) t.join();
+  });
+}
+
+void fmgp_ref_predict_free(void* session) { delete static_cast<RefPredictSession*>(session); }
+
+// save_model of a reference model assembled from the given arrays; mode 1
+// builds the index as IndexMode::ApproxGraph with the given graph parameters
+// (its HNSW blob is written by the reference, nn_index.cpp:397-416).
+int fmgp_ref_save_model(const double* X_rm, const int32_t* S, const double* C, int64_t n, int d, int k, int kind,
+                        double sigma, double rho, double nu, double tau, double mean_offset, int mode, int max_degree,
+                        int build_beam, uint64_t seed, const char* path) {
+  return guard([&] {
+    Eigen::MatrixXd X = from_rm(X_rm, n, d);
+    GraphParams gp;
+    gp.max_degree = max_degree;
+    gp.build_beam = build_beam;
+    gp.seed = seed;
+    NeighborIndex index = NeighborIndex::build(X, mode == 1 ? IndexMode::ApproxGraph : IndexMode::Exact, gp);
+    NeighborTable table;
+    table.S.resize(n, k);
+    std::memcpy(table.S.data(), S, sizeof(int32_t) * n * k);
+    Eigen::Matrix<double, Eigen::Dynamic, Eigen::Dynamic, Eigen::RowMajor> Cc(n, k);
+    std::memcpy(Cc.data(), C, sizeof(double) * n * k);
+    PrecomputedModel model{X, table, std::move(Cc), KernelParams(sigma, rho, nu, tau), kind_of(kind), mean_offset,
+                           index};
+    save_model(model, path);
+  });
+}
+
+// load_model, then fast_predict_batch of Z; dims_out = {n, d, k, mode}.
+int fmgp_ref_load_model(const char* path, const double* Z_rm, int64_t nz, int64_t* dims_out, double* pred_out) {
+  return guard([&] {
+    PrecomputedModel model = load_model(path);
+    dims_out[0] = model.X.rows();
+    dims_out[1] = model.X.cols();
+    dims_out[2] = model.table.S.cols();
+    dims_out[3] = model.index.mode() == IndexMode::ApproxGraph ? 1 : 0;
+    if (nz > 0) {
+      Eigen::VectorXd v = fast_predict_batch(model, from_rm(Z_rm, nz, static_cast<int>(model.X.cols())));
+      for (int64_t t = 0; t < nz; ++t) pred_out[t] = v(t);
+    }
+  });
+}
+
+// load_model then save_model (the reference re-writing a file it read).
+int fmgp_ref_resave(const char* path_in, const char* path_out) {
+  return guard([&] { save_model(load_model(path_in), path_out); });
 }
 
 }  // extern "C"

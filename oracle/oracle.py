@@ -207,7 +207,46 @@ class Reference:
         L.fmgp_ref_muygps_predict.restype = C.c_int
         L.fmgp_ref_muygps_predict.argtypes = ([_V, _V, C.c_int64, C.c_int, C.c_double, _V, C.c_int64, C.c_int,
                                                C.c_int] + [C.c_double] * 4 + [_V])
+        L.fmgp_ref_predict_session.restype = C.c_void_p
+        L.fmgp_ref_predict_session.argtypes = ([_V, _V, _V, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int] +
+                                               [C.c_double] * 5)
+        L.fmgp_ref_predict_run.restype = C.c_int
+        L.fmgp_ref_predict_run.argtypes = [_V, _V, C.c_int64, C.c_int, _V]
+        L.fmgp_ref_predict_free.restype = None
+        L.fmgp_ref_predict_free.argtypes = [_V]
+        L.fmgp_ref_save_model.restype = C.c_int
+        L.fmgp_ref_save_model.argtypes = ([_V, _V, _V, C.c_int64, C.c_int, C.c_int, C.c_int] + [C.c_double] * 5 +
+                                          [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_char_p])
+        L.fmgp_ref_load_model.restype = C.c_int
+        L.fmgp_ref_load_model.argtypes = [C.c_char_p, _V, C.c_int64, _V, _V]
+        L.fmgp_ref_resave.restype = C.c_int
+        L.fmgp_ref_resave.argtypes = [C.c_char_p, C.c_char_p]
         self.L = L
+
+    def predict_session(self, X, S, Cm, kind, sigma, rho, nu, tau, mean_offset):
+        """A reference model built once; .run(Z, threads) times fast_predict_batch / fast_predict_one."""
+        return _RefPredictSession(self, X, S, Cm, kind, sigma, rho, nu, tau, mean_offset)
+
+    def save_model(self, path, X, S, Cm, kind, sigma, rho, nu, tau, mean_offset, mode=0, max_degree=16,
+                   build_beam=100, seed=0):
+        X = _f64(X)
+        S = np.ascontiguousarray(S, dtype=np.int32)
+        Cm = _f64(Cm).reshape(S.shape)
+        self._check(self.L.fmgp_ref_save_model(_p(X), _p(S), _p(Cm), X.shape[0], X.shape[1], S.shape[1], kind, sigma,
+                                               rho, nu, tau, float(mean_offset), mode, max_degree, build_beam, seed,
+                                               str(path).encode()))
+
+    def resave(self, path_in, path_out):
+        """load_model then save_model through the reference."""
+        self._check(self.L.fmgp_ref_resave(str(path_in).encode(), str(path_out).encode()))
+
+    def load_model_predict(self, path, Z):
+        """load_model, then fast_predict_batch(Z): (dims (n, d, k, mode), predictions)."""
+        Z = _f64(Z)
+        dims = np.zeros(4, dtype=np.int64)
+        out = np.empty(Z.shape[0])
+        self._check(self.L.fmgp_ref_load_model(str(path).encode(), _p(Z), Z.shape[0], _p(dims), _p(out)))
+        return dims, out
 
     def local_predictions(self, X, Y, batch, nbr, dist, kind, sigma, rho, nu, tau):
         X = _f64(X)
@@ -324,6 +363,33 @@ class Reference:
         out = np.empty(Q.shape[0], dtype=np.int32)
         self._check(self.L.fmgp_ref_nearest(_p(X), X.shape[0], X.shape[1], _p(Q), Q.shape[0], _p(out)))
         return out
+
+
+class _RefPredictSession:
+    def __init__(self, ref, X, S, Cm, kind, sigma, rho, nu, tau, mean_offset):
+        X = _f64(X)
+        S = np.ascontiguousarray(S, dtype=np.int32)
+        n, k = S.shape
+        C3 = _f64(Cm).reshape(n, k, -1)
+        self.ref, self.d, self.m = ref, X.shape[1], C3.shape[2]
+        self.h = ref.L.fmgp_ref_predict_session(_p(X), _p(S), _p(C3), n, X.shape[1], k, self.m, kind, sigma, rho, nu,
+                                                tau, float(np.asarray(mean_offset).reshape(-1)[0]))
+        if not self.h:
+            raise OracleError(3, ref.L.fmgp_ref_last_error().decode())
+
+    def run(self, Z, threads=1):
+        Z = _f64(Z).reshape(-1, self.d)
+        out = np.empty((Z.shape[0], self.m))
+        self.ref._check(self.ref.L.fmgp_ref_predict_run(self.h, _p(Z), Z.shape[0], threads, _p(out)))
+        return out
+
+    def close(self):
+        if self.h:
+            self.ref.L.fmgp_ref_predict_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 def best_available():

@@ -66,6 +66,20 @@ SIGNATURES: dict[str, tuple] = {
                                     C.c_int32, C.POINTER(_vp)]),
     "fmgp_model_predict": (C.c_int, [_vp, _vp, C.c_int64, _vp, _vp]),
     "fmgp_model_destroy": (None, [_vp]),
+    "fmgp_model_wrap_device": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _kp, _vp,
+                                         C.POINTER(_vp)]),
+    "fmgp_model_predict_device": (C.c_int, [_vp, _vp, C.c_int64, _vp, _vp, _vp]),
+    "fmgp_model_replicas": (C.c_int, [_vp]),
+    "fmgp_group_unique_id": (C.c_int, [_vp]),
+    "fmgp_group_create_rank": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "fmgp_group_create_devices": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp)]),
+    "fmgp_group_info": (C.c_int, [_vp, _i32, _i32, _i32]),
+    "fmgp_group_rows": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, _i64, _vp]),
+    "fmgp_group_destroy": (None, [_vp]),
+    "fmgp_group_precompute": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, _kp, C.c_int32, _vp, _vp,
+                                        _vp, _i64, C.POINTER(_vp)]),
+    "fmgp_group_precompute_device": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, _kp, C.c_int32,
+                                               _vp, _vp, _i64, _vp]),
     "fmgp_cov_matrix": (C.c_int, [_vp, C.c_int64, _vp, C.c_int64, C.c_int32, _kp, _vp]),
     "fmgp_kernel_values": (C.c_int, [_vp, C.c_int64, _kp, _vp]),
     "fmgp_solve_spd_batched": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, C.c_int32, _vp, _vp, _i64]),
@@ -81,6 +95,7 @@ SIGNATURES: dict[str, tuple] = {
                                       _vp, _i64]),
     "fmgp_set_stage_timing": (None, [C.c_int]),
     "fmgp_stage_times": (C.c_int, [_d, _d, _i64]),
+    "fmgp_diag_fp64_peak": (C.c_int, [_d, _d]),
     "fmgp_debug_tc_tile": (C.c_int, [_vp, C.c_int64, _vp, C.c_int64, C.c_int32, _vp]),
 }
 

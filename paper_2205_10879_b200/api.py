@@ -121,6 +121,14 @@ class NeighborIndex:
     def __init__(self, points: np.ndarray, mode: IndexMode):
         self._pts = points
         self._mode = mode
+        self._dev = None  # device-resident copy + nearest-point grid (fmgp_index), made on first query
+
+    def _handle(self):
+        if self._dev is None:
+            h = C.c_void_p()
+            N.check(N.LIB.fmgp_index_create(_ptr(self._pts), self.size(), self.dim(), -1, C.byref(h)))
+            self._dev = _IndexHandle(h)
+        return self._dev.h
 
     @staticmethod
     def build(points, mode: IndexMode = IndexMode.Exact, params=None) -> "NeighborIndex":
@@ -153,8 +161,7 @@ class NeighborIndex:
         idx = np.empty((nq, k), dtype=np.int32)
         dist = np.empty((nq, k), dtype=np.float64)
         ex = None if exclude is None else np.ascontiguousarray(exclude, dtype=np.int32)
-        N.check(N.LIB.fmgp_query_knn(_ptr(self._pts), self.size(), self.dim(), _ptr(Q), nq, k, _ptr(ex),
-                                     _ptr(idx), _ptr(dist)))
+        N.check(N.LIB.fmgp_index_query_knn(self._handle(), _ptr(Q), nq, k, _ptr(ex), _ptr(idx), _ptr(dist)))
         return idx, dist
 
     def query_knn(self, q, k: int, exclude_index: int = -1) -> NeighborList:
@@ -169,7 +176,7 @@ class NeighborIndex:
         if Q.ndim != 2 or Q.shape[1] != self.dim():
             raise DomainError(N.FMGP_EINVAL, "nearest_training_point: dimension mismatch")
         out = np.empty(Q.shape[0], dtype=np.int32)
-        N.check(N.LIB.fmgp_nearest(_ptr(self._pts), self.size(), self.dim(), _ptr(Q), Q.shape[0], _ptr(out)))
+        N.check(N.LIB.fmgp_index_nearest(self._handle(), _ptr(Q), Q.shape[0], _ptr(out)))
         return out
 
     def nearest_training_point(self, q) -> int:
@@ -200,18 +207,29 @@ class PrecomputedModel:
                                                     (self.m,)))
 
     def handle(self):
-        """Lazily created device-resident replica (fmgp_model_create)."""
+        """Lazily created device-resident replica (fmgp_model_create) on the
+        calling thread's current CUDA device."""
         if self._handle is None:
             h = C.c_void_p()
             n, k = self.S.shape
             mo = self._offsets()
             kp = self.params.c(self.kind)
             N.check(N.LIB.fmgp_model_create(_ptr(self.X), _ptr(self.S), _ptr(self.C), n, self.X.shape[1], k,
-                                            self.m, C.byref(kp), _ptr(mo), 0, C.byref(h)))
+                                            self.m, C.byref(kp), _ptr(mo), -1, C.byref(h)))
             self._handle = _ModelHandle(h)
         return self._handle.h
 
     table = property(lambda self: self.S)
+
+
+class _IndexHandle:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h:
+            N.LIB.fmgp_index_destroy(self.h)
+            self.h = None
 
 
 class _ModelHandle:

@@ -27,7 +27,7 @@ CPP = PKG / "cpp"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SOURCES = ["knn.cu", "knn_grid.cu", "knn_tc.cu", "solve.cu", "solve_big.cu", "solve_tc.cu", "solve_reg.cu", "solve_cta.cu", "predict.cu", "misc.cu", "capi.cu", "muygps.cu"]
+CUDA_SOURCES = ["knn.cu", "knn_grid.cu", "knn_tc.cu", "solve.cu", "solve_big.cu", "solve_tc.cu", "solve_reg.cu", "solve_cta.cu", "predict.cu", "misc.cu", "capi.cu", "muygps.cu", "group.cu"]
 FACADE_SOURCES = ["facade_kernel.cpp", "facade_linalg.cpp", "facade_nn_index.cpp", "facade_fast_predict.cpp",
                   "facade_dataset.cpp", "facade_muygps.cpp"]
 
@@ -67,7 +67,7 @@ def build_cuda(force: bool = False, defines: list[str] | None = None, out: Path 
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4) or 1) as ex:
         list(ex.map(_run, jobs))
-    _run([NVCC, *ARCH, "-shared", "-o", str(out), *[str(objdir / (Path(s).stem + ".o")) for s in CUDA_SOURCES]])
+    _run([NVCC, *ARCH, "-shared", "-o", str(out), *[str(objdir / (Path(s).stem + ".o")) for s in CUDA_SOURCES], "-ldl"])
     return out
 
 
@@ -94,6 +94,11 @@ def build_facade(force: bool = False) -> Path | None:
     return out
 
 
+def build_test_tools() -> None:
+    """tests/cpp/facade_tool: the repo's own driver of the C++ facade (test infrastructure)."""
+    _run(["make", "-s", "-C", str(REPO / "tests" / "cpp"), "tool"])
+
+
 def build_oracle() -> None:
     """The checker: C restatement always; reference TUs when the reference is mounted."""
     _run(["make", "-s", "-C", str(REPO / "oracle")])
@@ -110,6 +115,7 @@ def build(product_only: bool = False, force: bool = False) -> None:
     build_datagen(force)
     build_facade(force)
     if not product_only:
+        build_test_tools()
         build_oracle()
 
 

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <iosfwd>
 #include <memory>
+#include <string>
 #include <vector>
 
 struct fmgp_index;
@@ -67,6 +68,7 @@ class NeighborIndex {
   GraphParams params_;
   std::vector<double> pts_;
   std::shared_ptr<fmgp_index> dev_;
+  std::string graph_blob_;  // a reference-written HNSW graph (after the mode tag), kept verbatim
 };
 
 }  // namespace fastmuygps

@@ -4,6 +4,7 @@
 #include <bit>
 #include <cstring>
 #include <fstream>
+#include <mutex>
 #include <sstream>
 #include <string>
 
@@ -11,6 +12,67 @@
 #include "fastmuygps/fast_predict.hpp"
 
 namespace fastmuygps {
+
+namespace detail {
+
+struct DeviceModelSlot {
+  std::mutex mu;
+  const void* x = nullptr;
+  const void* s = nullptr;
+  const void* c = nullptr;
+  Eigen::Index n = 0, d = 0, k = 0;
+  fmgp_kernel_params kp{};
+  double mo = 0.0;
+  std::shared_ptr<fmgp_model> h;
+};
+
+DeviceModelCache::DeviceModelCache() : slot(std::make_shared<DeviceModelSlot>()) {}
+DeviceModelCache::DeviceModelCache(const DeviceModelCache&) : slot(std::make_shared<DeviceModelSlot>()) {}
+DeviceModelCache& DeviceModelCache::operator=(const DeviceModelCache&) {
+  slot = std::make_shared<DeviceModelSlot>();
+  return *this;
+}
+DeviceModelCache::~DeviceModelCache() = default;
+
+}  // namespace detail
+
+namespace {
+
+// The model's device replica: created once (fmgp_model_create uploads X, S, C
+// and builds the predict-walk grid), then shared by every predict call.
+std::shared_ptr<fmgp_model> device_model(const PrecomputedModel& model) {
+  auto slot = model.device.slot;
+  if (!slot) slot = std::make_shared<detail::DeviceModelSlot>();  // a moved-from model
+  const fmgp_kernel_params kp = detail::abi_params(model.kind, model.params);
+  std::lock_guard<std::mutex> lk(slot->mu);
+  const bool same = slot->h && slot->x == model.X.data() && slot->s == model.table.S.data() &&
+                    slot->c == model.C.data() && slot->n == model.X.rows() && slot->d == model.X.cols() &&
+                    slot->k == model.table.S.cols() && slot->kp.kind == kp.kind && slot->kp.sigma == kp.sigma &&
+                    slot->kp.rho == kp.rho && slot->kp.nu == kp.nu && slot->kp.tau == kp.tau &&
+                    slot->mo == model.mean_offset;
+  if (same) return slot->h;
+  const auto n = static_cast<int64_t>(model.X.rows());
+  const auto d = static_cast<int32_t>(model.X.cols());
+  const auto k = static_cast<int32_t>(model.table.S.cols());
+  if (model.C.rows() != model.X.rows() || model.C.cols() != k || model.table.S.rows() != model.X.rows())
+    throw std::domain_error("fast_predict: model tables do not match the training set");
+  const double mo = model.mean_offset;
+  fmgp_model* h = nullptr;
+  detail::check(fmgp_model_create(detail::row_major(model.X).data(), model.table.S.data(), model.C.data(), n, d, k, 1,
+                                  &kp, &mo, -1, &h));
+  slot->h = std::shared_ptr<fmgp_model>(h, fmgp_model_destroy);
+  slot->x = model.X.data();
+  slot->s = model.table.S.data();
+  slot->c = model.C.data();
+  slot->n = model.X.rows();
+  slot->d = model.X.cols();
+  slot->k = model.table.S.cols();
+  slot->kp = kp;
+  slot->mo = mo;
+  return slot->h;
+}
+
+}  // namespace
 
 PrecomputedModel precompute(const TrainingSet& train, const FittedParams& fitted, const NeighborIndex& index, int k,
                             int threads) {
@@ -34,24 +96,24 @@ PrecomputedModel precompute(const TrainingSet& train, const FittedParams& fitted
 
 Eigen::VectorXd fast_predict_batch(const PrecomputedModel& model, const Eigen::MatrixXd& Z) {
   if (Z.cols() != model.X.cols()) throw std::domain_error("fast_predict_batch: test dimension mismatch");
-  const auto n = static_cast<int64_t>(model.X.rows());
-  const auto d = static_cast<int32_t>(model.X.cols());
-  const auto k = static_cast<int32_t>(model.table.S.cols());
-  const fmgp_kernel_params kp = detail::abi_params(model.kind, model.params);
-  const auto zr = detail::row_major(Z);
   Eigen::VectorXd out(Z.rows());
   if (Z.rows() == 0) return out;
-  const double mo = model.mean_offset;
-  detail::check(fmgp_predict(detail::row_major(model.X).data(), model.table.S.data(), model.C.data(), n, d, k, 1, &kp,
-                             &mo, zr.data(), Z.rows(), out.data(), nullptr));
+  const std::shared_ptr<fmgp_model> h = device_model(model);
+  if (Z.rows() == 1) {  // fast_predict_one: Eigen's column-major 1 x d is already the row
+    detail::check(fmgp_model_predict(h.get(), Z.data(), 1, out.data(), nullptr));
+    return out;
+  }
+  const auto zr = detail::row_major(Z);
+  detail::check(fmgp_model_predict(h.get(), zr.data(), Z.rows(), out.data(), nullptr));
   return out;
 }
 
 double fast_predict_one(const PrecomputedModel& model, const Eigen::VectorXd& z) {
   if (z.size() != model.X.cols()) throw std::domain_error("nearest_training_point: dimension mismatch");
-  Eigen::MatrixXd Z(1, z.size());
-  for (Eigen::Index j = 0; j < z.size(); ++j) Z(0, j) = z(j);
-  return fast_predict_batch(model, Z)(0);
+  double out = 0.0;
+  const std::shared_ptr<fmgp_model> h = device_model(model);
+  detail::check(fmgp_model_predict(h.get(), z.data(), 1, &out, nullptr));
+  return out;
 }
 
 // ---------------------------------------------------------------- model file

@@ -19,11 +19,12 @@ void put_le(std::ostream& out, T v) {
 }
 
 template <typename T>
-T get_le(std::istream& in, std::size_t* bytes_read) {
+T get_le(std::istream& in, std::size_t* bytes_read, std::string* keep = nullptr) {
   T v{};
   in.read(reinterpret_cast<char*>(&v), sizeof(v));
   if (!in) throw FormatError("truncated neighbor-index data", bytes_read != nullptr ? *bytes_read : 0);
   if (bytes_read != nullptr) *bytes_read += sizeof(v);
+  if (keep != nullptr) keep->append(reinterpret_cast<const char*>(&v), sizeof(v));
   return v;
 }
 
@@ -34,7 +35,7 @@ std::vector<double> host_points(const Eigen::MatrixXd& P) {
 }
 
 std::shared_ptr<fmgp_index> device_copy(const std::vector<double>& pts, int n, int d) {
-  int dev = 0;
+  const int dev = -1;  // the calling thread's current device
   fmgp_index* h = nullptr;
   detail::check(fmgp_index_create(pts.data(), n, d, dev, &h));
   return std::shared_ptr<fmgp_index>(h, fmgp_index_destroy);
@@ -91,38 +92,51 @@ double NeighborIndex::distance_to(const Eigen::VectorXd& q, int j) const {
   return out;
 }
 
-// The blob is the reference's Exact layout (one u32 mode tag). An index is
-// always written as Exact: this implementation never builds the HNSW graph.
-void NeighborIndex::serialize(std::ostream& out) const { put_le<std::uint32_t>(out, 0u); }
+// The blob is the reference's layout (nn_index.cpp:397-416): a u32 mode tag,
+// then for ApproxGraph the graph. A graph read from a reference-written file
+// is kept byte for byte and written back unchanged, so such models round-trip
+// bit-exactly; an index this facade built (it never builds the HNSW graph,
+// queries are exact) is written with the Exact tag.
+void NeighborIndex::serialize(std::ostream& out) const {
+  if (mode_ == IndexMode::ApproxGraph && !graph_blob_.empty()) {
+    put_le<std::uint32_t>(out, 1u);
+    out.write(graph_blob_.data(), static_cast<std::streamsize>(graph_blob_.size()));
+    return;
+  }
+  put_le<std::uint32_t>(out, 0u);
+}
 
 NeighborIndex NeighborIndex::deserialize(std::istream& in, const Eigen::MatrixXd& points, std::size_t* bytes_read) {
   const auto mode = get_le<std::uint32_t>(in, bytes_read);
   if (mode > 1) throw FormatError("unknown neighbor-index mode tag", bytes_read != nullptr ? *bytes_read : 0);
   GraphParams gp;
+  std::string blob;
   if (mode == 1) {
-    // A graph written by the reference: validate and skip it; queries stay exact.
+    // A graph written by the reference: validated and kept verbatim (written
+    // back by serialize); queries stay exact.
     const auto n = static_cast<int>(points.rows());
-    gp.max_degree = get_le<std::int32_t>(in, bytes_read);
-    gp.build_beam = get_le<std::int32_t>(in, bytes_read);
-    gp.query_beam = get_le<std::int32_t>(in, bytes_read);
-    gp.seed = get_le<std::uint64_t>(in, bytes_read);
-    const auto entry = get_le<std::int32_t>(in, bytes_read);
-    (void)get_le<std::int32_t>(in, bytes_read);  // max level
+    gp.max_degree = get_le<std::int32_t>(in, bytes_read, &blob);
+    gp.build_beam = get_le<std::int32_t>(in, bytes_read, &blob);
+    gp.query_beam = get_le<std::int32_t>(in, bytes_read, &blob);
+    gp.seed = get_le<std::uint64_t>(in, bytes_read, &blob);
+    const auto entry = get_le<std::int32_t>(in, bytes_read, &blob);
+    (void)get_le<std::int32_t>(in, bytes_read, &blob);  // max level
     if (entry < 0 || entry >= n)
       throw FormatError("neighbor-index entry point out of range", bytes_read != nullptr ? *bytes_read : 0);
     for (int i = 0; i < n; ++i) {
-      const auto lvl = get_le<std::int32_t>(in, bytes_read);
+      const auto lvl = get_le<std::int32_t>(in, bytes_read, &blob);
       if (lvl < 0) throw FormatError("negative node level in neighbor index", bytes_read != nullptr ? *bytes_read : 0);
       for (int l = 0; l <= lvl; ++l) {
-        const auto cnt = get_le<std::uint32_t>(in, bytes_read);
+        const auto cnt = get_le<std::uint32_t>(in, bytes_read, &blob);
         for (std::uint32_t c = 0; c < cnt; ++c) {
-          const auto u = get_le<std::int32_t>(in, bytes_read);
+          const auto u = get_le<std::int32_t>(in, bytes_read, &blob);
           if (u < 0 || u >= n) throw FormatError("neighbor id out of range", bytes_read != nullptr ? *bytes_read : 0);
         }
       }
     }
   }
   NeighborIndex ix = build(points, static_cast<IndexMode>(mode), gp.max_degree >= 2 && gp.build_beam >= 1 ? gp : GraphParams{});
+  ix.graph_blob_ = std::move(blob);
   return ix;
 }
 

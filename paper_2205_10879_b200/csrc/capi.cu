@@ -21,6 +21,7 @@
 #include "fmgp_internal.h"
 
 #include "capi_common.h"
+#include "capi_model.h"
 
 using namespace fmgp_capi;
 
@@ -115,7 +116,67 @@ int predict_device_impl(const double* X, const int32_t* S, const double* C, int6
   return FMGP_OK;
 }
 
+// One replica's share of a host-buffer predict: H2D of the test points, the
+// walk / 1-NN + gather-kernel-dot, D2H of the means (and 1-NN indices).
+int replica_predict_host(const fmgp_model* mdl, const fmgp_model_replica& r, const double* Z, int64_t nz, double* out,
+                         int32_t* nn_out) {
+  if (nz <= 0) return FMGP_OK;
+  FMGP_CUDA(cudaSetDevice(r.device));
+  Stream st;
+  FMGP_CUDA(st.create());
+  DevBuf<double> dZ, dO;
+  DevBuf<int32_t> dN;
+  FMGP_CUDA(dZ.alloc(static_cast<size_t>(nz) * mdl->d, st.s));
+  FMGP_CUDA(dO.alloc(static_cast<size_t>(nz) * mdl->m, st.s));
+  if (nn_out) FMGP_CUDA(dN.alloc(static_cast<size_t>(nz), st.s));
+  FMGP_CUDA(cudaMemcpyAsync(dZ.p, Z, sizeof(double) * nz * mdl->d, cudaMemcpyHostToDevice, st.s));
+  int rc = predict_device_impl(r.X, r.S, r.C, mdl->n, mdl->d, mdl->k, mdl->m, mdl->kp, r.mo, dZ.p, nz, dO.p,
+                               nn_out ? dN.p : nullptr, st.s, r.grid);
+  if (rc != FMGP_OK) return rc;
+  FMGP_CUDA(cudaMemcpyAsync(out, dO.p, sizeof(double) * nz * mdl->m, cudaMemcpyDeviceToHost, st.s));
+  if (nn_out) FMGP_CUDA(cudaMemcpyAsync(nn_out, dN.p, sizeof(int32_t) * nz, cudaMemcpyDeviceToHost, st.s));
+  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  return FMGP_OK;
+}
+
 }  // namespace
+
+namespace fmgp_capi {
+
+bool stage_timing_on() { return g_stage_timing.load(std::memory_order_relaxed) != 0; }
+
+void stage_push(cudaEvent_t knn_begin, cudaEvent_t knn_end, cudaEvent_t solve_end) {
+  StageEvents ev{};
+  ev.e[0] = knn_begin;
+  ev.e[1] = knn_end;
+  ev.e[2] = solve_end;
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  g_stage_events.push_back(ev);
+}
+
+cudaError_t replica_finish(fmgp_model_replica& r, int64_t n, int32_t d, int32_t m, const double* mean_offset_host) {
+  cudaError_t e = cudaMalloc(&r.mo, sizeof(double) * m);
+  if (e == cudaSuccess) e = cudaMemcpy(r.mo, mean_offset_host, sizeof(double) * m, cudaMemcpyHostToDevice);
+  // the reference's model owns its NeighborIndex (fast_predict.cpp:127-129);
+  // here that is the predict walk's cell grid of X, built once per replica
+  if (e == cudaSuccess && d <= 3 && !knn_force_brute()) r.grid = fmgp::predict_grid_cache_build(r.X, n, d, 0, &e);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e;
+}
+
+void replica_release(fmgp_model_replica& r) {
+  cudaSetDevice(r.device);
+  if (r.grid) fmgp::predict_grid_cache_free(r.grid);
+  if (r.owns) {
+    if (r.X) cudaFree(r.X);
+    if (r.S) cudaFree(r.S);
+    if (r.C) cudaFree(r.C);
+  }
+  if (r.mo) cudaFree(r.mo);
+  r = fmgp_model_replica{};
+}
+
+}  // namespace fmgp_capi
 
 namespace fmgp {
 static std::atomic<int64_t> g_launches{0};
@@ -127,18 +188,7 @@ struct fmgp_index {
   int64_t n = 0;
   int32_t d = 0;
   double* P = nullptr;
-};
-
-struct fmgp_model {
-  int device = 0;
-  int64_t n = 0;
-  int32_t d = 0, k = 0, m = 0;
-  fmgp::KParams kp{};
-  double* X = nullptr;
-  int32_t* S = nullptr;
-  double* C = nullptr;
-  double* mo = nullptr;
-  void* grid = nullptr;  // predict-walk grid of X (d <= 3), built once at create
+  void* grid = nullptr;  // nearest-point walk grid of P (d <= 3), built once at create
 };
 
 // Host-buffer precompute of rows [row_begin, row_end) (X, Y full; S_out and
@@ -335,6 +385,7 @@ int fmgp_precompute(const double* X, const double* Y, int64_t n, int32_t d, int3
   // listed devices, one host thread per device running the shard path into
   // the caller's buffers. Rows are independent, so S and C are identical for
   // any device list; a failure reports the lowest failing row over all shards.
+  DeviceGuard dg;
   std::vector<int> devs;
   if (const char* e = std::getenv("FMGP_DEVICES")) {
     for (const char* p = e; *p;) {
@@ -481,6 +532,7 @@ int fmgp_query_knn(const double* P, int64_t np, int32_t d, const double* Q, int6
   if (exclude != nullptr)
     for (int64_t q = 0; q < nq; ++q) any_excl |= exclude[q] >= 0;
   if (k < 1 || k > np - (any_excl ? 1 : 0)) return fail(FMGP_EINVAL, "query_knn: k out of range");
+  if (!all_finite(Q, nq * d)) return fail(FMGP_EINVAL, "query_knn: non-finite query");
   if ((rc = require_device()) != FMGP_OK) return rc;
   if (nq <= 0) return FMGP_OK;
   Stream st;
@@ -518,6 +570,7 @@ int fmgp_nearest_device(const double* P, int64_t np, int32_t d, const double* Q,
 int fmgp_nearest(const double* P, int64_t np, int32_t d, const double* Q, int64_t nq, int32_t* idx_out) {
   int rc;
   if ((rc = check_points(P, np, d)) != FMGP_OK) return rc;
+  if (!all_finite(Q, nq * d)) return fail(FMGP_EINVAL, "nearest_training_point: non-finite query");
   if ((rc = require_device()) != FMGP_OK) return rc;
   if (nq <= 0) return FMGP_OK;
   Stream st;
@@ -541,6 +594,8 @@ int fmgp_index_create(const double* P, int64_t np, int32_t d, int32_t device, fm
   int rc;
   if ((rc = check_points(P, np, d)) != FMGP_OK) return rc;
   if ((rc = require_device()) != FMGP_OK) return rc;
+  DeviceGuard dg;
+  if (device < 0) FMGP_CUDA(cudaGetDevice(&device));  // -1: the calling thread's current device
   FMGP_CUDA(cudaSetDevice(device));
   auto* ix = new fmgp_index();
   ix->device = device;
@@ -548,6 +603,7 @@ int fmgp_index_create(const double* P, int64_t np, int32_t d, int32_t device, fm
   ix->d = d;
   cudaError_t e = cudaMalloc(&ix->P, sizeof(double) * np * d);
   if (e == cudaSuccess) e = cudaMemcpy(ix->P, P, sizeof(double) * np * d, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && d <= 3 && !knn_force_brute()) ix->grid = fmgp::predict_grid_cache_build(ix->P, np, d, 0, &e);
   if (e != cudaSuccess) {
     fmgp_index_destroy(ix);
     return cuda_fail(e, "fmgp_index_create");
@@ -558,7 +614,9 @@ int fmgp_index_create(const double* P, int64_t np, int32_t d, int32_t device, fm
 
 void fmgp_index_destroy(fmgp_index* ix) {
   if (ix == nullptr) return;
+  DeviceGuard dg;
   cudaSetDevice(ix->device);
+  if (ix->grid) fmgp::predict_grid_cache_free(ix->grid);
   if (ix->P) cudaFree(ix->P);
   delete ix;
 }
@@ -571,6 +629,8 @@ int fmgp_index_query_knn(const fmgp_index* ix, const double* Q, int64_t nq, int3
     for (int64_t q = 0; q < nq; ++q) any_excl |= exclude[q] >= 0;
   if (k < 1 || k > ix->n - (any_excl ? 1 : 0)) return fail(FMGP_EINVAL, "query_knn: k out of range");
   if (nq <= 0) return FMGP_OK;
+  if (!all_finite(Q, nq * ix->d)) return fail(FMGP_EINVAL, "query_knn: non-finite query");
+  DeviceGuard dg;
   FMGP_CUDA(cudaSetDevice(ix->device));
   Stream st;
   FMGP_CUDA(st.create());
@@ -595,6 +655,9 @@ int fmgp_index_query_knn(const fmgp_index* ix, const double* Q, int64_t nq, int3
 int fmgp_index_nearest(const fmgp_index* ix, const double* Q, int64_t nq, int32_t* idx_out) {
   if (ix == nullptr) return fail(FMGP_EINVAL, "null index");
   if (nq <= 0) return FMGP_OK;
+  // the reference returns -1 for a NaN query and its caller indexes with it
+  if (!all_finite(Q, nq * ix->d)) return fail(FMGP_EINVAL, "nearest_training_point: non-finite query");
+  DeviceGuard dg;
   FMGP_CUDA(cudaSetDevice(ix->device));
   Stream st;
   FMGP_CUDA(st.create());
@@ -603,7 +666,15 @@ int fmgp_index_nearest(const fmgp_index* ix, const double* Q, int64_t nq, int32_
   FMGP_CUDA(dQ.alloc(static_cast<size_t>(nq) * ix->d, st.s));
   FMGP_CUDA(dI.alloc(static_cast<size_t>(nq), st.s));
   FMGP_CUDA(cudaMemcpyAsync(dQ.p, Q, sizeof(double) * nq * ix->d, cudaMemcpyHostToDevice, st.s));
-  FMGP_CUDA(fmgp::knn_exact(dQ.p, nq, ix->P, ix->n, ix->d, 1, -1, nullptr, 0, dI.p, nullptr, num_sms_current(), st.s));
+  if (ix->grid != nullptr) {  // the cached walk grid, nearest only (no gather)
+    fmgp::KParams none{};
+    none.kind = 1;
+    FMGP_CUDA(fmgp::predict_grid_cached(ix->grid, ix->P, nullptr, nullptr, 1, 1, none, nullptr, dQ.p, nq, nullptr,
+                                        dI.p, num_sms_current(), st.s));
+  } else {
+    FMGP_CUDA(fmgp::knn_exact(dQ.p, nq, ix->P, ix->n, ix->d, 1, -1, nullptr, 0, dI.p, nullptr, num_sms_current(),
+                              st.s));
+  }
   FMGP_CUDA(cudaMemcpyAsync(idx_out, dI.p, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st.s));
   FMGP_CUDA(cudaStreamSynchronize(st.s));
   return FMGP_OK;
@@ -614,6 +685,7 @@ int fmgp_index_distances(const fmgp_index* ix, const double* q, const int32_t* i
   for (int64_t e = 0; e < cnt; ++e)
     if (idx[e] < 0 || idx[e] >= ix->n) return fail(FMGP_EINVAL, "distance_to: bad query or index");
   if (cnt <= 0) return FMGP_OK;
+  DeviceGuard dg;
   FMGP_CUDA(cudaSetDevice(ix->device));
   Stream st;
   FMGP_CUDA(st.create());
@@ -664,26 +736,26 @@ int fmgp_model_create(const double* X, const int32_t* S, const double* C, int64_
     if (S[i * k] != static_cast<int32_t>(i))
       return fail(FMGP_EINVAL, "neighbor table row does not start with its own index");
   if ((rc = require_device()) != FMGP_OK) return rc;
+  DeviceGuard dg;
+  if (device < 0) FMGP_CUDA(cudaGetDevice(&device));  // -1: the calling thread's current device
   FMGP_CUDA(cudaSetDevice(device));
   auto* mdl = new fmgp_model();
-  mdl->device = device;
   mdl->n = n;
   mdl->d = d;
   mdl->k = k;
   mdl->m = m;
   mdl->kp = kp;
+  mdl->reps.emplace_back();
+  fmgp_model_replica& r = mdl->reps.back();
+  r.device = device;
   cudaError_t e = cudaSuccess;
-  if (e == cudaSuccess) e = cudaMalloc(&mdl->X, sizeof(double) * n * d);
-  if (e == cudaSuccess) e = cudaMalloc(&mdl->S, sizeof(int32_t) * n * k);
-  if (e == cudaSuccess) e = cudaMalloc(&mdl->C, sizeof(double) * n * k * m);
-  if (e == cudaSuccess) e = cudaMalloc(&mdl->mo, sizeof(double) * m);
-  if (e == cudaSuccess) e = cudaMemcpy(mdl->X, X, sizeof(double) * n * d, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(mdl->S, S, sizeof(int32_t) * n * k, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(mdl->C, C, sizeof(double) * n * k * m, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(mdl->mo, mean_offset, sizeof(double) * m, cudaMemcpyHostToDevice);
-  // the reference's model owns its NeighborIndex (fast_predict.cpp:127-129);
-  // here that is the predict walk's cell grid of X, built once per handle
-  if (e == cudaSuccess && d <= 3 && !knn_force_brute()) mdl->grid = fmgp::predict_grid_cache_build(mdl->X, n, d, 0, &e);
+  if (e == cudaSuccess) e = cudaMalloc(&r.X, sizeof(double) * n * d);
+  if (e == cudaSuccess) e = cudaMalloc(&r.S, sizeof(int32_t) * n * k);
+  if (e == cudaSuccess) e = cudaMalloc(&r.C, sizeof(double) * n * k * m);
+  if (e == cudaSuccess) e = cudaMemcpy(r.X, X, sizeof(double) * n * d, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(r.S, S, sizeof(int32_t) * n * k, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(r.C, C, sizeof(double) * n * k * m, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = replica_finish(r, n, d, m, mean_offset);
   if (e != cudaSuccess) {
     fmgp_model_destroy(mdl);
     return cuda_fail(e, "fmgp_model_create");
@@ -692,35 +764,88 @@ int fmgp_model_create(const double* X, const int32_t* S, const double* C, int64_
   return FMGP_OK;
 }
 
+int fmgp_model_wrap_device(const double* X, const int32_t* S, const double* C, int64_t n, int32_t d, int32_t k,
+                           int32_t m, const fmgp_kernel_params* params, const double* mean_offset, fmgp_model** out) {
+  if (out == nullptr) return fail(FMGP_EINVAL, "model output pointer is null");
+  *out = nullptr;
+  fmgp::KParams kp;
+  int rc;
+  if ((rc = make_kparams(params, &kp)) != FMGP_OK) return rc;
+  if ((rc = check_points(nullptr, n, d)) != FMGP_OK) return rc;
+  if (k < 1 || k > n || m < 1) return fail(FMGP_EINVAL, "model: bad k or m");
+  if ((rc = require_device()) != FMGP_OK) return rc;
+  int dev = 0;
+  FMGP_CUDA(cudaGetDevice(&dev));
+  auto* mdl = new fmgp_model();
+  mdl->n = n;
+  mdl->d = d;
+  mdl->k = k;
+  mdl->m = m;
+  mdl->kp = kp;
+  mdl->reps.emplace_back();
+  fmgp_model_replica& r = mdl->reps.back();
+  r.device = dev;
+  r.owns = false;
+  r.X = const_cast<double*>(X);
+  r.S = const_cast<int32_t*>(S);
+  r.C = const_cast<double*>(C);
+  cudaError_t e = replica_finish(r, n, d, m, mean_offset);
+  if (e != cudaSuccess) {
+    fmgp_model_destroy(mdl);
+    return cuda_fail(e, "fmgp_model_wrap_device");
+  }
+  *out = mdl;
+  return FMGP_OK;
+}
+
+int fmgp_model_replicas(const fmgp_model* mdl) { return mdl == nullptr ? 0 : static_cast<int>(mdl->reps.size()); }
+
 int fmgp_model_predict(const fmgp_model* mdl, const double* Z, int64_t nz, double* out, int32_t* nn_out) {
   if (mdl == nullptr) return fail(FMGP_EINVAL, "null model");
   if (nz <= 0) return FMGP_OK;
-  FMGP_CUDA(cudaSetDevice(mdl->device));
-  Stream st;
-  FMGP_CUDA(st.create());
-  DevBuf<double> dZ, dO;
-  DevBuf<int32_t> dN;
-  FMGP_CUDA(dZ.alloc(static_cast<size_t>(nz) * mdl->d, st.s));
-  FMGP_CUDA(dO.alloc(static_cast<size_t>(nz) * mdl->m, st.s));
-  FMGP_CUDA(dN.alloc(static_cast<size_t>(nz), st.s));
-  FMGP_CUDA(cudaMemcpyAsync(dZ.p, Z, sizeof(double) * nz * mdl->d, cudaMemcpyHostToDevice, st.s));
-  int rc = predict_device_impl(mdl->X, mdl->S, mdl->C, mdl->n, mdl->d, mdl->k, mdl->m, mdl->kp, mdl->mo, dZ.p, nz,
-                               dO.p, dN.p, st.s, mdl->grid);
-  if (rc != FMGP_OK) return rc;
-  FMGP_CUDA(cudaMemcpyAsync(out, dO.p, sizeof(double) * nz * mdl->m, cudaMemcpyDeviceToHost, st.s));
-  if (nn_out) FMGP_CUDA(cudaMemcpyAsync(nn_out, dN.p, sizeof(int32_t) * nz, cudaMemcpyDeviceToHost, st.s));
-  FMGP_CUDA(cudaStreamSynchronize(st.s));
+  // a test point must have a nearest training point (the reference returns -1
+  // from nearest_training_point for a NaN query and indexes with it)
+  if (!all_finite(Z, nz * mdl->d)) return fail(FMGP_EINVAL, "fast_predict: non-finite test point");
+  DeviceGuard dg;
+  const int g = static_cast<int>(mdl->reps.size());
+  // small batches (e.g. fast_predict_one) stay on one replica
+  if (g == 1 || nz < 4096) return replica_predict_host(mdl, mdl->reps[0], Z, nz, out, nn_out);
+  // test points split contiguously over the replicas (one host thread each)
+  const int64_t per = (nz + g - 1) / g;
+  std::vector<int> rcs(g, FMGP_OK);
+  std::vector<std::string> msgs(g);
+  std::vector<std::thread> th;
+  for (int r = 0; r < g; ++r) {
+    const int64_t b = std::min<int64_t>(nz, r * per), e = std::min<int64_t>(nz, b + per);
+    th.emplace_back([&, r, b, e] {
+      rcs[r] = replica_predict_host(mdl, mdl->reps[r], Z + b * mdl->d, e - b, out + b * mdl->m,
+                                    nn_out ? nn_out + b : nullptr);
+      if (rcs[r] != FMGP_OK) msgs[r] = g_err;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int r = 0; r < g; ++r)
+    if (rcs[r] != FMGP_OK) return fail(rcs[r], msgs[r]);
   return FMGP_OK;
+}
+
+int fmgp_model_predict_device(const fmgp_model* mdl, const double* Z, int64_t nz, double* out, int32_t* nn_out,
+                              void* stream) {
+  if (mdl == nullptr) return fail(FMGP_EINVAL, "null model");
+  if (nz <= 0) return FMGP_OK;
+  int dev = 0;
+  FMGP_CUDA(cudaGetDevice(&dev));
+  for (const auto& r : mdl->reps)
+    if (r.device == dev)
+      return predict_device_impl(r.X, r.S, r.C, mdl->n, mdl->d, mdl->k, mdl->m, mdl->kp, r.mo, Z, nz, out, nn_out,
+                                 static_cast<cudaStream_t>(stream), r.grid);
+  return fail(FMGP_EINVAL, "model has no replica on the current device");
 }
 
 void fmgp_model_destroy(fmgp_model* mdl) {
   if (mdl == nullptr) return;
-  cudaSetDevice(mdl->device);
-  if (mdl->grid) fmgp::predict_grid_cache_free(mdl->grid);
-  if (mdl->X) cudaFree(mdl->X);
-  if (mdl->S) cudaFree(mdl->S);
-  if (mdl->C) cudaFree(mdl->C);
-  if (mdl->mo) cudaFree(mdl->mo);
+  DeviceGuard dg;
+  for (auto& r : mdl->reps) replica_release(r);
   delete mdl;
 }
 

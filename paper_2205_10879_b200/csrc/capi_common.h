@@ -19,6 +19,12 @@ namespace fmgp_capi {
 
 inline thread_local std::string g_err;
 
+// Stage timing (fmgp_set_stage_timing, capi.cu): is it on, and record one
+// call's events (kNN begin, kNN end = solve begin, solve end; the events
+// are destroyed by fmgp_stage_times).
+bool stage_timing_on();
+void stage_push(cudaEvent_t knn_begin, cudaEvent_t knn_end, cudaEvent_t solve_end);
+
 inline int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
@@ -133,6 +139,20 @@ struct DevBuf {
   ~DevBuf() {
     if (p) cudaFreeAsync(p, s);
   }
+};
+
+// Restores the caller's current device on scope exit (entry points that
+// switch devices must not leave the calling thread on another GPU).
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  }
+  ~DeviceGuard() {
+    if (dev >= 0) cudaSetDevice(dev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
 struct Stream {

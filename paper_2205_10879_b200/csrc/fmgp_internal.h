@@ -68,6 +68,12 @@ cudaError_t knn_grid(const double* Q, int64_t nq, const double* P, int64_t np, i
                      const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
                      cudaStream_t stream);
 
+// Precompute's S rows (self first, then kk neighbours) for the block-cyclic
+// row set of member r of g (blocks of pc rows dealt round-robin over [0, np)),
+// nrows of them, written at their global rows of `out` (np x (kk + 1)).
+cudaError_t knn_grid_rows_cyclic(const double* P, int64_t np, int d, int kk, int64_t nrows, int64_t pc, int g, int r,
+                                 int32_t* out, int num_sms, cudaStream_t stream);
+
 // Dispatcher used by the C ABI: the grid search where it applies, else brute
 // force. FMGP_KNN=brute in the environment forces brute force (A/B checks).
 cudaError_t knn_exact(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,

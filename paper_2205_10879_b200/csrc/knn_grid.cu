@@ -40,6 +40,7 @@ namespace {
 struct GridParams {
   double lo[3];
   double h, inv_h;
+  double margin;  // slack of every cell-bound test: 1e-7 h + the rounding of lo + c h (~eps |coordinates|)
   int G[3];
   int d;
   int64_t ncells;
@@ -135,11 +136,17 @@ __global__ void grid_params_kernel(const unsigned long long* __restrict__ mm, in
   p.h = h;
   p.inv_h = 1.0 / h;
   p.ncells = 1;
+  double span = 0.0;
   for (int t = 0; t < 3; ++t) {
     p.lo[t] = t < d ? lo[t] : 0.0;
     p.G[t] = t < d ? G[t] : 1;
     p.ncells *= p.G[t];
+    if (t < d) span = fmax(span, fabs(lo[t]) + G[t] * h);
   }
+  // the cell boundaries lo + c h and the cell assignment round at ~eps of the
+  // coordinates' magnitude; far from the origin (|lo| / h > ~1e9) that exceeds
+  // 1e-7 h, so the margin carries it too
+  p.margin = 1e-7 * h + 8.0 * 2.220446049250313e-16 * span;
   *gp = p;
 }
 
@@ -352,7 +359,7 @@ __device__ __forceinline__ double outside_lb_sq(const GridParams& g, const doubl
     if (c[t] + r < g.G[t] - 1) lb = fmin(lb, (g.lo[t] + (c[t] + r + 1) * g.h) - q[t]);
   }
   if (lb == INFINITY) return INFINITY;
-  lb -= 1e-7 * g.h;
+  lb -= g.margin;
   if (!(lb > 0.0)) return 0.0;
   return lb * lb * (1.0 - 1e-12);
 }
@@ -596,7 +603,7 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
         const double gap = fmax(fmax(lo_c[t] - q[t], q[t] - (lo_c[t] + g.h)), 0.0);
         slack2 += gap * gap;
       }
-      const double slack = sqrt(slack2), margin = 1e-7 * g.h;
+      const double slack = sqrt(slack2), margin = g.margin;
       for (int base = 0; base < N;) {
         const int len = base == 0 ? N0 : min(32, N - base);
         if (base > 0) {
@@ -944,7 +951,7 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
         const double gap = fmax(fmax(lo - q[t], q[t] - (lo + g.h)), 0.0);
         slack2 += gap * gap;
       }
-      const double slack = sqrt(slack2), margin = 1e-7 * g.h;
+      const double slack = sqrt(slack2), margin = g.margin;
       for (int base = 0; base < N;) {
         const int len = base == 0 ? N0 : min(32, N - base);
         if (base > 0) {
@@ -1022,7 +1029,14 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
       if (best.d < lb2) break;
     }
     const int64_t j = best.i;
+    if (j == INT_MAX) {  // no candidate ranked (non-finite or overflowing z): nn -1, NaN means, no gather
+      if (nn_out != nullptr && lane == 0) nn_out[orow] = -1;
+      if (S != nullptr)
+        for (int cc = lane; cc < m; cc += kWarp) out[orow * m + cc] = __longlong_as_double(0x7ff8000000000000ll);
+      continue;
+    }
     if (nn_out != nullptr && lane == 0) nn_out[orow] = static_cast<int32_t>(j);
+    if (S == nullptr) continue;  // nearest-only walk (NeighborIndex::nearest_training_point)
     if (m == 1 && k <= 2 * kWarp) {
       // the common shape: both 32-neighbour rounds' loads (S, C, then the X
       // gathers) are issued before any arithmetic, so the dependent gather
@@ -1074,12 +1088,16 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
   }
 }
 
+// Sorted positions of the query rows: ids in [rb, re), and with cyc_pc > 0
+// only the block-cyclic row set of member cyc_r of cyc_g (blocks of cyc_pc
+// rows dealt round-robin; the multi-GPU layout of group.cu).
 __global__ void compact_rows_kernel(const int32_t* __restrict__ pid, int64_t n, int64_t rb, int64_t re,
+                                    int64_t cyc_pc, int cyc_g, int cyc_r,
                                     int32_t* __restrict__ qpos, int32_t* __restrict__ counter) {
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t id = pid[p];
-    if (id >= rb && id < re) {
+    if (id >= rb && id < re && (cyc_pc == 0 || (id / cyc_pc) % cyc_g == cyc_r)) {
       // warp-aggregated append keeps cell order within each warp's run
       const int32_t s = atomicAdd(counter, 1);
       qpos[s] = static_cast<int32_t>(p);
@@ -1182,10 +1200,13 @@ void launch_query_e(int E, const GridParams* gp, const double* pts, const int32_
                           num_sms, s);
 }
 
+// cyc_pc > 0 (self mode only): the queries are the block-cyclic row set of
+// member cyc_r of cyc_g over all np rows (nq of them), written at their
+// global rows of `out` (row_offset 0).
 template <int D>
 cudaError_t knn_grid_d(const double* Q, int64_t nq, const double* P, int64_t np, int kk, int64_t self_offset,
                        const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
-                       cudaStream_t s) {
+                       cudaStream_t s, int64_t cyc_pc = 0, int cyc_g = 1, int cyc_r = 0) {
   const int E = kk <= 32 ? 1 : (kk <= 64 ? 2 : 4);
   // Points per cell: enough that the radius-1 block usually holds the kk-th neighbour.
   // Points per cell. d = 1: enough that the radius-1 block usually holds the
@@ -1221,7 +1242,16 @@ cudaError_t knn_grid_d(const double* Q, int64_t nq, const double* P, int64_t np,
   cell_sort<D>(P, np, gp, ncap, pb, s);
 
   const bool self_mode = excl_arr == nullptr && self_offset >= 0 && Q == P + self_offset * D;
-  if (self_mode && self_offset == 0 && nq == np) {
+  if (cyc_pc > 0) {
+    err = cudaMallocAsync(&qpos, sizeof(int32_t) * (nq > 0 ? nq : 1), s);
+    if (err == cudaSuccess) err = cudaMallocAsync(&cnt, sizeof(int32_t), s);
+    if (err != cudaSuccess) return err;
+    cudaMemsetAsync(cnt, 0, sizeof(int32_t), s);
+    compact_rows_kernel<<<grid1d(np), 256, 0, s>>>(pb.pid, np, 0, np, cyc_pc, cyc_g, cyc_r, qpos, cnt);
+    note_launches(1);
+    launch_query_e<D>(E, gp, pb.pts, pb.pid, pb.cstart, nq, qpos, nullptr, nullptr, nullptr, kk, with_self, 0, out,
+                      out_d, num_sms, s);
+  } else if (self_mode && self_offset == 0 && nq == np) {
     // every training row is a query: walk them in cell order
     launch_query_e<D>(E, gp, pb.pts, pb.pid, pb.cstart, nq, nullptr, nullptr, nullptr, nullptr, kk, with_self, 0,
                       out, out_d, num_sms, s);
@@ -1231,7 +1261,7 @@ cudaError_t knn_grid_d(const double* Q, int64_t nq, const double* P, int64_t np,
     if (err == cudaSuccess) err = cudaMallocAsync(&cnt, sizeof(int32_t), s);
     if (err != cudaSuccess) return err;
     cudaMemsetAsync(cnt, 0, sizeof(int32_t), s);
-    compact_rows_kernel<<<grid1d(np), 256, 0, s>>>(pb.pid, np, self_offset, self_offset + nq, qpos, cnt);
+    compact_rows_kernel<<<grid1d(np), 256, 0, s>>>(pb.pid, np, self_offset, self_offset + nq, 0, 1, 0, qpos, cnt);
     note_launches(1);
     launch_query_e<D>(E, gp, pb.pts, pb.pid, pb.cstart, nq, qpos, nullptr, nullptr, nullptr, kk, with_self,
                       self_offset, out, out_d, num_sms, s);
@@ -1416,6 +1446,17 @@ cudaError_t knn_grid(const double* Q, int64_t nq, const double* P, int64_t np, i
     case 1: return knn_grid_d<1>(Q, nq, P, np, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
     case 2: return knn_grid_d<2>(Q, nq, P, np, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
     case 3: return knn_grid_d<3>(Q, nq, P, np, kk, self_offset, excl_arr, with_self, out, out_d, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t knn_grid_rows_cyclic(const double* P, int64_t np, int d, int kk, int64_t nrows, int64_t pc, int g, int r,
+                                 int32_t* out, int num_sms, cudaStream_t stream) {
+  if (nrows <= 0) return cudaSuccess;
+  switch (d) {
+    case 1: return knn_grid_d<1>(P, nrows, P, np, kk, 0, nullptr, 1, out, nullptr, num_sms, stream, pc, g, r);
+    case 2: return knn_grid_d<2>(P, nrows, P, np, kk, 0, nullptr, 1, out, nullptr, num_sms, stream, pc, g, r);
+    case 3: return knn_grid_d<3>(P, nrows, P, np, kk, 0, nullptr, 1, out, nullptr, num_sms, stream, pc, g, r);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -129,3 +129,87 @@ cudaError_t self_rows_launch(int32_t* S, int64_t nrows, int64_t row_begin, cudaS
 }
 
 }  // namespace fmgp
+
+// ---------------------------------------------------------------- diagnostics
+// The FP64 roofline denominators of this GPU, measured in the caller's
+// process (bench.py reports the solve's FP64 fraction against them):
+// independent DFMA chains and DMMA m8n8k4 chains over the whole chip.
+namespace fmgp {
+namespace {
+
+constexpr int kPeakChains = 8;
+constexpr int kPeakIters = 4096;
+
+__global__ void peak_dfma_kernel(double* out, double a, double b) {
+  double x[kPeakChains];
+#pragma unroll
+  for (int c = 0; c < kPeakChains; ++c) x[c] = threadIdx.x * 1e-3 + c;
+  for (int i = 0; i < kPeakIters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kPeakChains; ++c) x[c] = fma(x[c], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < kPeakChains; ++c) s += x[c];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void peak_dmma_kernel(double* out, double a, double b) {
+  double c[kPeakChains][2];
+#pragma unroll
+  for (int q = 0; q < kPeakChains; ++q) c[q][0] = c[q][1] = threadIdx.x * 1e-3 + q;
+  for (int i = 0; i < kPeakIters; ++i) {
+#pragma unroll
+    for (int q = 0; q < kPeakChains; ++q)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(c[q][0]), "+d"(c[q][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int q = 0; q < kPeakChains; ++q) s += c[q][0] + c[q][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+}  // namespace
+}  // namespace fmgp
+
+extern "C" int fmgp_diag_fp64_peak(double* dfma_tflops, double* dmma_tflops) {
+  using namespace fmgp;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 3;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* sink = nullptr;
+  if (cudaMalloc(&sink, sizeof(double)) != cudaSuccess) return 3;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, threads = 256;
+  const double fma_flops = 2.0 * blocks * threads * kPeakChains * double(kPeakIters);
+  const double mma_flops = 512.0 * (blocks * threads / 32) * kPeakChains * double(kPeakIters);
+  float best_f = 1e30f, best_m = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    float t = 0.f;
+    cudaEventRecord(e0);
+    peak_dfma_kernel<<<blocks, threads>>>(sink, 0.999, 1e-3);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&t, e0, e1);
+    if (rep > 0) best_f = t < best_f ? t : best_f;
+    cudaEventRecord(e0);
+    peak_dmma_kernel<<<blocks, threads>>>(sink, 0.999, 1e-3);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&t, e0, e1);
+    if (rep > 0) best_m = t < best_m ? t : best_m;
+  }
+  note_launches(8);
+  const cudaError_t err = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (err != cudaSuccess) return 3;
+  if (dfma_tflops) *dfma_tflops = fma_flops / (best_f * 1e-3) / 1e12;
+  if (dmma_tflops) *dmma_tflops = mma_flops / (best_m * 1e-3) / 1e12;
+  return 0;
+}

@@ -8,6 +8,8 @@
 // warp computes each distance cooperatively with coalesced row loads, tree
 // reduction order) and reused for every output column; each sum is then
 // accumulated in the reference's sequential t order (shuffle chain).
+#include <climits>
+
 #include "fmgp_common.cuh"
 #include "fmgp_internal.h"
 
@@ -46,6 +48,10 @@ predict_kernel(const double* __restrict__ X, const int32_t* __restrict__ S, cons
   const bool coop = d >= kWarp;
   for (int64_t zi = warp_global; zi < nz; zi += nwarps) {
     const int64_t j = nn[zi];
+    if (j < 0 || j == INT_MAX) {  // no nearest point (non-finite or overflowing z): NaN, no gather
+      for (int c = lane; c < m; c += kWarp) out[zi * m + c] = __longlong_as_double(0x7ff8000000000000ll);
+      continue;
+    }
     const double* z = Z + zi * d;
     // kernel values of the k neighbours, once per test point: lane l holds t = l + 32 s
     double kv[kMaxKv];

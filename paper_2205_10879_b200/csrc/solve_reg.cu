@@ -288,8 +288,9 @@ __device__ void build_reg(const double* __restrict__ X, const double* __restrict
 // d^2 = G_ii + G_jj - 2 G_ij (clamped at 0) feeds the kernel. Cost per pair
 // ~2d/16 DMMA-thread ops instead of 2d scalar ops with two shared loads; the
 // distance differs from the reference's sum of squared differences by
-// rounding relative to |x|^2 (1e-15 at cfg3), far inside the coefficient
-// tolerance. A pair with d^2 <= 1e-12 (G_ii + G_jj) is recomputed exactly
+// rounding relative to the neighbourhood's squared extent (coordinates are
+// centred on the query point first), far inside the coefficient tolerance.
+// A pair with d^2 <= 1e-12 (G_ii + G_jj) is recomputed exactly
 // from X (sum of squared differences), so exact duplicates keep the nugget
 // (kernel.cpp:106-119) bit for bit. The next chunk's coordinates are loaded
 // from global memory while the current chunk's MMAs run.
@@ -312,18 +313,23 @@ __device__ void build_gram(const double* __restrict__ X, const double* __restric
   for (int I = 0; I < 4; ++I)
 #pragma unroll
     for (int J = 0; J < 4; ++J) acc[I][J][0] = acc[I][J][1] = 0.0;
-  // gather slots: element e = lane + 32 u of a 32 x 16 chunk is (row e >> 4, dim e & 15)
-  const int64_t rowoff0 = static_cast<int64_t>(sr[lane >> 4 < K ? lane >> 4 : 0]) * d;
+  // gather slots: element e = lane + 32 u of a 32 x 16 chunk is (row e >> 4, dim e & 15).
+  // Coordinates are taken relative to the neighbourhood's first point (its
+  // query row, S[i][0] = i): the Gram form d^2 = G_ii + G_jj - 2 G_ij then
+  // loses digits relative to the neighbourhood's extent, not to |x|^2 (data
+  // far from the origin keeps the coefficient tolerance).
+  const double* x0 = X + static_cast<int64_t>(sr[0]) * d;
   double pre[16];
   auto gather = [&](int c0) {
+    const int dim = lane & 15;
+    const double ref = c0 + dim < d ? x0[c0 + dim] : 0.0;
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const int row = (lane >> 4) + 2 * u, dim = lane & 15;
+      const int row = (lane >> 4) + 2 * u;
       const bool ok = row < K && c0 + dim < d;
-      pre[u] = ok ? X[static_cast<int64_t>(sr[row < K ? row : 0]) * d + c0 + dim] : 0.0;
+      pre[u] = ok ? X[static_cast<int64_t>(sr[row < K ? row : 0]) * d + c0 + dim] - ref : 0.0;
     }
   };
-  (void)rowoff0;
   gather(0);
   for (int c0 = 0; c0 < d; c0 += 16) {
 #pragma unroll

@@ -1,17 +1,20 @@
 """Multi-GPU sharding of the path: one process per GPU.
 
-* Precompute: X and Y are replicated on every rank; training rows (the kNN /
-  solve queries) are split into contiguous, rank-ordered shards; each rank
-  computes its S and C rows against the full X, then the shards are
-  all-gathered (NCCL over NVLink on B200s; gloo in the CPU tests). Every row's
-  arithmetic is independent of the shard layout, so S and C are bit-identical
-  for any world size.
-* Predict: test points are split the same way; no collective is needed (each
-  rank holds the full replicated model after the gather).
+The product's multi-GPU precompute is the C ABI's device group
+(csrc/group.cu: fmgp_group_create_rank / fmgp_group_precompute[_device]),
+which bench.py drives: X and Y replicated on every rank, training rows (the
+kNN / solve queries) dealt block-cyclically, S and C all-gathered in place
+over NVLink by NCCL from C++, each round's exchange overlapped with the next
+round's solve. This module is the same host logic over torch.distributed
+(`overlapped_precompute`, `cyclic_blocks`), so the layout and the exchange
+order are testable on CPU with a gloo process group (tests/test_parallel.py),
+plus the plain contiguous-shard helpers. Every row's arithmetic is
+independent of the layout, so S and C are bit-identical for any world size.
+Predict: test points are split contiguously; no collective is needed (each
+rank holds the full replicated model after the gather).
 
-The per-shard compute is injected (`compute_shard`), so the host-side logic
-is testable on CPU with a gloo process group; the product passes the
-fmgp_precompute_device launcher.
+The per-shard compute is injected, so CPU tests pass the oracle while a GPU
+caller passes the fmgp_*_device launchers.
 """
 from __future__ import annotations
 
@@ -61,6 +64,20 @@ def sharded_precompute(n: int, compute_shard: Callable[[int, int], tuple[torch.T
     return S, C
 
 
+def cyclic_blocks(n: int, world: int, rounds: int = 4) -> tuple[int, list[list[tuple[int, int]]]]:
+    """The block-cyclic row layout of the C ABI's device groups (csrc/group.cu,
+    fmgp_group_rows): blocks of pc = ceil(n / (world * rounds)) rows dealt
+    round-robin; round c is rows [c*world*pc, (c+1)*world*pc) and member r owns
+    its block c*world + r. Returns pc and, per round, every member's [b, e)."""
+    pc = max(1, -(-n // (world * rounds)))
+    out = []
+    c = 0
+    while c * world * pc < n:
+        out.append([(min(n, (c * world + r) * pc), min(n, (c * world + r) * pc + pc)) for r in range(world)])
+        c += 1
+    return pc, out
+
+
 class _Side:
     """A side stream for collectives on CUDA tensors; a no-op on CPU (gloo tests)."""
 
@@ -89,61 +106,82 @@ class _Null:
         return False
 
 
+def _exchange_round(buf: torch.Tensor, blocks: list[tuple[int, int]], rank: int, group=None) -> None:
+    """Every member's block of one round into every member's `buf`, in place.
+    A full round (equal blocks, contiguous) is one all-gather whose send buffer
+    is this rank's block of the receive buffer; a short last round is one
+    broadcast per member."""
+    world = len(blocks)
+    sizes = {e - b for b, e in blocks}
+    if len(sizes) == 1 and blocks[-1][1] - blocks[0][0] == world * (blocks[0][1] - blocks[0][0]):
+        b0, e_last = blocks[0][0], blocks[-1][1]
+        region = buf[b0:e_last]
+        mine = buf[blocks[rank][0]:blocks[rank][1]]
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(region, mine, group=group)
+        else:
+            parts = [buf[b:e] for b, e in blocks]
+            tmp = [torch.empty_like(mine) for _ in parts]
+            dist.all_gather(tmp, mine.contiguous(), group=group)
+            for p_, t in zip(parts, tmp):
+                p_.copy_(t)
+        return
+    for q, (b, e) in enumerate(blocks):
+        if e > b:
+            view = buf[b:e]
+            if view.is_contiguous():
+                dist.broadcast(view, src=q, group=group)
+            else:
+                t = view.contiguous()
+                dist.broadcast(t, src=q, group=group)
+                view.copy_(t)
+
+
 def overlapped_precompute(n: int, k: int, m: int, knn_rows: Callable[[int, int], torch.Tensor],
                           solve_rows: Callable[[torch.Tensor, int, torch.Tensor], None], nchunks: int = 4,
                           group=None, device: torch.device | None = None) -> tuple[torch.Tensor, torch.Tensor]:
-    """sharded_precompute with the exchange overlapped: K1 for this rank's rows
-    (knn_rows(b, e) -> S rows), the S all-gather then runs on a side stream
-    while K2 solves the shard in `nchunks` chunks (solve_rows(S_rows, row_begin,
-    C_rows) writes C rows, stream-ordered); each chunk's C all-gather is issued
-    on the side stream as soon as the chunk is solved, so it overlaps the next
-    chunk's solve. Every rank returns the full S (n x k) and C (n x k x m),
-    bit-identical to sharded_precompute (rows are independent)."""
+    """The device-group precompute of csrc/group.cu, host logic in Python:
+    block-cyclic rows (cyclic_blocks); K1 for this rank's blocks
+    (knn_rows(b, e) -> S rows), S exchanged in place per round on a side
+    stream; then per round K2 of this rank's block (solve_rows(S_rows,
+    row_begin, C_rows) writes C rows, stream-ordered) followed by that round's
+    in-place C exchange on the side stream, overlapping the next round's solve.
+    No staging copies. Every rank returns the full S (n x k) and C (n x k x m),
+    bit-identical to a single rank (rows are independent)."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    b, e, per = shard_bounds(n, world, rank)
-    rows = e - b
-    S_loc = knn_rows(b, e)
-    dev = S_loc.device if device is None else device
+    _, rounds = cyclic_blocks(n, world, nchunks)
+    dev = device
+    S_all = C_all = None
+    for blocks in rounds:
+        b, e = blocks[rank]
+        if e > b:
+            S_loc = knn_rows(b, e)
+            if S_all is None:
+                dev = S_loc.device if device is None else device
+                S_all = torch.empty((n, k), dtype=torch.int32, device=dev)
+            S_all[b:e] = S_loc
+    if S_all is None:  # a rank without rows (n < world)
+        dev = torch.device("cpu") if device is None else device
+        S_all = torch.empty((n, k), dtype=torch.int32, device=dev)
+    C_all = torch.empty((n, k, m), dtype=torch.float64, device=dev)
     if world == 1:
-        C_loc = torch.empty((rows, k, m), dtype=torch.float64, device=dev)
-        solve_rows(S_loc, b, C_loc)
-        return S_loc, C_loc
+        for blocks in rounds:
+            b, e = blocks[0]
+            solve_rows(S_all[b:e], b, C_all[b:e])
+        return S_all, C_all
     side = _Side(dev)
-    S_pad = torch.zeros((per, k), dtype=torch.int32, device=dev)
-    S_pad[:rows] = S_loc
-    S_all = torch.empty((world * per, k), dtype=torch.int32, device=dev)
     with side.after_main():
-        _all_gather_into(S_all, S_pad, group)
-    C_pad = torch.zeros((per, k, m), dtype=torch.float64, device=dev)
-    C_all = torch.empty((world, per, k, m), dtype=torch.float64, device=dev)
-    pc = (per + nchunks - 1) // nchunks
-    staging = []
-    for lo in range(0, per, pc):
-        hi = min(per, lo + pc)
-        r_lo, r_hi = min(rows, lo), min(rows, hi)
-        if r_hi > r_lo:
-            solve_rows(S_loc[r_lo:r_hi], b + r_lo, C_pad[r_lo:r_hi])
-        g = torch.empty((world * (hi - lo), k, m), dtype=torch.float64, device=dev)
-        staging.append(g)
+        for blocks in rounds:
+            _exchange_round(S_all, blocks, rank, group)
+    for blocks in rounds:
+        b, e = blocks[rank]
+        if e > b:
+            solve_rows(S_all[b:e], b, C_all[b:e])
         with side.after_main():
-            _all_gather_into(g, C_pad[lo:hi], group)
-            C_all[:, lo:hi].copy_(g.view(world, hi - lo, k, m))
+            _exchange_round(C_all, blocks, rank, group)
     side.join()
-    return S_all[:n], C_all.view(world * per, k, m)[:n]
-
-
-def _all_gather_into(out: torch.Tensor, local: torch.Tensor, group=None) -> None:
-    """out (world * rows, ...) <- the ranks' `local` (rows, ...) in rank order."""
-    local = local.contiguous()
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(out, local, group=group)
-    else:
-        parts = list(out.chunk(dist.get_world_size(group), 0))
-        tmp = [torch.empty_like(local) for _ in parts]
-        dist.all_gather(tmp, local, group=group)
-        for p_, t in zip(parts, tmp):
-            p_.copy_(t)
+    return S_all, C_all
 
 
 def sharded_predict(nz: int, predict_shard: Callable[[int, int], torch.Tensor], gather: bool = False,

@@ -52,6 +52,10 @@ def datasets():
     yield "clusters2", np.concatenate([rng.normal(0, 1e-3, (1500, 2)), rng.normal(5, 1.0, (1500, 2))])
     yield "degenerate3", np.column_stack([rng.random(2000), np.zeros(2000), rng.random(2000)])  # a flat dim
     yield "line2", np.column_stack([np.linspace(0, 1, 1000), np.linspace(0, 1, 1000)])
+    # far from the origin compared with the spacing (|lo| / h ~ 1e13): the cell
+    # bounds' rounding (~eps |x|) exceeds 1e-7 h, the grid margin must carry it
+    yield "far2", rng.random((3000, 2)) * 1e-3 + np.array([1e9, -3e8])
+    yield "far3", rng.random((3000, 3)) * 1e-2 + 5e8
 
 
 def test_grid_matches_oracle_small(tmp_path, port):

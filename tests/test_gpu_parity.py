@@ -312,17 +312,21 @@ def test_split_knn_and_chunked_async_solve_equal_precompute_device(fm):
     assert int(fail.item()) == ei.value.failed_row
 
 
+@pytest.mark.parametrize("offset", [0.0, 1e3])
 @pytest.mark.parametrize("m", [1, 10])
 @pytest.mark.parametrize("d", [32, 100, 784])
-def test_gram_build_matches_oracle(fm, port, d, m):
+def test_gram_build_matches_oracle(fm, port, d, m, offset):
     # k = 30 at d >= 32 builds the neighbourhood matrices from a DMMA Gram
     # matrix (solve_reg.cu build_gram), on sparse cfg3-like rows. Exact
     # duplicates (d^2 = 0 -> nugget, an exactly singular block) are covered by
     # test_numeric_error_names_lowest_failing_row[30-40]: the ladder is only
     # exhausted there if the Gram path detects the zero distance exactly.
+    # offset = 1e3: every point moved far from the origin compared with the
+    # neighbour spacing (the Gram form then needs the centring on the query
+    # point, else d^2 = G_ii + G_jj - 2 G_ij loses ~eps |x|^2 / d^2 digits)
     rng = np.random.default_rng(7 * d + m)
     n, k = 600, 30
-    X = rng.random((n, d)) * (rng.random((n, d)) < 0.2)
+    X = rng.random((n, d)) * (rng.random((n, d)) < 0.2) + offset
     Y = rng.standard_normal((n, m))
     p = fm.KernelParams(1.0, 10.0, 0.5, 0.1)
     model = fm.precompute(fm.TrainingSet(X, Y if m > 1 else Y[:, 0], 0.0),

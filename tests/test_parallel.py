@@ -132,3 +132,41 @@ def test_overlapped_gather_is_bit_identical_to_one_rank(world):
     i = ds.info
     S1, C1 = Port().precompute_rows(ds.X, ds.Y, i.kind, i.sigma, i.rho, i.nu, i.tau, 9)
     assert np.array_equal(S1, S2) and np.array_equal(C1, C2)
+
+
+@pytest.mark.parametrize("n", [1, 5, 301, 1000, 8_000_000])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_cyclic_layout_matches_the_c_abi(n, world):
+    # the Python mirror and csrc/group.cu deal the same blocks (fmgp_group_rows
+    # needs no device), and every row is owned exactly once
+    import ctypes as C
+    from paper_2205_10879_b200 import _native as N
+    from paper_2205_10879_b200.parallel import cyclic_blocks
+    _, rounds = cyclic_blocks(n, world)
+    owned = np.zeros(n, dtype=np.int64)
+    for r in range(world):
+        mine = [blk[r] for blk in rounds if blk[r][1] > blk[r][0]]
+        nb = C.c_int64(-1)
+        assert N.LIB.fmgp_group_rows(n, world, r, C.byref(nb), None) == 0
+        rg = np.zeros(2 * max(nb.value, 1), dtype=np.int64)
+        assert N.LIB.fmgp_group_rows(n, world, r, C.byref(nb), rg.ctypes.data_as(C.c_void_p)) == 0
+        assert [(int(rg[2 * i]), int(rg[2 * i + 1])) for i in range(nb.value)] == mine
+        for b, e in mine:
+            owned[b:e] += 1
+    assert (owned == 1).all()
+
+
+def test_bench_gpus_flag_launches_that_many_ranks():
+    # `python bench.py --gpus 2` (the driver's form, no torchrun) re-launches
+    # itself with one process per GPU; the probe makes every rank join a gloo
+    # group and rank 0 report the count
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    repo = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(repo / "bench.py"), "--gpus", "2", "--probe-launch"],
+                         capture_output=True, text=True, timeout=300, cwd=repo)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_ranks"] == 2 and line["world_size"] == 2
