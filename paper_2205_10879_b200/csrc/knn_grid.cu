@@ -450,7 +450,7 @@ __device__ __forceinline__ int32_t ord_entry(int i) {
 #define FMGP_GQ_MINB 4
 #endif
 #ifndef FMGP_GP_MINB
-#define FMGP_GP_MINB 4
+#define FMGP_GP_MINB 3
 #endif
 template <int D, int E>
 __global__ void __launch_bounds__(kQueryThreads, FMGP_GQ_MINB)
@@ -864,43 +864,17 @@ grid_query_thread_kernel(const GridParams* __restrict__ gpp, const double* __res
   }
 }
 
-// Fused predict for d <= 3 (fast_predict_one, fast_predict.cpp:132-144): one
-// warp per test point finds the nearest training point (argmin over
-// (key, index), the reference's std::min over pairs) with the same
-// distance-ordered cell walk as grid_query_kernel (cells of ~1.5 points in
-// 2-D, ~1 in 3-D: the 3^D block almost always holds the answer and the next
-// chunk's static bound stops the walk), then evaluates the k
-// cross-covariances (kernel_from_sq_build, KF = kernel kind) against C_j and
-// reduces the dot over the warp by a shuffle tree, without writing the 1-NN
-// index out in between. The sum order differs from the reference's
-// sequential loop by rounding only (posterior means within 1e-15 relative of
-// the sequential sum here, tolerance 1e-9).
-template <int D, int KF>
-__global__ void __launch_bounds__(kQueryThreads, FMGP_GP_MINB)
-grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
-                    const int32_t* __restrict__ cstart, int64_t nq, const double* __restrict__ Qs,
-                    const int32_t* __restrict__ qout, const double* __restrict__ X, const int32_t* __restrict__ S,
-                    const double* __restrict__ Cf, int k, int m, KParams kp, const double* __restrict__ mean_offset,
-                    double* __restrict__ out, int32_t* __restrict__ nn_out) {
-  __shared__ int32_t s_beg[kQueryThreads / 32][kSlots];
-  __shared__ int32_t s_pre[kQueryThreads / 32][kSlots + 1];
-  const GridParams g = *gpp;
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  int32_t* rb = s_beg[wib];
-  int32_t* rp = s_pre[wib];
-  const double kc = kernel_scale_build<KF>(kp);
-  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t w = warp0; w < nq; w += nwarps) {
-    double q[D];
-#pragma unroll
-    for (int t = 0; t < D; ++t) q[t] = Qs[w * D + t];
-    const int64_t orow = qout != nullptr ? qout[w] : w;  // unsorted small batches: identity
+// Warp-cooperative exact 1-NN of q (argmin over (key, index), the reference's
+// std::min over pairs, nn_index.cpp:351-366): the distance-ordered cell walk
+// of grid_query_kernel (the 3^D block first, then chunks of up to 32 cells
+// skipped by their box bound, then Chebyshev rings), candidates 32 at a time.
+template <int D>
+__device__ __forceinline__ Cand warp_nn_walk(const GridParams& g, const double* __restrict__ pts,
+                                             const int32_t* __restrict__ pid, const int32_t* __restrict__ cstart,
+                                             const double (&q)[D], int32_t* rb, int32_t* rp, int lane) {
     int c[3];
     cell_key<D>(q, g, c);
     Cand best{INFINITY, INT_MAX};
-
     // argmin over up to 64 ranges (two per lane), then over the warp
     auto scan_ranges = [&](int32_t b0, int32_t l0, int32_t b1, int32_t l1) {
       int32_t incl = l0 + l1;
@@ -1028,62 +1002,183 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
       if (lb2 == INFINITY) break;
       if (best.d < lb2) break;
     }
-    const int64_t j = best.i;
-    if (j == INT_MAX) {  // no candidate ranked (non-finite or overflowing z): nn -1, NaN means, no gather
-      if (nn_out != nullptr && lane == 0) nn_out[orow] = -1;
-      if (S != nullptr)
-        for (int cc = lane; cc < m; cc += kWarp) out[orow * m + cc] = __longlong_as_double(0x7ff8000000000000ll);
-      continue;
+    return best;
+}
+
+// Fused predict for d <= 3 (fast_predict_one, fast_predict.cpp:132-144).
+// Each warp takes 32 consecutive (cell-sorted) test points.
+// 1-NN, one lane per test point: the lane scans the 3^D block of cells
+// around its point (cells of ~1.5 points in 2-D, ~1 in 3-D; a block row of
+// cells is one contiguous range of the cell-ordered points) and keeps the
+// (key, index) minimum; the answer is final when it is below the bound on
+// every point outside the block (outside_lb_sq, conservative by the grid
+// margin). Lanes whose block does not certify (empty neighbourhood, a test
+// point outside the training box) are finished by the warp-cooperative walk.
+// Gather-kernel-dot, one test point at a time over the warp: lanes t and
+// t + 32 take neighbours t, t + 32 of the 1-NN's row (S, C coalesced, X
+// gathered), evaluate the cross-covariances (kernel_from_sq_build, KF =
+// kernel kind) and reduce the dot by a shuffle tree; the S/C row of the next
+// test point and the X rows of the current one are loaded one step ahead, so
+// the dependent 1-NN -> S -> X chain overlaps the arithmetic. The sum order
+// differs from the reference's sequential loop by rounding only (tolerance
+// 1e-9, tested). FMGP_PGRID_WARP=1 selects the warp walk for every point
+// (A/B).
+template <int D, int KF, bool kThreadNN>
+__global__ void __launch_bounds__(kQueryThreads, FMGP_GP_MINB)
+grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict__ pts, const int32_t* __restrict__ pid,
+                    const int32_t* __restrict__ cstart, int64_t nq, const double* __restrict__ Qs,
+                    const int32_t* __restrict__ qout, const double* __restrict__ X, const int32_t* __restrict__ S,
+                    const double* __restrict__ Cf, int k, int m, KParams kp, const double* __restrict__ mean_offset,
+                    double* __restrict__ out, int32_t* __restrict__ nn_out) {
+  __shared__ int32_t s_beg[kQueryThreads / 32][kSlots];
+  __shared__ int32_t s_pre[kQueryThreads / 32][kSlots + 1];
+  const GridParams g = *gpp;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int32_t* rb = s_beg[wib];
+  int32_t* rp = s_pre[wib];
+  const double kc = kernel_scale_build<KF>(kp);
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool fast = m == 1 && k <= 2 * kWarp && S != nullptr;
+  for (int64_t w0 = warp0 * kWarp; w0 < nq; w0 += nwarps * kWarp) {
+    const int nv = nq - w0 < kWarp ? static_cast<int>(nq - w0) : kWarp;
+    const bool has = lane < nv;
+    double q[D];
+#pragma unroll
+    for (int t = 0; t < D; ++t) q[t] = has ? Qs[(w0 + lane) * D + t] : 0.0;
+    const int64_t orow = !has ? 0 : (qout != nullptr ? qout[w0 + lane] : w0 + lane);
+    Cand best{INFINITY, INT_MAX};
+    bool certified = !has;
+    if constexpr (kThreadNN) {
+      if (has) {
+        int c[3];
+        cell_key<D>(q, g, c);
+        const int x0 = max(c[0] - 1, 0), x1 = min(c[0] + 1, g.G[0] - 1);
+        const int y0 = D >= 2 ? max(c[1] - 1, 0) : 0, y1 = D >= 2 ? min(c[1] + 1, g.G[1] - 1) : 0;
+        const int z0 = D >= 3 ? max(c[2] - 1, 0) : 0, z1 = D >= 3 ? min(c[2] + 1, g.G[2] - 1) : 0;
+        for (int z = z0; z <= z1; ++z) {
+          for (int y = y0; y <= y1; ++y) {
+            const int64_t rowkey = (static_cast<int64_t>(z) * g.G[1] + y) * g.G[0];
+            const int32_t pb = __ldg(&cstart[rowkey + x0]), pe = __ldg(&cstart[rowkey + x1 + 1]);
+            for (int32_t p = pb; p < pe; ++p) {
+              double x[D];
+#pragma unroll
+              for (int t = 0; t < D; ++t) x[t] = __ldg(&pts[static_cast<int64_t>(p) * D + t]);
+              const Cand cd{dist_sq_fixed<D>(q, x), __ldg(&pid[p])};
+              if (cless(cd, best)) best = cd;
+            }
+          }
+        }
+        const double lb2 = outside_lb_sq<D>(g, q, c, 1);
+        certified = best.d < INFINITY && (lb2 == INFINITY || best.d < lb2);
+      }
     }
-    if (nn_out != nullptr && lane == 0) nn_out[orow] = static_cast<int32_t>(j);
+    unsigned need = __ballot_sync(0xffffffffu, !certified);
+    while (need != 0) {
+      const int src = __ffs(need) - 1;
+      need &= need - 1;
+      double qq[D];
+#pragma unroll
+      for (int t = 0; t < D; ++t) qq[t] = __shfl_sync(0xffffffffu, q[t], src);
+      const Cand r = warp_nn_walk<D>(g, pts, pid, cstart, qq, rb, rp, lane);
+      if (lane == src) best = r;
+    }
+    const bool found = best.i != INT_MAX;
+    if (has && nn_out != nullptr) nn_out[orow] = found ? best.i : -1;
     if (S == nullptr) continue;  // nearest-only walk (NeighborIndex::nearest_training_point)
-    if (m == 1 && k <= 2 * kWarp) {
-      // the common shape: both 32-neighbour rounds' loads (S, C, then the X
-      // gathers) are issued before any arithmetic, so the dependent gather
-      // chain is paid once per test point, not once per round
+    if (has && !found)  // no candidate ranked (non-finite or overflowing z): NaN means, no gather
+      for (int cc = 0; cc < m; ++cc) out[orow * m + cc] = __longlong_as_double(0x7ff8000000000000ll);
+    if (fast) {
       const int t0 = lane, t1 = lane + kWarp;
       const bool h0 = t0 < k, h1 = t1 < k;
-      const int64_t nb0 = h0 ? S[j * k + t0] : 0, nb1 = h1 ? S[j * k + t1] : 0;
-      const double c0 = h0 ? Cf[j * k + t0] : 0.0, c1 = h1 ? Cf[j * k + t1] : 0.0;
-      double x0[D], x1[D];
+      const double mo = mean_offset[0];
+      // stage loads of point i: its S/C row (needs j_i) and, one step later, its X rows (need S)
+      auto load_sc = [&](int i, int64_t& nb0, int64_t& nb1, double& c0, double& c1) {
+        const int32_t jj = __shfl_sync(0xffffffffu, best.i, i);
+        const bool ok = i < nv && jj != INT_MAX;
+        const int64_t j = ok ? jj : 0;
+        nb0 = ok && h0 ? __ldg(&S[j * k + t0]) : 0;
+        nb1 = ok && h1 ? __ldg(&S[j * k + t1]) : 0;
+        c0 = ok && h0 ? __ldg(&Cf[j * k + t0]) : 0.0;
+        c1 = ok && h1 ? __ldg(&Cf[j * k + t1]) : 0.0;
+      };
+      auto load_x = [&](int64_t nb0, int64_t nb1, double (&x0)[D], double (&x1)[D]) {
 #pragma unroll
-      for (int u = 0; u < D; ++u) {
-        x0[u] = X[nb0 * D + u];
-        x1[u] = X[nb1 * D + u];
-      }
-      double dq0 = q[0] - x0[0], dq1 = q[0] - x1[0];
-      double s0 = dq0 * dq0, s1 = dq1 * dq1;
+        for (int u = 0; u < D; ++u) {
+          x0[u] = __ldg(&X[nb0 * D + u]);
+          x1[u] = __ldg(&X[nb1 * D + u]);
+        }
+      };
+      int64_t nbA0, nbA1;
+      double cA0, cA1, xA0[D], xA1[D];
+      load_sc(0, nbA0, nbA1, cA0, cA1);
+      load_x(nbA0, nbA1, xA0, xA1);
+      int64_t nbB0, nbB1;
+      double cB0, cB1;
+      load_sc(1, nbB0, nbB1, cB0, cB1);
+      for (int i = 0; i < nv; ++i) {
+        // prefetch: X rows of point i + 1, S/C of point i + 2
+        double xB0[D], xB1[D];
+        load_x(nbB0, nbB1, xB0, xB1);
+        int64_t nbC0, nbC1;
+        double cC0, cC1;
+        load_sc(i + 2, nbC0, nbC1, cC0, cC1);
+        double qi[D];
 #pragma unroll
-      for (int u = 1; u < D; ++u) {
-        dq0 = q[u] - x0[u];
-        dq1 = q[u] - x1[u];
-        s0 = fma(dq0, dq0, s0);
-        s1 = fma(dq1, dq1, s1);
-      }
-      double acc = h0 ? kernel_from_sq_build<KF>(s0, kc, kp) * c0 : 0.0;
-      if (h1) acc = fma(kernel_from_sq_build<KF>(s1, kc, kp), c1, acc);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) out[orow] = acc + mean_offset[0];
-      continue;
-    }
-    for (int cc = 0; cc < m; ++cc) {
-      double acc = 0.0;
-      for (int t = lane; t < k; t += kWarp) {
-        const int64_t nb = S[j * k + t];
-        const double* xn = X + nb * D;
-        const double d0 = q[0] - xn[0];
-        double dsq = d0 * d0;
+        for (int u = 0; u < D; ++u) qi[u] = __shfl_sync(0xffffffffu, q[u], i);
+        const bool ok = __shfl_sync(0xffffffffu, best.i, i) != INT_MAX;
+        double dq0 = qi[0] - xA0[0], dq1 = qi[0] - xA1[0];
+        double s0 = dq0 * dq0, s1 = dq1 * dq1;
 #pragma unroll
         for (int u = 1; u < D; ++u) {
-          const double du = q[u] - xn[u];
-          dsq = fma(du, du, dsq);
+          dq0 = qi[u] - xA0[u];
+          dq1 = qi[u] - xA1[u];
+          s0 = fma(dq0, dq0, s0);
+          s1 = fma(dq1, dq1, s1);
         }
-        acc = fma(kernel_from_sq_build<KF>(dsq, kc, kp), Cf[(j * k + t) * m + cc], acc);
-      }
+        double acc = h0 ? kernel_from_sq_build<KF>(s0, kc, kp) * cA0 : 0.0;
+        if (h1) acc = fma(kernel_from_sq_build<KF>(s1, kc, kp), cA1, acc);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) out[orow * m + cc] = acc + mean_offset[cc];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const int64_t orow_i = __shfl_sync(0xffffffffu, orow, i);
+        if (lane == 0 && ok) out[orow_i] = acc + mo;
+        nbA0 = nbB0; nbA1 = nbB1; cA0 = cB0; cA1 = cB1;
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+          xA0[u] = xB0[u];
+          xA1[u] = xB1[u];
+        }
+        nbB0 = nbC0; nbB1 = nbC1; cB0 = cC0; cB1 = cC1;
+      }
+      continue;
+    }
+    for (int i = 0; i < nv; ++i) {
+      const int32_t jj = __shfl_sync(0xffffffffu, best.i, i);
+      const int64_t orow_i = __shfl_sync(0xffffffffu, orow, i);
+      if (jj == INT_MAX) continue;
+      const int64_t j = jj;
+      double qi[D];
+#pragma unroll
+      for (int u = 0; u < D; ++u) qi[u] = __shfl_sync(0xffffffffu, q[u], i);
+      for (int cc = 0; cc < m; ++cc) {
+        double acc = 0.0;
+        for (int t = lane; t < k; t += kWarp) {
+          const int64_t nb = S[j * k + t];
+          const double* xn = X + nb * D;
+          const double d0 = qi[0] - xn[0];
+          double dsq = d0 * d0;
+#pragma unroll
+          for (int u = 1; u < D; ++u) {
+            const double du = qi[u] - xn[u];
+            dsq = fma(du, du, dsq);
+          }
+          acc = fma(kernel_from_sq_build<KF>(dsq, kc, kp), Cf[(j * k + t) * m + cc], acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[orow_i * m + cc] = acc + mean_offset[cc];
+      }
     }
   }
 }
@@ -1350,15 +1445,23 @@ cudaError_t run_predict_grid(const PredictGridCache& g, const double* X, const i
     Qs = qb.pts;
     qo = qb.pid;
   }
-  int64_t blocks = (nz * 32 + kQueryThreads - 1) / kQueryThreads;
+  int64_t blocks = (nz + kQueryThreads - 1) / kQueryThreads;  // 32 test points per warp
   const int64_t cap = static_cast<int64_t>(num_sms) * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
+  static const bool warp_nn = [] {  // FMGP_PGRID_WARP=1: warp-cooperative 1-NN walk for every point (A/B)
+    const char* e = std::getenv("FMGP_PGRID_WARP");
+    return e != nullptr && e[0] == '1';
+  }();
   switch (kp.kind == 1 ? 0 : 1 + kp.nu_code) {  // kernel_code(), evaluated on the host
 #define FMGP_PRED_CASE(KF)                                                                                      \
   case KF:                                                                                                      \
-    grid_predict_kernel<D, KF><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                         \
-        g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out);     \
+    if (warp_nn)                                                                                                \
+      grid_predict_kernel<D, KF, false><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                \
+          g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out);   \
+    else                                                                                                        \
+      grid_predict_kernel<D, KF, true><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                 \
+          g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out);   \
     break;
     FMGP_PRED_CASE(0)
     FMGP_PRED_CASE(1)
