@@ -111,6 +111,13 @@ cudaError_t fused_solve_cta(const double* X, const double* Y, int d, int m, cons
                             int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
                             int num_sms, cudaStream_t stream);
 
+// 2-D cyclic right-looking variant for the small-d shapes (d in {2, 3},
+// k in {30, 50}, m = 1, closed-form kernels); FMGP_SOLVE_2D=0 turns it off.
+bool fused_solve_2d_supported(int k, int d, int m, const KParams& kp);
+cudaError_t fused_solve_2d(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows,
+                           int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
+                           int num_sms, cudaStream_t stream);
+
 // Register-resident-row variant of fused_solve for compile-time shapes.
 bool fused_solve_reg_supported(int k, int d, int m);
 cudaError_t fused_solve_reg(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,

@@ -383,6 +383,8 @@ cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const in
     const std::string v(e);
     return v == "tc" ? 1 : (v == "scalar" ? 2 : 0);
   }();
+  if (mode == 0 && status == nullptr && fused_solve_2d_supported(k, d, m, kp))
+    return fused_solve_2d(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
   if (mode == 0 && status == nullptr && fused_solve_reg_supported(k, d, m))
     return fused_solve_reg(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
   if (mode == 0 && status == nullptr && fused_solve_cta_supported(k, d, m))
