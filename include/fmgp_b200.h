@@ -160,6 +160,39 @@ int fmgp_index_distances(const fmgp_index* index, const double* q, const int32_t
                          double* out);
 void fmgp_index_destroy(fmgp_index* index);
 
+/* ---- ApproxGraph index (IndexMode::ApproxGraph; nn_index.cpp:83-237, :288-341,
+ * :351-366, :397-470) ------------------------------------------------------
+ * A navigable-small-world graph over an index's points (the index must
+ * outlive it). fmgp_graph_build: levels from the reference's seeded
+ * generator (splitmix64 of seed ^ 0xa02bdbf7bb3c0a7, floor(-ln u / ln M)),
+ * so layer sizes, maximum level and entry point are the reference's; each
+ * layer links every node to its 2M (layer 0) / M (above) exact nearest
+ * neighbours among the layer's nodes (one batched exact search per layer, in
+ * place of the reference's sequential insertion; build_beam is recorded).
+ * fmgp_graph_load: a serialized graph (the reference's blob after its mode
+ * tag, parsed by the caller: levels[n]; counts[] node-major, layer 0 first;
+ * ids[] concatenated). fmgp_graph_info / fmgp_graph_export give the same
+ * arrays back for serialize(). Queries run the reference's search (greedy
+ * descent on the upper layers, best-first beam search on layer 0 with beam
+ * query_beam or max(64, 2k), nearest: query_beam or 64) one warp per query,
+ * with the exact scan for any query that returns fewer than k results;
+ * dist_evals (nullable) accumulates the distance evaluations, as the
+ * reference's counter does. */
+typedef struct fmgp_graph fmgp_graph;
+int fmgp_graph_build(const fmgp_index* index, int32_t max_degree, int32_t build_beam, int32_t query_beam,
+                     uint64_t seed, fmgp_graph** out);
+int fmgp_graph_load(const fmgp_index* index, int32_t max_degree, int32_t build_beam, int32_t query_beam,
+                    uint64_t seed, int32_t entry, int32_t max_level, const int32_t* levels,
+                    const uint32_t* counts, const int32_t* ids, fmgp_graph** out);
+int fmgp_graph_info(const fmgp_graph* graph, int32_t* entry, int32_t* max_level, int64_t* counts_total,
+                    int64_t* ids_total);
+int fmgp_graph_export(const fmgp_graph* graph, int32_t* levels, uint32_t* counts, int32_t* ids);
+int fmgp_graph_query_knn(const fmgp_graph* graph, const double* Q, int64_t nq, int32_t k,
+                         const int32_t* exclude, int32_t* idx_out, double* dist_out, uint64_t* dist_evals);
+int fmgp_graph_nearest(const fmgp_graph* graph, const double* Q, int64_t nq, int32_t* idx_out,
+                       uint64_t* dist_evals);
+void fmgp_graph_destroy(fmgp_graph* graph);
+
 /* ---- predict (fast_predict.cpp:132-156) -----------------------------------
  * out[t*m + c] = sum_s kernel(||z_t - x_{S[j,s]}||) C[j,s,c] + mean_offset[c],
  * j = nearest training point of z_t (nn_out, nullable, receives j). */

@@ -11,7 +11,7 @@ from __future__ import annotations
 import importlib
 
 _API = {
-    "KernelKind", "KernelParams", "FittedParams", "TrainingSet", "detrend", "IndexMode", "NeighborIndex",
+    "KernelKind", "KernelParams", "FittedParams", "TrainingSet", "detrend", "IndexMode", "GraphParams", "NeighborIndex",
     "NeighborList", "PrecomputedModel", "precompute", "fast_predict_one", "fast_predict_batch",
     "kernel_value", "kernel_values", "matern_value", "rbf_value", "cov_matrix", "cov_matrix_self",
     "solve_spd", "solve_spd_batched", "precompute_device", "predict_device", "DomainError", "NumericError",

@@ -58,6 +58,14 @@ SIGNATURES: dict[str, tuple] = {
     "fmgp_index_nearest": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
     "fmgp_index_distances": (C.c_int, [_vp, _vp, _vp, C.c_int64, _vp]),
     "fmgp_index_destroy": (None, [_vp]),
+    "fmgp_graph_build": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.POINTER(_vp)]),
+    "fmgp_graph_load": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int32, _vp,
+                                  _vp, _vp, C.POINTER(_vp)]),
+    "fmgp_graph_info": (C.c_int, [_vp, _i32, _i32, _i64, _i64]),
+    "fmgp_graph_export": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "fmgp_graph_query_knn": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp, _vp, _vp, C.POINTER(C.c_uint64)]),
+    "fmgp_graph_nearest": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.POINTER(C.c_uint64)]),
+    "fmgp_graph_destroy": (None, [_vp]),
     "fmgp_predict": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _kp, _vp, _vp,
                                C.c_int64, _vp, _vp]),
     "fmgp_predict_device": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _kp, _vp, _vp,

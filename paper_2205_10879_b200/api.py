@@ -37,6 +37,15 @@ class IndexMode(enum.IntEnum):
 
 
 @dataclass(frozen=True)
+class GraphParams:
+    """nn_index.hpp:14-19 (query_beam <= 0: max(64, 2k) at query time)."""
+    max_degree: int = 16
+    build_beam: int = 100
+    query_beam: int = 0
+    seed: int = 0
+
+
+@dataclass(frozen=True)
 class KernelParams:
     """kernel.hpp:12-33; validated like kernel.cpp:13-28."""
     sigma: float
@@ -116,12 +125,30 @@ class NeighborList:
 
 
 class NeighborIndex:
-    """Exact neighbour index (nn_index.hpp:33-60) on the GPU. Immutable."""
+    """Neighbour index (nn_index.hpp:33-60) on the GPU. Immutable.
 
-    def __init__(self, points: np.ndarray, mode: IndexMode):
+    Exact: exact search (cell grid / tcgen05 / brute force). ApproxGraph: the
+    GPU navigable-small-world graph of graph.cu (fmgp_graph_build; the
+    reference's seeded levels, layers linked to their exact nearest
+    neighbours), searched with the reference's graph search; `dist_evals`
+    counts its distance evaluations (nn_index.hpp:39-44)."""
+
+    def __init__(self, points: np.ndarray, mode: IndexMode, params: GraphParams | None = None):
         self._pts = points
-        self._mode = mode
+        self._mode = IndexMode(mode)
+        self._params = params or GraphParams()
         self._dev = None  # device-resident copy + nearest-point grid (fmgp_index), made on first query
+        self.dist_evals = 0
+        if self._mode == IndexMode.ApproxGraph:
+            g = C.c_void_p()
+            p = self._params
+            N.check(N.LIB.fmgp_graph_build(self._handle(), p.max_degree, p.build_beam, p.query_beam,
+                                           C.c_uint64(p.seed), C.byref(g)))
+            self._dev.g = g.value
+
+    @property
+    def _graph_h(self):
+        return self._dev.g if self._dev is not None else None
 
     def _handle(self):
         if self._dev is None:
@@ -131,13 +158,49 @@ class NeighborIndex:
         return self._dev.h
 
     @staticmethod
-    def build(points, mode: IndexMode = IndexMode.Exact, params=None) -> "NeighborIndex":
+    def build(points, mode: IndexMode = IndexMode.Exact, params: GraphParams | None = None) -> "NeighborIndex":
+        p = params or GraphParams()
+        if p.max_degree < 2 or p.build_beam < 1:
+            raise DomainError(N.FMGP_EINVAL, "NeighborIndex: invalid graph parameters")
         P = _f64(points)
         if P.ndim != 2 or P.shape[0] < 1:
             raise DomainError(N.FMGP_EINVAL, "NeighborIndex: empty point set")
         if not np.all(np.isfinite(P)):
             raise DomainError(N.FMGP_EINVAL, "NeighborIndex: non-finite coordinates")
-        return NeighborIndex(P, mode)
+        return NeighborIndex(P, mode, p)
+
+    def params(self) -> GraphParams:
+        return self._params
+
+    def graph_arrays(self):
+        """ApproxGraph: (entry, max_level, levels, counts, ids) in the reference's
+        serialization order (nn_index.cpp:397-416)."""
+        if self._graph_h is None:
+            raise DomainError(N.FMGP_EINVAL, "not an ApproxGraph index")
+        entry, ml = C.c_int32(), C.c_int32()
+        ct, it = C.c_int64(), C.c_int64()
+        N.check(N.LIB.fmgp_graph_info(self._graph_h, C.byref(entry), C.byref(ml), C.byref(ct), C.byref(it)))
+        levels = np.empty(self.size(), dtype=np.int32)
+        counts = np.empty(ct.value, dtype=np.uint32)
+        ids = np.empty(max(it.value, 1), dtype=np.int32)
+        N.check(N.LIB.fmgp_graph_export(self._graph_h, _ptr(levels), _ptr(counts), _ptr(ids)))
+        return entry.value, ml.value, levels, counts, ids[:it.value]
+
+    @staticmethod
+    def from_graph_arrays(points, params: GraphParams, entry, max_level, levels, counts, ids) -> "NeighborIndex":
+        """A serialized graph (e.g. reference-written) over `points`."""
+        ix = NeighborIndex.build(points, IndexMode.Exact)
+        ix._mode = IndexMode.ApproxGraph
+        ix._params = params
+        lv = np.ascontiguousarray(levels, dtype=np.int32)
+        ct = np.ascontiguousarray(counts, dtype=np.uint32)
+        idv = np.ascontiguousarray(ids if len(ids) else [0], dtype=np.int32)
+        g = C.c_void_p()
+        N.check(N.LIB.fmgp_graph_load(ix._handle(), params.max_degree, params.build_beam, params.query_beam,
+                                      C.c_uint64(params.seed), int(entry), int(max_level), _ptr(lv), _ptr(ct),
+                                      _ptr(idv), C.byref(g)))
+        ix._dev.g = g.value
+        return ix
 
     def size(self) -> int:
         return self._pts.shape[0]
@@ -161,7 +224,14 @@ class NeighborIndex:
         idx = np.empty((nq, k), dtype=np.int32)
         dist = np.empty((nq, k), dtype=np.float64)
         ex = None if exclude is None else np.ascontiguousarray(exclude, dtype=np.int32)
+        if self._graph_h is not None:
+            ev = C.c_uint64(0)
+            N.check(N.LIB.fmgp_graph_query_knn(self._graph_h, _ptr(Q), nq, k, _ptr(ex), _ptr(idx), _ptr(dist),
+                                               C.byref(ev)))
+            self.dist_evals += ev.value
+            return idx, dist
         N.check(N.LIB.fmgp_index_query_knn(self._handle(), _ptr(Q), nq, k, _ptr(ex), _ptr(idx), _ptr(dist)))
+        self.dist_evals += nq * (self.size() - (0 if ex is None else int(np.count_nonzero(ex >= 0)) // max(nq, 1)))
         return idx, dist
 
     def query_knn(self, q, k: int, exclude_index: int = -1) -> NeighborList:
@@ -176,7 +246,13 @@ class NeighborIndex:
         if Q.ndim != 2 or Q.shape[1] != self.dim():
             raise DomainError(N.FMGP_EINVAL, "nearest_training_point: dimension mismatch")
         out = np.empty(Q.shape[0], dtype=np.int32)
+        if self._graph_h is not None:
+            ev = C.c_uint64(0)
+            N.check(N.LIB.fmgp_graph_nearest(self._graph_h, _ptr(Q), Q.shape[0], _ptr(out), C.byref(ev)))
+            self.dist_evals += ev.value
+            return out
         N.check(N.LIB.fmgp_index_nearest(self._handle(), _ptr(Q), Q.shape[0], _ptr(out)))
+        self.dist_evals += Q.shape[0] * self.size()
         return out
 
     def nearest_training_point(self, q) -> int:
@@ -223,10 +299,18 @@ class PrecomputedModel:
 
 
 class _IndexHandle:
+    """fmgp_index and, in ApproxGraph mode, its fmgp_graph: one owner, so the
+    graph is always destroyed before the points it searches (a garbage
+    collection of both in one cycle finalizes them in arbitrary order)."""
+
     def __init__(self, h):
         self.h = h
+        self.g = None
 
     def __del__(self):
+        if self.g:
+            N.LIB.fmgp_graph_destroy(self.g)
+            self.g = None
         if self.h:
             N.LIB.fmgp_index_destroy(self.h)
             self.h = None

@@ -1,9 +1,12 @@
 // Drop-in facade (B200): nearest-neighbour index of the FastMuyGPs API.
-// Public surface of proj/core/include/fastmuygps/nn_index.hpp. Queries are
-// exact and run on the GPU (cell grid for d <= 3, brute force otherwise)
-// against a device-resident copy of the points. IndexMode::ApproxGraph is
-// accepted for source compatibility but answered exactly (the exact answer is
-// what the HNSW graph approximates); GraphParams are validated and stored.
+// Public surface of proj/core/include/fastmuygps/nn_index.hpp. Exact-mode
+// queries run on the GPU (cell grid for d <= 3, tcgen05 filter / brute force
+// otherwise) against a device-resident copy of the points. ApproxGraph mode
+// builds a navigable-small-world graph on the GPU (fmgp_graph_build: the
+// reference's seeded levels, each layer linked to its exact nearest
+// neighbours) and answers query_knn / nearest_training_point with the
+// reference's graph search, one warp per query (fmgp_graph_query_knn); graphs
+// serialize in the reference's layout and reference-written graphs load.
 #pragma once
 
 #include <Eigen/Dense>
@@ -14,6 +17,7 @@
 #include <vector>
 
 struct fmgp_index;
+struct fmgp_graph;
 
 namespace fastmuygps {
 
@@ -38,8 +42,8 @@ class NeighborIndex {
   static NeighborIndex build(const Eigen::MatrixXd& points, IndexMode mode, const GraphParams& params = {});
 
   // k nearest stored points to q, excluding index exclude_index (>= 0) by
-  // identity. dist_evals (if given) is incremented by the exact-scan
-  // equivalent count.
+  // identity. dist_evals (if given) accumulates the distance evaluations
+  // (Exact: the scan's count; ApproxGraph: the graph search's).
   NeighborList query_knn(const Eigen::VectorXd& q, int k, int exclude_index = -1,
                          std::size_t* dist_evals = nullptr) const;
   // Nearest stored point; ties go to the lower index.
@@ -68,7 +72,7 @@ class NeighborIndex {
   GraphParams params_;
   std::vector<double> pts_;
   std::shared_ptr<fmgp_index> dev_;
-  std::string graph_blob_;  // a reference-written HNSW graph (after the mode tag), kept verbatim
+  std::shared_ptr<fmgp_graph> graph_;  // ApproxGraph mode: the device graph (keeps dev_ alive)
 };
 
 }  // namespace fastmuygps

@@ -183,13 +183,6 @@ static std::atomic<int64_t> g_launches{0};
 void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 }  // namespace fmgp
 
-struct fmgp_index {
-  int device = 0;
-  int64_t n = 0;
-  int32_t d = 0;
-  double* P = nullptr;
-  void* grid = nullptr;  // nearest-point walk grid of P (d <= 3), built once at create
-};
 
 // Host-buffer precompute of rows [row_begin, row_end) (X, Y full; S_out and
 // C_out hold the shard's rows). K1 for the shard, then K2 in row chunks; a

@@ -35,6 +35,17 @@ struct fmgp_model {
   std::vector<fmgp_model_replica> reps;
 };
 
+// The device-resident point set of NeighborIndex (fmgp_index_create): a
+// row-major device copy of the points; the ApproxGraph index (graph.cu)
+// searches over it.
+struct fmgp_index {
+  int device = 0;
+  int64_t n = 0;
+  int32_t d = 0;
+  double* P = nullptr;
+  void* grid = nullptr;  // nearest-point walk grid of P (d <= 3), built once at create
+};
+
 namespace fmgp_capi {
 
 // Finish a replica whose X/S/C are set on the current device: mean offsets

@@ -312,7 +312,7 @@ __device__ __forceinline__ double rsqrt_pivot(double x) {
 // by the 1.5*2^52 shift (m is the low word of the shifted value) and
 // 2^-(m>>6) applied as an exponent-field subtraction on the table value
 // (a <= 708 keeps the result normal). Within 2 ulp of exp(-a).
-__device__ __forceinline__ double exp_neg_build(double a) {
+__device__ __forceinline__ double exp_neg_build(double a, const double* tab = kExp2NegTab) {
   // a >= 0: clamp at 708 (0x40862000'00000000) by the high word, an integer
   // compare + two selects (a double compare compiles to fmin with NaN fix-ups);
   // NaN (an overflowed distance) also maps to the clamp
@@ -327,9 +327,14 @@ __device__ __forceinline__ double exp_neg_build(double a) {
   q = fma(q, r, 0.5);
   q = fma(q, r, 1.0);
   q = fma(q, r, 1.0);
-  const double tj = __ldg(&kExp2NegTab[m & 63]);
+  const double tj = tab[m & 63];
   const double sj = __hiloint2double(__double2hiint(tj) - ((m >> 6) << 20), __double2loint(tj));
   return sj * q;
+}
+
+// Copy of the exp table into shared memory (call with every thread of the CTA, then __syncthreads).
+__device__ __forceinline__ void stage_exp_table(double* dst) {
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) dst[i] = kExp2NegTab[i];
 }
 
 // Kernel value from the squared distance on the register-solve build path
@@ -339,20 +344,24 @@ __device__ __forceinline__ double exp_neg_build(double a) {
 // register demand does not set the register budget of the solve kernels.
 static __device__ __noinline__ double kernel_eval_general(double dist, const KParams& p);
 
+// `tab`: the 2^(-j/64) table of exp_neg_build; the fused solves pass a copy
+// in shared memory (the global table's divergent lookups were ~90% of the
+// solve's L1 sector traffic, profiles/r02/ncu_solve_cfg5_full.txt).
 template <int KF>
-__device__ __forceinline__ double kernel_from_sq_build(double acc, double c, const KParams& p) {
+__device__ __forceinline__ double kernel_from_sq_build(double acc, double c, const KParams& p,
+                                                       const double* tab = kExp2NegTab) {
   double v;
   if constexpr (KF == 0) {
-    v = p.s2 * exp_neg_build(acc * c);
+    v = p.s2 * exp_neg_build(acc * c, tab);
   } else if constexpr (KF == 1) {
-    v = p.s2 * exp_neg_build(sqrt_build(acc) * c);
+    v = p.s2 * exp_neg_build(sqrt_build(acc) * c, tab);
   } else if constexpr (KF == 2) {
     const double a = sqrt_build(acc) * c;
-    const double e = exp_neg_build(a);
+    const double e = exp_neg_build(a, tab);
     v = p.s2 * fma(a, e, e);
   } else if constexpr (KF == 3) {
     const double a = sqrt_build(acc) * c;
-    v = p.s2 * (fma(a, a * (1.0 / 3.0), 1.0 + a) * exp_neg_build(a));
+    v = p.s2 * (fma(a, a * (1.0 / 3.0), 1.0 + a) * exp_neg_build(a, tab));
   } else {
     v = kernel_eval_general(sqrt(acc), p);
   }

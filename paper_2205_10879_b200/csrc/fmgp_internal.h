@@ -64,6 +64,8 @@ cudaError_t predict_grid_cached(const void* cache, const double* X, const int32_
                                 const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz,
                                 double* out, int32_t* nn_out, int num_sms, cudaStream_t stream);
 bool knn_grid_supported(int d, int kk);
+// Rows [0, n) of P (d <= 3) in a cell order (a processing order for the fused solve).
+cudaError_t spatial_row_order(const double* P, int64_t n, int d, int32_t* order, cudaStream_t stream);
 cudaError_t knn_grid(const double* Q, int64_t nq, const double* P, int64_t np, int d, int kk, int64_t self_offset,
                      const int32_t* excl_arr, int with_self, int32_t* out, double* out_d, int num_sms,
                      cudaStream_t stream);
@@ -116,13 +118,13 @@ cudaError_t fused_solve_cta(const double* X, const double* Y, int d, int m, cons
 bool fused_solve_2d_supported(int k, int d, int m, const KParams& kp);
 cudaError_t fused_solve_2d(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows,
                            int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
-                           int num_sms, cudaStream_t stream);
+                           int num_sms, cudaStream_t stream, const int32_t* order = nullptr);
 
 // Register-resident-row variant of fused_solve for compile-time shapes.
 bool fused_solve_reg_supported(int k, int d, int m);
 cudaError_t fused_solve_reg(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
                             int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
-                            int num_sms, cudaStream_t stream);
+                            int num_sms, cudaStream_t stream, const int32_t* order = nullptr);
 
 }  // namespace fmgp
 

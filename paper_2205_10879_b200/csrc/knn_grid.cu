@@ -1032,6 +1032,9 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
                     double* __restrict__ out, int32_t* __restrict__ nn_out) {
   __shared__ int32_t s_beg[kQueryThreads / 32][kSlots];
   __shared__ int32_t s_pre[kQueryThreads / 32][kSlots + 1];
+  __shared__ double s_exp[64];
+  stage_exp_table(s_exp);
+  __syncthreads();
   const GridParams g = *gpp;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -1137,8 +1140,8 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
           s0 = fma(dq0, dq0, s0);
           s1 = fma(dq1, dq1, s1);
         }
-        double acc = h0 ? kernel_from_sq_build<KF>(s0, kc, kp) * cA0 : 0.0;
-        if (h1) acc = fma(kernel_from_sq_build<KF>(s1, kc, kp), cA1, acc);
+        double acc = h0 ? kernel_from_sq_build<KF>(s0, kc, kp, s_exp) * cA0 : 0.0;
+        if (h1) acc = fma(kernel_from_sq_build<KF>(s1, kc, kp, s_exp), cA1, acc);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         const int64_t orow_i = __shfl_sync(0xffffffffu, orow, i);
@@ -1173,7 +1176,7 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
             const double du = qi[u] - xn[u];
             dsq = fma(du, du, dsq);
           }
-          acc = fma(kernel_from_sq_build<KF>(dsq, kc, kp), Cf[(j * k + t) * m + cc], acc);
+          acc = fma(kernel_from_sq_build<KF>(dsq, kc, kp, s_exp), Cf[(j * k + t) * m + cc], acc);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1536,6 +1539,64 @@ cudaError_t predict_grid_cached(const void* cache, const double* X, const int32_
     case 1: return run_predict_grid<1>(*g, X, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
     case 2: return run_predict_grid<2>(*g, X, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
     default: return run_predict_grid<3>(*g, X, S, Cf, k, m, kp, mean_offset_dev, Z, nz, out, nn_out, num_sms, stream);
+  }
+}
+
+// Processing order of the fused solve (d <= 3): the rows [0, n) of P sorted by
+// a coarse cell grid (~16 points per cell, counting sort), so the warps in
+// flight work on spatially close neighbourhoods and their coordinate gathers
+// hit L2 instead of HBM. Any permutation gives the same per-row results.
+namespace {
+__global__ void order_scatter_kernel(int64_t n, const int32_t* __restrict__ key, const int32_t* __restrict__ slot,
+                                     const int32_t* __restrict__ start, int32_t* __restrict__ order) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    order[start[key[i]] + slot[i]] = static_cast<int32_t>(i);
+}
+
+template <int D>
+cudaError_t spatial_order_d(const double* P, int64_t n, int32_t* order, cudaStream_t s) {
+  const int64_t ncap = n / 16 + 1;
+  GridParams* gp = nullptr;
+  unsigned long long* mm = nullptr;
+  SortBufs b;
+  b.nb = (ncap + 1 + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems);
+  cudaError_t e = cudaMallocAsync(&gp, sizeof(GridParams), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&mm, sizeof(unsigned long long) * 6, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&b.counts, sizeof(int32_t) * (ncap + 1), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&b.cstart, sizeof(int32_t) * (ncap + 2), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&b.bsums, sizeof(int32_t) * (b.nb + 1), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&b.key, sizeof(int32_t) * n, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&b.slot, sizeof(int32_t) * n, s);
+  if (e == cudaSuccess) {
+    cudaMemsetAsync(mm, 0, sizeof(unsigned long long) * 6, s);
+    for (int t = 0; t < D; ++t) cudaMemsetAsync(mm + 2 * t, 0xFF, sizeof(unsigned long long), s);
+    bbox_kernel<<<grid1d(n), 256, 0, s>>>(P, n, D, mm);
+    grid_params_kernel<<<1, 1, 0, s>>>(mm, n, D, 16.0, ncap, gp);
+    cudaMemsetAsync(b.counts, 0, sizeof(int32_t) * (ncap + 1), s);
+    count_kernel<D><<<grid1d(n), 256, 0, s>>>(P, n, gp, b.counts, b.key, b.slot);
+    const int64_t m = ncap + 1;
+    scan_local_kernel<<<static_cast<unsigned>(b.nb), kScanBlock, 0, s>>>(b.counts, m, b.cstart, b.bsums);
+    scan_sums_kernel<<<1, kScanBlock, 0, s>>>(b.bsums, b.nb, b.bsums + b.nb);
+    scan_add_kernel<<<static_cast<unsigned>(b.nb), kScanBlock, 0, s>>>(b.cstart, m, b.bsums);
+    order_scatter_kernel<<<grid1d(n), 256, 0, s>>>(n, b.key, b.slot, b.cstart, order);
+    note_launches(7);
+    e = cudaGetLastError();
+  }
+  if (gp) cudaFreeAsync(gp, s);
+  if (mm) cudaFreeAsync(mm, s);
+  b.release(s);
+  return e;
+}
+}  // namespace
+
+cudaError_t spatial_row_order(const double* P, int64_t n, int d, int32_t* order, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  switch (d) {
+    case 1: return spatial_order_d<1>(P, n, order, stream);
+    case 2: return spatial_order_d<2>(P, n, order, stream);
+    case 3: return spatial_order_d<3>(P, n, order, stream);
+    default: return cudaErrorInvalidValue;
   }
 }
 

@@ -372,6 +372,8 @@ size_t solve_smem_per_warp(int k, int d, int m, int* ld, int* dchunk) {
   return per_warp_doubles(k, *dchunk, m) * sizeof(double);
 }
 
+constexpr int64_t kOrderMinRows = 1 << 16;  // below this the batch is L2-resident anyway
+
 cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
                         int64_t row_begin, int k, const KParams& kp, double* C, int32_t* status,
                         unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
@@ -383,10 +385,30 @@ cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const in
     const std::string v(e);
     return v == "tc" ? 1 : (v == "scalar" ? 2 : 0);
   }();
-  if (mode == 0 && status == nullptr && fused_solve_2d_supported(k, d, m, kp))
-    return fused_solve_2d(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
-  if (mode == 0 && status == nullptr && fused_solve_reg_supported(k, d, m))
-    return fused_solve_reg(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
+  if (mode == 0 && status == nullptr && (fused_solve_2d_supported(k, d, m, kp) || fused_solve_reg_supported(k, d, m))) {
+    // Large low-d batches are solved in a cell order of their rows (FMGP_SOLVE_ORDER=0: index order):
+    // warps in flight then gather overlapping neighbourhoods, so X stays in L2.
+    static const bool use_order = [] {
+      const char* e = std::getenv("FMGP_SOLVE_ORDER");
+      return !(e != nullptr && e[0] == '0');
+    }();
+    int32_t* order = nullptr;
+    if (use_order && d <= 3 && nrows >= kOrderMinRows) {
+      cudaError_t e = cudaMallocAsync(&order, sizeof(int32_t) * nrows, stream);
+      if (e != cudaSuccess) return e;
+      e = spatial_row_order(X + row_begin * d, nrows, d, order, stream);
+      if (e != cudaSuccess) {
+        cudaFreeAsync(order, stream);
+        return e;
+      }
+    }
+    const cudaError_t e = fused_solve_2d_supported(k, d, m, kp)
+                              ? fused_solve_2d(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order)
+                              : fused_solve_reg(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream,
+                                                order);
+    if (order != nullptr) cudaFreeAsync(order, stream);
+    return e;
+  }
   if (mode == 0 && status == nullptr && fused_solve_cta_supported(k, d, m))
     return fused_solve_cta(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream);
   if (mode == 1 && status == nullptr && fused_solve_tc_supported(k, d, m))

@@ -102,7 +102,7 @@ template <int K, int D, int KF>
 __global__ void __launch_bounds__(128, (K > 32 ? FMGP_S2D_MINB : 4))
 solve2d_kernel(const double* __restrict__ X, const double* __restrict__ Y, const int32_t* __restrict__ S,
                int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
-               unsigned long long* __restrict__ fail_min) {
+               unsigned long long* __restrict__ fail_min, const int32_t* __restrict__ order) {
   using G = G2<K>;
   constexpr int NI = G::NI, NK = G::NK;
   extern __shared__ double smem[];
@@ -116,6 +116,9 @@ solve2d_kernel(const double* __restrict__ X, const double* __restrict__ Y, const
   double* ys = area + 4 * K;
   const int a = lane & 3, b = lane >> 2;
   const double cs = kernel_scale_build<KF>(kp);
+  __shared__ double s_exp[64];
+  stage_exp_table(s_exp);
+  __syncthreads();
 
   // backward-solve geometry of the lane's two x entries (j0 = lane, j1 = lane + 32)
   const int j0 = lane, j1 = lane + kWarp;
@@ -126,8 +129,9 @@ solve2d_kernel(const double* __restrict__ X, const double* __restrict__ Y, const
   }
   const int st0 = G::st(j0), ln0 = G::len(j0), st1 = G::st(j1), ln1 = G::len(j1);
 
-  for (int64_t r = static_cast<int64_t>(blockIdx.x) * warps + warp; r < nrows;
-       r += static_cast<int64_t>(gridDim.x) * warps) {
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * warps + warp; it < nrows;
+       it += static_cast<int64_t>(gridDim.x) * warps) {
+    const int64_t r = order != nullptr ? order[it] : it;
     for (int t = lane; t < K; t += kWarp) sr[t] = S[r * K + t];
     __syncwarp();
     bool ok = false;
@@ -158,7 +162,7 @@ solve2d_kernel(const double* __restrict__ X, const double* __restrict__ Y, const
             const double dd = xi[c] - xk[c];
             acc = fma(dd, dd, acc);
           }
-          double v = kernel_from_sq_build<KF>(acc, cs, kp);
+          double v = kernel_from_sq_build<KF>(acc, cs, kp, s_exp);
           v = i == k ? dg : v;
           v = i == K ? yk : v;
           L[ii][kk] = v;
@@ -269,7 +273,8 @@ solve2d_kernel(const double* __restrict__ X, const double* __restrict__ Y, const
 
 template <int K, int D, int KF>
 cudaError_t launch_2d(const double* X, const double* Y, const int32_t* S, int64_t nrows, int64_t row_begin,
-                      const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
+                      const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream,
+                      const int32_t* order) {
   using G = G2<K>;
   constexpr int kWarps = 4;
   const size_t smem = sizeof(double) * G::kPerWarp * kWarps;
@@ -283,7 +288,7 @@ cudaError_t launch_2d(const double* X, const double* Y, const int32_t* S, int64_
   const int64_t need = (nrows + kWarps - 1) / kWarps;
   const int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(num_sms) * per_sm);
   solve2d_kernel<K, D, KF><<<static_cast<unsigned>(grid), kWarps * kWarp, smem, stream>>>(X, Y, S, nrows, row_begin,
-                                                                                        kp, C, fail_min);
+                                                                                        kp, C, fail_min, order);
   note_launches(1);
   return cudaGetLastError();
 }
@@ -291,12 +296,12 @@ cudaError_t launch_2d(const double* X, const double* Y, const int32_t* S, int64_
 template <int K, int D>
 cudaError_t launch_2d_kind(const double* X, const double* Y, const int32_t* S, int64_t nrows, int64_t row_begin,
                            const KParams& kp, double* C, unsigned long long* fail_min, int num_sms,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, const int32_t* order) {
   switch (kp.kind == 1 ? 0 : 1 + kp.nu_code) {  // kernel_code(), on the host
-    case 0: return launch_2d<K, D, 0>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
-    case 1: return launch_2d<K, D, 1>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
-    case 2: return launch_2d<K, D, 2>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
-    default: return launch_2d<K, D, 3>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+    case 0: return launch_2d<K, D, 0>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream, order);
+    case 1: return launch_2d<K, D, 1>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream, order);
+    case 2: return launch_2d<K, D, 2>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream, order);
+    default: return launch_2d<K, D, 3>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream, order);
   }
 }
 
@@ -312,14 +317,14 @@ bool fused_solve_2d_supported(int k, int d, int m, const KParams& kp) {
 
 cudaError_t fused_solve_2d(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows,
                            int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
-                           int num_sms, cudaStream_t stream) {
+                           int num_sms, cudaStream_t stream, const int32_t* order) {
   if (nrows <= 0) return cudaSuccess;
   if (k == 50) {
-    return d == 2 ? launch_2d_kind<50, 2>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream)
-                  : launch_2d_kind<50, 3>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+    return d == 2 ? launch_2d_kind<50, 2>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream, order)
+                  : launch_2d_kind<50, 3>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream, order);
   }
-  return d == 2 ? launch_2d_kind<30, 2>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream)
-                : launch_2d_kind<30, 3>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream);
+  return d == 2 ? launch_2d_kind<30, 2>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream, order)
+                : launch_2d_kind<30, 3>(X, Y, S, nrows, row_begin, kp, C, fail_min, num_sms, stream, order);
 }
 
 }  // namespace fmgp

@@ -117,28 +117,24 @@ __device__ __forceinline__ void load_pair(const double* xs, uint32_t t, double (
 #endif
 template <int K, int D, int KF, int NL = kWarp>
 __device__ __forceinline__ void pair_loop(const double* xs, const uint32_t* ptab, const KParams& kp, double* A,
-                                          int lane) {
+                                          int lane, const double* tab) {
   constexpr int PP = D <= 2 ? FMGP_BUILD_PP : FMGP_BUILD_PP3;  // fewer in flight for d = 3 (registers)
   constexpr int npairs = (K * (K - 1)) / 2;
   static_assert(npairs >= PP * NL, "first step loads PP entries per lane");
   const double c = kernel_scale_build<KF>(kp);
-  uint32_t t[PP];
-  double u[PP][D], w[PP][D];
-#pragma unroll
-  for (int i = 0; i < PP; ++i) {
-    t[i] = ptab[lane + i * NL];
-    load_pair<D>(xs, t[i], u[i], w[i]);
-  }
-#pragma unroll 1
-  for (int e = lane; e < npairs; e += PP * NL) {
-    uint32_t tn[PP];
-    double un[PP][D], wn[PP][D];
+  // Two register sets (a, b) in ping-pong: a step evaluates one set while the
+  // other is loaded for the next step, with no register copies between steps.
+  uint32_t ta[PP], tb[PP];
+  double ua[PP][D], wa[PP][D], ub[PP][D], wb[PP][D];
+  auto load = [&](int e, uint32_t (&t)[PP], double (&u)[PP][D], double (&w)[PP][D]) {
 #pragma unroll
     for (int i = 0; i < PP; ++i) {
-      const int f = e + (PP + i) * NL;
-      tn[i] = ptab[f < npairs ? f : e];
-      load_pair<D>(xs, tn[i], un[i], wn[i]);
+      const int f = e + i * NL;
+      t[i] = ptab[f < npairs ? f : lane];
+      load_pair<D>(xs, t[i], u[i], w[i]);
     }
+  };
+  auto eval = [&](int e, const uint32_t (&t)[PP], const double (&u)[PP][D], const double (&w)[PP][D]) {
     double v[PP];
 #pragma unroll
     for (int i = 0; i < PP; ++i) {
@@ -149,20 +145,20 @@ __device__ __forceinline__ void pair_loop(const double* xs, const uint32_t* ptab
         const double dd = u[i][cc] - w[i][cc];
         acc = fma(dd, dd, acc);
       }
-      v[i] = kernel_from_sq_build<KF>(acc, c, kp);
+      v[i] = kernel_from_sq_build<KF>(acc, c, kp, tab);
     }
 #pragma unroll
     for (int i = 0; i < PP; ++i)
-      if (i == 0 || e + i * NL < npairs) A[t[i] >> 16] = v[i];
-#pragma unroll
-    for (int i = 0; i < PP; ++i) {
-      t[i] = tn[i];
-#pragma unroll
-      for (int cc = 0; cc < D; ++cc) {
-        u[i][cc] = un[i][cc];
-        w[i][cc] = wn[i][cc];
-      }
-    }
+      if (e + i * NL < npairs) A[t[i] >> 16] = v[i];
+  };
+  load(lane, ta, ua, wa);
+#pragma unroll 1
+  for (int e = lane; e < npairs; e += 2 * PP * NL) {
+    load(e + PP * NL, tb, ub, wb);
+    eval(e, ta, ua, wa);
+    if (e + PP * NL >= npairs) break;
+    load(e + 2 * PP * NL, ta, ua, wa);
+    eval(e + PP * NL, tb, ub, wb);
   }
 }
 
@@ -170,7 +166,8 @@ __device__ __forceinline__ void pair_loop(const double* xs, const uint32_t* ptab
 // one pair per lane per step from the pair table, no index decode.
 template <int K, int M, int D>
 __device__ void build_small(const double* __restrict__ X, const double* __restrict__ Y, const int32_t* sr,
-                            const KParams& kp, int attempt, double* A, double* xs, const uint32_t* ptab, int lane) {
+                            const KParams& kp, int attempt, double* A, double* xs, const uint32_t* ptab, int lane,
+                            const double* tab) {
   using Sh = RegShape<K, M>;
   for (int e = lane; e < K * D; e += kWarp) {
     const int t = e / D, c = e - t * D;
@@ -178,11 +175,11 @@ __device__ void build_small(const double* __restrict__ X, const double* __restri
   }
   __syncwarp();
   switch (kernel_code(kp)) {  // uniform: one pair loop per kernel kind, no per-pair dispatch
-    case 0: pair_loop<K, D, 0>(xs, ptab, kp, A, lane); break;
-    case 1: pair_loop<K, D, 1>(xs, ptab, kp, A, lane); break;
-    case 2: pair_loop<K, D, 2>(xs, ptab, kp, A, lane); break;
-    case 3: pair_loop<K, D, 3>(xs, ptab, kp, A, lane); break;
-    default: pair_loop<K, D, 4>(xs, ptab, kp, A, lane); break;
+    case 0: pair_loop<K, D, 0>(xs, ptab, kp, A, lane, tab); break;
+    case 1: pair_loop<K, D, 1>(xs, ptab, kp, A, lane, tab); break;
+    case 2: pair_loop<K, D, 2>(xs, ptab, kp, A, lane, tab); break;
+    case 3: pair_loop<K, D, 3>(xs, ptab, kp, A, lane, tab); break;
+    default: pair_loop<K, D, 4>(xs, ptab, kp, A, lane, tab); break;
   }
   const double dg = jitter_r(kp.diag, attempt);
   for (int i = lane; i < K; i += kWarp) A[ro_r(i) + i] = dg;
@@ -719,11 +716,11 @@ __device__ void build_small_half(const double* __restrict__ X, const double* __r
   }
   __syncwarp();
   switch (kernel_code(kp)) {
-    case 0: pair_loop<K, D, 0, 16>(xs, ptab, kp, A, hl); break;
-    case 1: pair_loop<K, D, 1, 16>(xs, ptab, kp, A, hl); break;
-    case 2: pair_loop<K, D, 2, 16>(xs, ptab, kp, A, hl); break;
-    case 3: pair_loop<K, D, 3, 16>(xs, ptab, kp, A, hl); break;
-    default: pair_loop<K, D, 4, 16>(xs, ptab, kp, A, hl); break;
+    case 0: pair_loop<K, D, 0, 16>(xs, ptab, kp, A, hl, kExp2NegTab); break;
+    case 1: pair_loop<K, D, 1, 16>(xs, ptab, kp, A, hl, kExp2NegTab); break;
+    case 2: pair_loop<K, D, 2, 16>(xs, ptab, kp, A, hl, kExp2NegTab); break;
+    case 3: pair_loop<K, D, 3, 16>(xs, ptab, kp, A, hl, kExp2NegTab); break;
+    default: pair_loop<K, D, 4, 16>(xs, ptab, kp, A, hl, kExp2NegTab); break;
   }
   const double dg = jitter_r(kp.diag, rung);
   for (int i = hl; i < K; i += 16) A[ro_r(i) + i] = dg;
@@ -815,29 +812,30 @@ template <int K, int M, int D>
 __global__ void __launch_bounds__(RegLaunch<K, M>::kWarps * kWarp, RegLaunch<K, M>::kMinBlocks)
 solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
                  int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
-                 unsigned long long* __restrict__ fail_min, int gram_min_d) {
+                 unsigned long long* __restrict__ fail_min, int gram_min_d, const int32_t* __restrict__ order) {
   using Sh = RegShape<K, M>;
   extern __shared__ double smem[];
   const int lane = threadIdx.x % kWarp;
   const int warp = threadIdx.x / kWarp;
   const int warps = blockDim.x / kWarp;
   uint32_t* ptab = reinterpret_cast<uint32_t*>(smem);
-  if constexpr (D > 0) {
-    fill_pair_table<K>(ptab);
-    __syncthreads();
-  }
+  __shared__ double s_exp[64];
+  stage_exp_table(s_exp);
+  if constexpr (D > 0) fill_pair_table<K>(ptab);
+  __syncthreads();
   double* A = smem + (D > 0 ? Sh::kTabDoubles : 0) + warp * Sh::per_warp(D);
   double* dinv = A + Sh::kAug;
   double* xs = dinv + ((K + 1) & ~1);
   int32_t* sr = reinterpret_cast<int32_t*>(xs + Sh::xs_doubles(D));
-  for (int64_t r = static_cast<int64_t>(blockIdx.x) * warps + warp; r < nrows;
-       r += static_cast<int64_t>(gridDim.x) * warps) {
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * warps + warp; it < nrows;
+       it += static_cast<int64_t>(gridDim.x) * warps) {
+    const int64_t r = order != nullptr ? order[it] : it;
     for (int t = lane; t < K; t += kWarp) sr[t] = S[r * K + t];
     __syncwarp();
     bool ok = false;
     for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
       if constexpr (D > 0)
-        build_small<K, M, D>(X, Y, sr, kp, attempt, A, xs, ptab, lane);
+        build_small<K, M, D>(X, Y, sr, kp, attempt, A, xs, ptab, lane, s_exp);
       else
       {
         if constexpr (K <= 32) {
@@ -865,7 +863,8 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
 
 template <int K, int M, int D>
 cudaError_t launch_reg(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows, int64_t row_begin,
-                       const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
+                       const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream,
+                       const int32_t* order) {
   using Sh = RegShape<K, M>;
   constexpr int kWarps = RegLaunch<K, M>::kWarps;
   const size_t smem = sizeof(double) * ((D > 0 ? Sh::kTabDoubles : 0) + Sh::per_warp(D) * kWarps);
@@ -883,7 +882,7 @@ cudaError_t launch_reg(const double* X, const double* Y, int d, const int32_t* S
     return (e != nullptr && e[0] == '0') ? INT_MAX : kGramMinD;
   }();
   solve_reg_kernel<K, M, D><<<static_cast<unsigned>(grid), kWarps * kWarp, smem, stream>>>(
-      X, Y, d, S, nrows, row_begin, kp, C, fail_min, gram_min_d);
+      X, Y, d, S, nrows, row_begin, kp, C, fail_min, gram_min_d, order);
   note_launches(1);
   return cudaGetLastError();
 }
@@ -897,10 +896,10 @@ bool fused_solve_reg_supported(int k, int d, int m) {
 
 cudaError_t fused_solve_reg(const double* X, const double* Y, int d, int m, const int32_t* S, int64_t nrows,
                             int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,
-                            int num_sms, cudaStream_t stream) {
+                            int num_sms, cudaStream_t stream, const int32_t* order) {
   if (nrows <= 0) return cudaSuccess;
 #define FMGP_REG_CASE(KK, MM, DD) \
-  return launch_reg<KK, MM, DD>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream)
+  return launch_reg<KK, MM, DD>(X, Y, d, S, nrows, row_begin, kp, C, fail_min, num_sms, stream, order)
   // FMGP_SOLVE_PAIR=1 selects two neighbourhoods per warp for small d (A/B:
   // fewer instructions and shared wavefronts per row, but only 8 warps/SM fit
   // and it is latency-bound: cfg2 solve 14.2 ms vs 13.9 ms for the default)

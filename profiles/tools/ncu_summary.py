@@ -13,7 +13,10 @@ WANT_DETAILS = ["Duration", "Elapsed Cycles", "SM Frequency", "DRAM Throughput",
                 "Achieved Occupancy", "Achieved Active Warps Per SM", "Dynamic Shared Memory Per Block",
                 "Warp Cycles Per Issued Instruction", "Grid Size", "Block Size"]
 RAW_PREFIX = ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_tensor", "sm__inst_executed_pipe_fp64",
-              "sm__pipe_fp64", "sm__pipe_fma_cycles_active", "sm__inst_executed_pipe_tc", "gpu__time_duration.sum"]
+              "sm__pipe_fp64", "sm__pipe_fma_cycles_active", "sm__inst_executed_pipe_tc", "gpu__time_duration.sum",
+              "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime", "sm__inst_executed_pipe_tensor_subpipe_hmma",
+              "sm__mem_tensor_cycles_active.avg", "smsp__thread_inst_executed_per_inst_executed.ratio",
+              "lts__t_sector_hit_rate.pct"]
 
 
 def run(args):

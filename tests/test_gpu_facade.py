@@ -13,13 +13,7 @@ pytestmark = pytest.mark.gpu
 BUILD = Path(__file__).resolve().parent / "cpp" / "_build"
 
 # test case name -> why it cannot pass on this path
-EXPECTED_FAIL = {
-    "test_nn_index": {
-        # HNSW cost model: the facade answers ApproxGraph queries exactly and
-        # reports the exact-scan evaluation count.
-        "graph queries cost far fewer distance evaluations than a scan",
-    },
-}
+EXPECTED_FAIL: dict = {}
 
 
 def parse(stdout):

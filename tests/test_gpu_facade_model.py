@@ -6,7 +6,8 @@
 * FMGP v1 model files move between the reference (oracle/_ref, the
   reference's own TUs) and the facade in both directions: predictions agree
   to the parity bar, and re-saving a loaded file reproduces it byte for byte
-  (Exact and, for reference-written files, ApproxGraph indexes).
+  (Exact and ApproxGraph indexes: a reference-written graph is searched by
+  the facade, a facade-built graph by the reference).
 """
 import json
 import struct
@@ -82,16 +83,19 @@ def test_reference_written_model_loads_into_the_facade(fm, ref, tmp_path, mode):
     assert p_re.read_bytes() == p_ref.read_bytes()  # byte-identical round trip (graph blob kept verbatim)
 
 
-def test_facade_written_model_loads_into_the_reference(fm, ref, tmp_path):
+@pytest.mark.parametrize("mode", [0, 1])
+def test_facade_written_model_loads_into_the_reference(fm, ref, tmp_path, mode):
+    """mode 1: the facade's GPU-built ApproxGraph is written in the reference's
+    layout; the reference loads it and its fast_predict searches that graph."""
     X, Y, mo = _dataset(seed=4)
     k = 20
     data = tmp_path / "data.bin"
-    _write_data(data, X, Y, k, 0, *KP, mo)
+    _write_data(data, X, Y, k, mode, *KP, mo)
     p_fac = tmp_path / "facade.fmgp"
     pred_fac = np.asarray(_tool("save", data, p_fac)["pred"])
     Z = X[: pred_fac.size] + 1e-3
     dims, pred_ref = ref.load_model_predict(p_fac, Z)
-    assert list(dims[:3]) == [X.shape[0], 2, k] and dims[3] == 0
+    assert list(dims[:3]) == [X.shape[0], 2, k] and dims[3] == mode
     assert mean_rel_err(pred_fac, pred_ref).max() <= MEAN_TOL
     # the file holds the facade's S (bit-exact with the reference's) and C (within the parity bar)
     S_ref, C_ref = ref.precompute(X, Y, *KP, k)
