@@ -307,11 +307,27 @@ __device__ __forceinline__ double rsqrt_pivot(double x) {
   return fma(y, t, y);
 }
 
-// exp(-a) for a >= 0 (NaN-free): the exp_neg reduction (m = rint(64 a / ln2),
-// Cody-Waite r, degree-5 polynomial, 2^(-j/64) table) with the rounding done
-// by the 1.5*2^52 shift (m is the low word of the shifted value) and
-// 2^-(m>>6) applied as an exponent-field subtraction on the table value
-// (a <= 708 keeps the result normal). Within 2 ulp of exp(-a).
+// exp(-a) for a >= 0 (NaN-free) on the build paths (kernel-matrix and
+// cross-covariance entries): m = rint(64 a / ln2) by the 1.5*2^52 shift (m is
+// the low word of the shifted value), Cody-Waite r = m ln2/64 - a
+// (|r| <= ln2/128), exp(-a) = 2^-(m>>6) * 2^-((m&63)/64) * e^r with a degree-5
+// polynomial and the 64-entry table of 2^(-j/64) (read from a shared-memory
+// copy, `tab`); 2^-(m>>6) is an exponent-field subtraction on the table value
+// (a <= 708 keeps the result normal). Within 2 ulp of exp(-a). A/B variant
+// (FMGP_EXP_TAB32): a 32-entry table (fewer bank conflicts) and a degree-6
+// polynomial; measured slower at cfg5 in the spatially ordered solve
+// (profiles/r02/ab_exp_table.txt), so not the default.
+__device__ const double kExp2NegTab32[32] = {
+    1.0, 0.9785720620877001, 0.9576032806985737, 0.93708381705515,
+    0.9170040432046712, 0.8973545375015536, 0.8781260801866497, 0.859309649061239,
+    0.8408964152537145, 0.8228777390769825, 0.8052451659746271, 0.7879904225539432,
+    0.7711054127039704, 0.7545822137967114, 0.7384130729697497, 0.7225904034885233,
+    0.7071067811865476, 0.691954940981916, 0.6771277734684463, 0.6626183215798707,
+    0.6484197773255048, 0.6345254785958666, 0.620928906036742, 0.6076236799902345,
+    0.5946035575013605, 0.5818624293887887, 0.5693943173783458, 0.5571933712979462,
+    0.5452538663326288, 0.5335702003384118, 0.5221368912137069, 0.5109485743270583,
+};
+#ifndef FMGP_EXP_TAB32
 __device__ __forceinline__ double exp_neg_build(double a, const double* tab = kExp2NegTab) {
   // a >= 0: clamp at 708 (0x40862000'00000000) by the high word, an integer
   // compare + two selects (a double compare compiles to fmin with NaN fix-ups);
@@ -331,11 +347,29 @@ __device__ __forceinline__ double exp_neg_build(double a, const double* tab = kE
   const double sj = __hiloint2double(__double2hiint(tj) - ((m >> 6) << 20), __double2loint(tj));
   return sj * q;
 }
-
-// Copy of the exp table into shared memory (call with every thread of the CTA, then __syncthreads).
-__device__ __forceinline__ void stage_exp_table(double* dst) {
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) dst[i] = kExp2NegTab[i];
+#define FMGP_BUILD_TAB kExp2NegTab
+#define FMGP_BUILD_TAB_N 64
+#else
+#define FMGP_BUILD_TAB kExp2NegTab32
+#define FMGP_BUILD_TAB_N 32
+__device__ __forceinline__ double exp_neg_build(double a, const double* tab = kExp2NegTab32) {
+  a = __double2hiint(a) < 0x40862000 ? a : 708.0;
+  const double tm = fma(a, 46.16624130844683, 6755399441055744.0);
+  const int m = __double2loint(tm);
+  const double mf = tm - 6755399441055744.0;
+  double r = fma(mf, 0.02166084938653512, -a);  // (ln2/32)_hi, 33 significant bits: mf * hi exact
+  r = fma(mf, 5.9631716539705866e-12, r);        // (ln2/32)_lo
+  double q = fma(r, 1.388888888888889e-03, 8.333333333333333e-03);
+  q = fma(q, r, 4.1666666666666664e-02);
+  q = fma(q, r, 1.6666666666666666e-01);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  const double tj = tab[m & 31];
+  const double sj = __hiloint2double(__double2hiint(tj) - ((m >> 5) << 20), __double2loint(tj));
+  return sj * q;
 }
+#endif
 
 // Kernel value from the squared distance on the register-solve build path
 // (KF as in kernel_from_sq; `c` = the kind's distance scale: sqrt(3)/rho,
@@ -344,12 +378,19 @@ __device__ __forceinline__ void stage_exp_table(double* dst) {
 // register demand does not set the register budget of the solve kernels.
 static __device__ __noinline__ double kernel_eval_general(double dist, const KParams& p);
 
+// Copy of the build exp table into shared memory (32 doubles; call with
+// every thread of the CTA, then __syncthreads).
+__device__ __forceinline__ void stage_exp_table(double* dst) {
+  for (int i = threadIdx.x; i < FMGP_BUILD_TAB_N; i += blockDim.x) dst[i] = FMGP_BUILD_TAB[i];
+}
+
+
 // `tab`: the 2^(-j/64) table of exp_neg_build; the fused solves pass a copy
 // in shared memory (the global table's divergent lookups were ~90% of the
 // solve's L1 sector traffic, profiles/r02/ncu_solve_cfg5_full.txt).
 template <int KF>
 __device__ __forceinline__ double kernel_from_sq_build(double acc, double c, const KParams& p,
-                                                       const double* tab = kExp2NegTab) {
+                                                       const double* tab = FMGP_BUILD_TAB) {
   double v;
   if constexpr (KF == 0) {
     v = p.s2 * exp_neg_build(acc * c, tab);

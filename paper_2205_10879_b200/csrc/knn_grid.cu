@@ -1032,7 +1032,7 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
                     double* __restrict__ out, int32_t* __restrict__ nn_out) {
   __shared__ int32_t s_beg[kQueryThreads / 32][kSlots];
   __shared__ int32_t s_pre[kQueryThreads / 32][kSlots + 1];
-  __shared__ double s_exp[64];
+  __shared__ double s_exp[FMGP_BUILD_TAB_N];
   stage_exp_table(s_exp);
   __syncthreads();
   const GridParams g = *gpp;

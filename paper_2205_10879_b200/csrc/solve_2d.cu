@@ -116,7 +116,7 @@ solve2d_kernel(const double* __restrict__ X, const double* __restrict__ Y, const
   double* ys = area + 4 * K;
   const int a = lane & 3, b = lane >> 2;
   const double cs = kernel_scale_build<KF>(kp);
-  __shared__ double s_exp[64];
+  __shared__ double s_exp[FMGP_BUILD_TAB_N];
   stage_exp_table(s_exp);
   __syncthreads();
 

@@ -819,7 +819,7 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
   const int warp = threadIdx.x / kWarp;
   const int warps = blockDim.x / kWarp;
   uint32_t* ptab = reinterpret_cast<uint32_t*>(smem);
-  __shared__ double s_exp[64];
+  __shared__ double s_exp[FMGP_BUILD_TAB_N];
   stage_exp_table(s_exp);
   if constexpr (D > 0) fill_pair_table<K>(ptab);
   __syncthreads();

@@ -19,6 +19,7 @@ def main():
     import torch
     import paper_2205_10879_b200 as fm
     from paper_2205_10879_b200 import _native as N, datagen
+    from bench import ClockSampler  # nvidia-smi clocks + throttle reasons during the timed calls
     s = torch.cuda.current_stream()
     for cfg in [int(c) for c in a.configs.split(",")]:
         t0 = time.time()
@@ -47,16 +48,17 @@ def main():
                     times.append(e0.elapsed_time(e1))
             return min(times)
 
-        pre = ev(lambda: fm.precompute_device(X, Y, fit, i.k, 0, i.n, S, Cm, s))
-        knn = ev(lambda: N.check(N.LIB.fmgp_query_knn_device(C.c_void_p(X.data_ptr()), i.n, i.d,
-                                                              C.c_void_p(X.data_ptr()), i.n, i.k - 1, 0,
-                                                              C.c_void_p(idx.data_ptr()), None,
-                                                              C.c_void_p(s.cuda_stream))))
-        pred = ev(lambda: fm.predict_device(X, S, Cm, fit, ds.mean_offset, Z, out, None, s))
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            pre = ev(lambda: fm.precompute_device(X, Y, fit, i.k, 0, i.n, S, Cm, s))
+            knn = ev(lambda: N.check(N.LIB.fmgp_query_knn_device(C.c_void_p(X.data_ptr()), i.n, i.d,
+                                                                  C.c_void_p(X.data_ptr()), i.n, i.k - 1, 0,
+                                                                  C.c_void_p(idx.data_ptr()), None,
+                                                                  C.c_void_p(s.cuda_stream))))
+            pred = ev(lambda: fm.predict_device(X, S, Cm, fit, ds.mean_offset, Z, out, None, s))
         line = {"cfg": cfg, "d": i.d, "n_train": i.n, "n_test": i.n_test, "k": i.k, "m": i.m,
                 "precompute_ms": pre, "knn_ms": knn, "solve_ms": pre - knn, "predict_ms": pred,
                 "precompute_train_pts_per_s": i.n / (pre / 1e3), "predict_test_pts_per_s": i.n_test / (pred / 1e3),
-                "gen_s": gen_s}
+                "gen_s": gen_s, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
         del X, Y, Z, S, Cm, out, idx
         torch.cuda.empty_cache()
