@@ -154,12 +154,15 @@ void stage_push(cudaEvent_t knn_begin, cudaEvent_t knn_end, cudaEvent_t solve_en
   g_stage_events.push_back(ev);
 }
 
-cudaError_t replica_finish(fmgp_model_replica& r, int64_t n, int32_t d, int32_t m, const double* mean_offset_host) {
+cudaError_t replica_finish(fmgp_model_replica& r, int64_t n, int32_t d, int32_t k, int32_t m, const double* mean_offset_host) {
   cudaError_t e = cudaMalloc(&r.mo, sizeof(double) * m);
   if (e == cudaSuccess) e = cudaMemcpy(r.mo, mean_offset_host, sizeof(double) * m, cudaMemcpyHostToDevice);
   // the reference's model owns its NeighborIndex (fast_predict.cpp:127-129);
   // here that is the predict walk's cell grid of X, built once per replica
   if (e == cudaSuccess && d <= 3 && !knn_force_brute()) r.grid = fmgp::predict_grid_cache_build(r.X, n, d, 0, &e);
+  // and a cell-ordered copy of the model rows, so predict reads them (and the
+  // neighbours' coordinates) with the locality of the cell-sorted test points
+  if (e == cudaSuccess && r.grid != nullptr) e = fmgp::predict_grid_cache_attach(r.grid, r.S, r.C, k, m, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return e;
 }
@@ -748,7 +751,7 @@ int fmgp_model_create(const double* X, const int32_t* S, const double* C, int64_
   if (e == cudaSuccess) e = cudaMemcpy(r.X, X, sizeof(double) * n * d, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(r.S, S, sizeof(int32_t) * n * k, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(r.C, C, sizeof(double) * n * k * m, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = replica_finish(r, n, d, m, mean_offset);
+  if (e == cudaSuccess) e = replica_finish(r, n, d, k, m, mean_offset);
   if (e != cudaSuccess) {
     fmgp_model_destroy(mdl);
     return cuda_fail(e, "fmgp_model_create");
@@ -782,7 +785,7 @@ int fmgp_model_wrap_device(const double* X, const int32_t* S, const double* C, i
   r.X = const_cast<double*>(X);
   r.S = const_cast<int32_t*>(S);
   r.C = const_cast<double*>(C);
-  cudaError_t e = replica_finish(r, n, d, m, mean_offset);
+  cudaError_t e = replica_finish(r, n, d, k, m, mean_offset);
   if (e != cudaSuccess) {
     fmgp_model_destroy(mdl);
     return cuda_fail(e, "fmgp_model_wrap_device");

@@ -50,7 +50,7 @@ namespace fmgp_capi {
 
 // Finish a replica whose X/S/C are set on the current device: mean offsets
 // (host array of m) and the predict grid. Synchronous.
-cudaError_t replica_finish(fmgp_model_replica& r, int64_t n, int32_t d, int32_t m, const double* mean_offset_host);
+cudaError_t replica_finish(fmgp_model_replica& r, int64_t n, int32_t d, int32_t k, int32_t m, const double* mean_offset_host);
 void replica_release(fmgp_model_replica& r);
 
 }  // namespace fmgp_capi

@@ -60,6 +60,10 @@ namespace fmgp {
 // Predict-walk grid of the training points, built once per model handle (d <= 3).
 void* predict_grid_cache_build(const double* X, int64_t n, int d, cudaStream_t stream, cudaError_t* err);
 void predict_grid_cache_free(void* cache);
+// Attach a grid-ordered copy of the model (m = 1, k <= 64) that predict then
+// reads in cell order (FMGP_PGRID_PERM=0 disables). Synchronous.
+cudaError_t predict_grid_cache_attach(void* cache, const int32_t* S, const double* C, int k, int m,
+                                      cudaStream_t stream);
 cudaError_t predict_grid_cached(const void* cache, const double* X, const int32_t* S, const double* Cf, int k, int m,
                                 const KParams& kp, const double* mean_offset_dev, const double* Z, int64_t nz,
                                 double* out, int32_t* nn_out, int num_sms, cudaStream_t stream);

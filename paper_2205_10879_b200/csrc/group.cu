@@ -695,7 +695,7 @@ int fmgp_group_precompute(fmgp_group* g, const double* X, const double* Y, int64
     Xd[mi] = nullptr;
     cx.S[mi] = nullptr;
     cx.C[mi] = nullptr;
-    if (e == cudaSuccess) e = replica_finish(r, n, d, m, mean_offset);
+    if (e == cudaSuccess) e = replica_finish(r, n, d, k, m, mean_offset);
   }
   if (e != cudaSuccess) {
     fmgp_model_destroy(mdl);

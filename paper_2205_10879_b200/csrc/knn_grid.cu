@@ -1029,7 +1029,8 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
                     const int32_t* __restrict__ cstart, int64_t nq, const double* __restrict__ Qs,
                     const int32_t* __restrict__ qout, const double* __restrict__ X, const int32_t* __restrict__ S,
                     const double* __restrict__ Cf, int k, int m, KParams kp, const double* __restrict__ mean_offset,
-                    double* __restrict__ out, int32_t* __restrict__ nn_out) {
+                    double* __restrict__ out, int32_t* __restrict__ nn_out, const int32_t* __restrict__ pos_of,
+                    const int32_t* __restrict__ s_pos, const double* __restrict__ c_perm) {
   __shared__ int32_t s_beg[kQueryThreads / 32][kSlots];
   __shared__ int32_t s_pre[kQueryThreads / 32][kSlots + 1];
   __shared__ double s_exp[FMGP_BUILD_TAB_N];
@@ -1052,6 +1053,7 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
     for (int t = 0; t < D; ++t) q[t] = has ? Qs[(w0 + lane) * D + t] : 0.0;
     const int64_t orow = !has ? 0 : (qout != nullptr ? qout[w0 + lane] : w0 + lane);
     Cand best{INFINITY, INT_MAX};
+    int32_t bpos = 0;  // grid position of best (the grid-ordered model's row)
     bool certified = !has;
     if constexpr (kThreadNN) {
       if (has) {
@@ -1069,7 +1071,10 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
 #pragma unroll
               for (int t = 0; t < D; ++t) x[t] = __ldg(&pts[static_cast<int64_t>(p) * D + t]);
               const Cand cd{dist_sq_fixed<D>(q, x), __ldg(&pid[p])};
-              if (cless(cd, best)) best = cd;
+              if (cless(cd, best)) {
+                best = cd;
+                bpos = p;
+              }
             }
           }
         }
@@ -1085,7 +1090,10 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
 #pragma unroll
       for (int t = 0; t < D; ++t) qq[t] = __shfl_sync(0xffffffffu, q[t], src);
       const Cand r = warp_nn_walk<D>(g, pts, pid, cstart, qq, rb, rp, lane);
-      if (lane == src) best = r;
+      if (lane == src) {
+        best = r;
+        if (pos_of != nullptr && r.i != INT_MAX) bpos = pos_of[r.i];
+      }
     }
     const bool found = best.i != INT_MAX;
     if (has && nn_out != nullptr) nn_out[orow] = found ? best.i : -1;
@@ -1096,21 +1104,28 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
       const int t0 = lane, t1 = lane + kWarp;
       const bool h0 = t0 < k, h1 = t1 < k;
       const double mo = mean_offset[0];
+      // the grid-ordered model when attached (rows and neighbour coordinates in
+      // cell order), else the model as given
+      const bool perm = s_pos != nullptr;
+      const int32_t* Sr = perm ? s_pos : S;
+      const double* Cr = perm ? c_perm : Cf;
+      const double* Xr = perm ? pts : X;
+      const int32_t rowid = perm ? bpos : best.i;
       // stage loads of point i: its S/C row (needs j_i) and, one step later, its X rows (need S)
       auto load_sc = [&](int i, int64_t& nb0, int64_t& nb1, double& c0, double& c1) {
-        const int32_t jj = __shfl_sync(0xffffffffu, best.i, i);
-        const bool ok = i < nv && jj != INT_MAX;
+        const int32_t jj = __shfl_sync(0xffffffffu, rowid, i);
+        const bool ok = i < nv && __shfl_sync(0xffffffffu, best.i, i) != INT_MAX;
         const int64_t j = ok ? jj : 0;
-        nb0 = ok && h0 ? __ldg(&S[j * k + t0]) : 0;
-        nb1 = ok && h1 ? __ldg(&S[j * k + t1]) : 0;
-        c0 = ok && h0 ? __ldg(&Cf[j * k + t0]) : 0.0;
-        c1 = ok && h1 ? __ldg(&Cf[j * k + t1]) : 0.0;
+        nb0 = ok && h0 ? __ldg(&Sr[j * k + t0]) : 0;
+        nb1 = ok && h1 ? __ldg(&Sr[j * k + t1]) : 0;
+        c0 = ok && h0 ? __ldg(&Cr[j * k + t0]) : 0.0;
+        c1 = ok && h1 ? __ldg(&Cr[j * k + t1]) : 0.0;
       };
       auto load_x = [&](int64_t nb0, int64_t nb1, double (&x0)[D], double (&x1)[D]) {
 #pragma unroll
         for (int u = 0; u < D; ++u) {
-          x0[u] = __ldg(&X[nb0 * D + u]);
-          x1[u] = __ldg(&X[nb1 * D + u]);
+          x0[u] = __ldg(&Xr[nb0 * D + u]);
+          x1[u] = __ldg(&Xr[nb1 * D + u]);
         }
       };
       int64_t nbA0, nbA1;
@@ -1238,14 +1253,15 @@ struct SortBufs {
 // Counting sort of P (np x D) by the cells of `gp`: pts/pid in cell order,
 // cstart = cell offsets.
 template <int D>
-void cell_sort(const double* P, int64_t np, const GridParams* gp, int64_t ncap, SortBufs& b, cudaStream_t s) {
+void cell_sort(const double* P, int64_t np, const GridParams* gp, int64_t ncap, SortBufs& b, cudaStream_t s,
+               int32_t* pos_of = nullptr) {
   cudaMemsetAsync(b.counts, 0, sizeof(int32_t) * (ncap + 1), s);
   count_kernel<D><<<grid1d(np), 256, 0, s>>>(P, np, gp, b.counts, b.key, b.slot);
   const int64_t m = ncap + 1;
   scan_local_kernel<<<static_cast<unsigned>(b.nb), kScanBlock, 0, s>>>(b.counts, m, b.cstart, b.bsums);
   scan_sums_kernel<<<1, kScanBlock, 0, s>>>(b.bsums, b.nb, b.bsums + b.nb);
   scan_add_kernel<<<static_cast<unsigned>(b.nb), kScanBlock, 0, s>>>(b.cstart, m, b.bsums);
-  scatter_kernel<D><<<grid1d(np), 256, 0, s>>>(P, np, b.key, b.slot, b.cstart, b.pts, b.pid, nullptr);
+  scatter_kernel<D><<<grid1d(np), 256, 0, s>>>(P, np, b.key, b.slot, b.cstart, b.pts, b.pid, pos_of);
   note_launches(5);
 }
 
@@ -1386,11 +1402,34 @@ cudaError_t knn_grid_d(const double* Q, int64_t nq, const double* P, int64_t np,
 // model handle (PredictGridCache) and reused by every predict on it.
 constexpr int64_t kPredictSortMin = 4096;  // test batches at least this large are cell-sorted first
 
+// Grid-ordered copy of a model: row p of (s_pos, c_perm) is training point
+// pid[p]'s row of (S, C) with neighbour ids mapped to grid positions. One
+// warp per row (k <= 64: lanes t and t + 32).
+__global__ void permute_model_kernel(int64_t n, int k, int m, const int32_t* __restrict__ pid,
+                                     const int32_t* __restrict__ pos_of, const int32_t* __restrict__ S,
+                                     const double* __restrict__ C, int32_t* __restrict__ s_pos,
+                                     double* __restrict__ c_perm) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; p < n;
+       p += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t j = pid[p];
+    for (int t = lane; t < k; t += 32) s_pos[p * k + t] = pos_of[S[j * k + t]];
+    for (int t = lane; t < k * m; t += 32) c_perm[p * k * m + t] = C[j * k * m + t];
+  }
+}
+
 struct PredictGridCache {
   int d = 0;
   int64_t n = 0;
   GridParams* gp = nullptr;
   SortBufs pb;
+  int32_t* pos_of = nullptr;  // n: grid position of training point i (inverse of pb.pid)
+  // grid-ordered model (predict_grid_cache_attach): row p = training point
+  // pid[p]; neighbour ids as grid positions, so a test point's 1-NN row and
+  // the neighbours' coordinates (pb.pts) are read in cell order
+  int32_t* s_pos = nullptr;
+  double* c_perm = nullptr;
+  int pk = 0, pm = 0;
 };
 
 template <int D>
@@ -1417,7 +1456,9 @@ cudaError_t build_predict_grid(const double* X, int64_t n, PredictGridCache& g, 
   bbox_kernel<<<grid1d(n), 256, 0, s>>>(X, n, D, mm);
   grid_params_kernel<<<1, 1, 0, s>>>(mm, n, D, per_cell, ncap, g.gp);
   note_launches(2);
-  cell_sort<D>(X, n, g.gp, ncap, g.pb, s);
+  err = cudaMallocAsync(&g.pos_of, sizeof(int32_t) * n, s);
+  if (err != cudaSuccess) return err;
+  cell_sort<D>(X, n, g.gp, ncap, g.pb, s, g.pos_of);
   cudaFreeAsync(mm, s);
   return cudaGetLastError();
 }
@@ -1425,6 +1466,10 @@ cudaError_t build_predict_grid(const double* X, int64_t n, PredictGridCache& g, 
 void release_predict_grid(PredictGridCache& g, cudaStream_t s) {
   if (g.gp) cudaFreeAsync(g.gp, s);
   g.gp = nullptr;
+  for (void* p : {static_cast<void*>(g.pos_of), static_cast<void*>(g.s_pos), static_cast<void*>(g.c_perm)})
+    if (p) cudaFreeAsync(p, s);
+  g.pos_of = g.s_pos = nullptr;
+  g.c_perm = nullptr;
   g.pb.release(s);
   g.pb = SortBufs{};
 }
@@ -1452,6 +1497,10 @@ cudaError_t run_predict_grid(const PredictGridCache& g, const double* X, const i
   const int64_t cap = static_cast<int64_t>(num_sms) * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
+  // the grid-ordered model replica, when attached to this grid for these S/C shapes
+  const bool use_perm = g.s_pos != nullptr && S != nullptr && g.pk == k && g.pm == m && m == 1;
+  const int32_t* sp = use_perm ? g.s_pos : nullptr;
+  const double* cp = use_perm ? g.c_perm : nullptr;
   static const bool warp_nn = [] {  // FMGP_PGRID_WARP=1: warp-cooperative 1-NN walk for every point (A/B)
     const char* e = std::getenv("FMGP_PGRID_WARP");
     return e != nullptr && e[0] == '1';
@@ -1461,10 +1510,12 @@ cudaError_t run_predict_grid(const PredictGridCache& g, const double* X, const i
   case KF:                                                                                                      \
     if (warp_nn)                                                                                                \
       grid_predict_kernel<D, KF, false><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                \
-          g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out);   \
+          g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out,    \
+          g.pos_of, sp, cp);                                                                                    \
     else                                                                                                        \
       grid_predict_kernel<D, KF, true><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                 \
-          g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out);   \
+          g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out,    \
+          g.pos_of, sp, cp);                                                                                    \
     break;
     FMGP_PRED_CASE(0)
     FMGP_PRED_CASE(1)
@@ -1528,6 +1579,29 @@ void predict_grid_cache_free(void* cache) {
   release_predict_grid(*g, 0);
   cudaStreamSynchronize(0);
   delete g;
+}
+
+cudaError_t predict_grid_cache_attach(void* cache, const int32_t* S, const double* C, int k, int m,
+                                      cudaStream_t stream) {
+  auto* g = static_cast<PredictGridCache*>(cache);
+  if (g == nullptr || m != 1 || k > 2 * kWarp || g->s_pos != nullptr) return cudaSuccess;
+  static const bool off = [] {  // FMGP_PGRID_PERM=0: predict from the model as given (A/B)
+    const char* e = std::getenv("FMGP_PGRID_PERM");
+    return e != nullptr && e[0] == '0';
+  }();
+  if (off) return cudaSuccess;
+  cudaError_t e = cudaMallocAsync(&g->s_pos, sizeof(int32_t) * g->n * k, stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(&g->c_perm, sizeof(double) * g->n * k * m, stream);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = std::min<int64_t>((g->n * 32 + 255) / 256, 65535);
+  permute_model_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(g->n, k, m, g->pb.pid, g->pos_of, S, C,
+                                                                          g->s_pos, g->c_perm);
+  note_launches(1);
+  g->pk = k;
+  g->pm = m;
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  return e;
 }
 
 cudaError_t predict_grid_cached(const void* cache, const double* X, const int32_t* S, const double* Cf, int k, int m,
