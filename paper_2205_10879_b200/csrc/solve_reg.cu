@@ -805,8 +805,17 @@ cudaError_t launch_pair(const double* X, const double* Y, const int32_t* S, int6
 template <int K, int M>
 struct RegLaunch {
   static constexpr int kWarps = FMGP_REG_WARPS;
-  static constexpr int kMinBlocks = 4;
+  static constexpr int kMinBlocks = 16 / kWarps;  // 16 warps/SM at <= 128 registers
 };
+// FMGP_REG_LOCKSTEP (default 1): the CTA's warps start every row together (a
+// CTA barrier per row), so they run the same region of the ~8 k-instruction
+// unrolled kernel at the same time. Without it the warps drift apart and, in
+// some row orders, miss in the 32 KB instruction cache (cfg5 through
+// fmgp_precompute_device: 128.7 -> 111.7 ms with it; the group path
+// 110.8 -> 112.2 ms; cfg2 13.45 -> 13.23 ms; profiles/r02/ab_cta_shape.txt).
+#ifndef FMGP_REG_LOCKSTEP
+#define FMGP_REG_LOCKSTEP 1
+#endif
 
 template <int K, int M, int D>
 __global__ void __launch_bounds__(RegLaunch<K, M>::kWarps * kWarp, RegLaunch<K, M>::kMinBlocks)
@@ -827,8 +836,11 @@ solve_reg_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
   double* dinv = A + Sh::kAug;
   double* xs = dinv + ((K + 1) & ~1);
   int32_t* sr = reinterpret_cast<int32_t*>(xs + Sh::xs_doubles(D));
-  for (int64_t it = static_cast<int64_t>(blockIdx.x) * warps + warp; it < nrows;
-       it += static_cast<int64_t>(gridDim.x) * warps) {
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * warps; base < nrows;
+       base += static_cast<int64_t>(gridDim.x) * warps) {
+    if constexpr (FMGP_REG_LOCKSTEP) __syncthreads();
+    const int64_t it = base + warp;
+    if (it >= nrows) continue;
     const int64_t r = order != nullptr ? order[it] : it;
     for (int t = lane; t < K; t += kWarp) sr[t] = S[r * K + t];
     __syncwarp();
