@@ -129,8 +129,11 @@ solve2d_kernel(const double* __restrict__ X, const double* __restrict__ Y, const
   }
   const int st0 = G::st(j0), ln0 = G::len(j0), st1 = G::st(j1), ln1 = G::len(j1);
 
-  for (int64_t it = static_cast<int64_t>(blockIdx.x) * warps + warp; it < nrows;
-       it += static_cast<int64_t>(gridDim.x) * warps) {
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * warps; base < nrows;
+       base += static_cast<int64_t>(gridDim.x) * warps) {
+    __syncthreads();  // the CTA's warps start every row together (instruction-cache locality, as solve_reg)
+    const int64_t it = base + warp;
+    if (it >= nrows) continue;
     const int64_t r = order != nullptr ? order[it] : it;
     for (int t = lane; t < K; t += kWarp) sr[t] = S[r * K + t];
     __syncwarp();
