@@ -485,6 +485,10 @@ def main():
 
     # ---- rooflines: algorithmic work per launch / that kernel's average launch time (CUDA events)
     hbm, hbm_src = hbm_peak()
+    # measured DRAM traffic of the same kernels (committed ncu capture of this command), scaled to the step
+    tr = load_json(REPO / "profiles" / "r02" / "traffic.json") or {}
+    tr_solve = tr.get(f"solve_reg_kernel<{k},{m},{d}>") if info.cfg == 5 else None
+    tr_pred = tr.get(f"grid_predict_kernel<{d},3,1>") if info.cfg == 5 else None
     rows_per_rank = (n + ws - 1) // ws
     roof = None
     if solve_ms is not None and knn_ms is not None:
@@ -493,7 +497,11 @@ def main():
             achieved = flops / (solve_ms / 1e3) / 1e12
             roof = {"bound": "fp64", "kernel": "fused solve (gather / kernel build / jitter-Cholesky / solve)",
                     "achieved": achieved, "peak": dfma.value, "unit": "TFLOP/s", "frac": achieved / dfma.value,
-                    "traffic": None,
+                    "traffic": ((tr_solve["dram_read_bytes"] + tr_solve["dram_write_bytes"]) / tr_solve["rows_per_launch"]
+                                * rows_per_rank) if tr_solve else None,
+                    "traffic_unit": "DRAM bytes for the step's rows (ncu per-launch bytes scaled by rows)",
+                    "traffic_source": "profiles/r02/traffic.json" if tr_solve else None,
+                    "fp64_pipe_active_pct_ncu": tr_solve.get("fp64_pipe_active_pct") if tr_solve else None,
                     "work": f"{solve_flops_per_row(info):.0f} fp64 flops per training row (SURVEY 8(d): k^3/3 + "
                             f"2k^2m + 3d k(k-1)/2; the k(k-1)/2 kernel evaluations are not counted) x {rows_per_rank} "
                             "rows per rank",
@@ -520,7 +528,9 @@ def main():
                                  "frac": pred_gbs / hbm, "peak_source": hbm_src,
                                  "work": f"{predict_bytes_per_point(info)} B per test point (SURVEY 8(d)) x "
                                          f"{pred_pts} points per rank; the stage also runs the grid 1-NN walk",
-                                 "traffic": None},
+                                 "traffic": ((tr_pred["dram_read_bytes"] + tr_pred["dram_write_bytes"])
+                                             / tr_pred["points_per_launch"] * pred_pts) if tr_pred else None,
+                                 "traffic_source": "profiles/r02/traffic.json" if tr_pred else None},
                     "e2e": pred_e2e, "gpu_launches": pred_launch},
         "stages_ms": {"knn": knn_ms, "solve": solve_ms, "precompute": pre_ms, "predict": pred_ms},
         "e2e": e2e,
