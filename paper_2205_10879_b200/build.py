@@ -27,7 +27,7 @@ CPP = PKG / "cpp"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SOURCES = ["knn.cu", "knn_grid.cu", "knn_tc.cu", "solve.cu", "solve_big.cu", "solve_tc.cu", "solve_reg.cu", "solve_2d.cu", "solve_cta.cu", "predict.cu", "misc.cu", "capi.cu", "muygps.cu", "group.cu", "graph.cu"]
+CUDA_SOURCES = ["knn.cu", "knn_grid.cu", "knn_tc.cu", "solve.cu", "solve_big.cu", "solve_tc.cu", "solve_reg.cu", "solve_2d.cu", "solve_dm.cu", "solve_cta.cu", "predict.cu", "misc.cu", "capi.cu", "muygps.cu", "group.cu", "graph.cu"]
 FACADE_SOURCES = ["facade_kernel.cpp", "facade_linalg.cpp", "facade_nn_index.cpp", "facade_fast_predict.cpp",
                   "facade_dataset.cpp", "facade_muygps.cpp"]
 

@@ -385,7 +385,9 @@ cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const in
     const std::string v(e);
     return v == "tc" ? 1 : (v == "scalar" ? 2 : 0);
   }();
-  if (mode == 0 && status == nullptr && (fused_solve_2d_supported(k, d, m, kp) || fused_solve_reg_supported(k, d, m))) {
+  if (mode == 0 && status == nullptr &&
+      (fused_solve_dm_supported(k, d, m, kp) || fused_solve_2d_supported(k, d, m, kp) ||
+       fused_solve_reg_supported(k, d, m))) {
     // Large low-d batches are solved in a cell order of their rows (FMGP_SOLVE_ORDER=0: index order):
     // warps in flight then gather overlapping neighbourhoods, so X stays in L2.
     static const bool use_order = [] {
@@ -402,10 +404,12 @@ cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const in
         return e;
       }
     }
-    const cudaError_t e = fused_solve_2d_supported(k, d, m, kp)
-                              ? fused_solve_2d(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order)
-                              : fused_solve_reg(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream,
-                                                order);
+    const cudaError_t e =
+        fused_solve_dm_supported(k, d, m, kp)
+            ? fused_solve_dm(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order)
+            : (fused_solve_2d_supported(k, d, m, kp)
+                   ? fused_solve_2d(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order)
+                   : fused_solve_reg(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order));
     if (order != nullptr) cudaFreeAsync(order, stream);
     return e;
   }
