@@ -22,18 +22,24 @@
 //             rounding, subnormals included) and eps_q = (2 DP + 32) 2^-22
 //             (n^_q + max n^_p)(1+1e-3) + 2^-20 (fp32 accumulation of the dot and
 //             norm terms even with truncating adds, the norm split, n^_q in fp32).
-//   epilogue  per query a max-heap of the kk smallest v plus a buffer of the points
-//             with v <= W - n^_q, W = T~ + 2 E(T~) (T~ = heap root + n^_q): every
-//             point of the exact top-kk is in heap u buffer at all times. Per
-//             32-column chunk one max over g decides whether any lane needs it.
-//   recheck   tc_recheck_kernel: exact fp64 keys of heap u buffer from the original
+//   epilogue  per query an unsorted, append-only candidate buffer (cap entries, 32/64/128)
+//             holding every point seen so far with v <= win, win = W - n^_q,
+//             W = T~ + 2 E(T~), T~ >= the kk-th smallest D~ seen: every point of the
+//             exact top-kk is in the buffer at all times. An admission is one
+//             shared-memory append; when a query's buffer is full the WARP compacts
+//             it (each lane takes cap/32 entries: bisection on the ordered key bits
+//             for the kk-th smallest, new window, ballot-prefix compaction), so the
+//             expensive step runs on 32 lanes instead of the one diverged lane a
+//             per-query heap sift occupies. Per 32-column chunk one max over g
+//             decides whether any lane needs it.
+//   recheck   tc_recheck_kernel: exact fp64 keys of the buffer from the original
 //             coordinates, top-kk by (key, index) — the reference's order. A
-//             buffer that would overflow flags its query for the fp64 brute force.
+//             buffer a compaction cannot shrink flags its query for the fp64 brute force.
 // Roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer (one elected
 // lane), warps 2-5 epilogue (thread = TMEM lane = query). When both candidate
 // lists fit (cap <= 64, i.e. kk <= 35) and DP == 64, warps 6-9 form a second epilogue set:
-// each set takes half of every tile's columns with its own heap + window
-// buffer per query, and the recheck merges the two candidate sets.
+// each set takes half of every tile's columns with its own candidate buffer
+// per query, and the recheck merges the two candidate sets.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
@@ -287,9 +293,77 @@ struct TcArgs {
 
 // Admission window W = T + 2 E(T), E(T) = 2 eta (sqrt(T) + 2 eta) + eta^2 + eps (scaled units).
 __device__ __forceinline__ float window_of(float T, double eta, double eps) {
-  const double t = static_cast<double>(T);
+  const double t = fmax(static_cast<double>(T), 0.0);  // D~ of a near-duplicate can round below 0
   const double E = 2.0 * eta * (sqrt(t) + 2.0 * eta) + eta * eta + eps;
   return static_cast<float>((t + 2.0 * E) * 1.0001 + 1e-30);
+}
+
+// Order-preserving map float -> uint32 (and back) for the selection below.
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return b ^ (static_cast<uint32_t>(static_cast<int32_t>(b) >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u ^ 0x80000000u) : ~u);
+}
+
+// Warp-cooperative compaction of ONE query's candidate buffer (sk / si: its n
+// entries, n <= 128, contiguous in shared memory). Every lane takes the entries
+// t = lane, lane + 32, ...; T = a value with at least kk entries <= T, found by
+// bisection on the ordered key bits between the buffer's minimum and maximum
+// (stops at a count of kk or kk + 1: T is then the kk-th or (kk+1)-th smallest
+// v); the new admission bound is win = W(T + n^_q) - n^_q and the entries
+// above it are dropped (ballot-prefix compaction, order preserved). Returns
+// the new count; win_out = the new bound. All 32 lanes call it with the same
+// arguments (n >= kk).
+__device__ __noinline__ int compact_candidates(float* sk, int32_t* si, int n, int kk, float nqf, double eta, double eps,
+                                               float* win_out) {
+  const int lane = threadIdx.x & 31;
+  float f[4];
+  int32_t id[4];
+  uint32_t u[4];
+  uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int t = s * 32 + lane;
+    const bool in = t < n;
+    f[s] = in ? sk[t] : INFINITY;
+    id[s] = in ? si[t] : 0;
+    u[s] = in ? f2ord(f[s]) : 0xffffffffu;
+    mn = min(mn, u[s]);
+    mx = in ? max(mx, u[s]) : mx;
+  }
+  __syncwarp();
+  uint32_t H = __reduce_max_sync(0xffffffffu, mx);      // count(u <= H) = n >= kk
+  uint32_t L = __reduce_min_sync(0xffffffffu, mn) - 1u;  // count(u <= L) = 0 < kk
+  for (int round = 0; round < 32 && H - L > 1u; ++round) {
+    const uint32_t mid = L + ((H - L) >> 1);
+    const int c = __reduce_add_sync(0xffffffffu, (u[0] <= mid ? 1 : 0) + (u[1] <= mid ? 1 : 0) +
+                                                     (u[2] <= mid ? 1 : 0) + (u[3] <= mid ? 1 : 0));
+    if (c >= kk) {
+      H = mid;
+      if (c <= kk + 1) break;
+    } else {
+      L = mid;
+    }
+  }
+  const float win = window_of(ord2f(H) + nqf, eta, eps) - nqf;
+  int base = 0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (s * 32 >= n) break;
+    const bool keep = s * 32 + lane < n && f[s] <= win;
+    const uint32_t b = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int pos = base + __popc(b & ((1u << lane) - 1u));
+      sk[pos] = f[s];
+      si[pos] = id[s];
+    }
+    base += __popc(b);
+  }
+  __syncwarp();
+  *win_out = win;
+  return base;
 }
 
 __global__ void __launch_bounds__(kMaxThreads, 1)
@@ -304,9 +378,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   const bool ares = a.KB == 1;
   const int nst = a.stages;
   const int halves = a.halves;
-  float* lk = reinterpret_cast<float*>(slots + a.nslots * kABytes);  // [halves][cap][128] candidate v (column = query)
-  int32_t* li = reinterpret_cast<int32_t*>(lk + halves * a.cap * kBM);  // [halves][cap][128] candidate index
-  float* scratch = reinterpret_cast<float*>(li + halves * a.cap * kBM);   // [4*halves warps][32][kScrStride]
+  // candidate buffers, one row per (half, query): cap entries + 1 pad (row stride odd: both the
+  // per-lane appends and the warp-cooperative compaction of one row are bank-conflict free)
+  const int lstride = a.cap + 1;
+  float* lk = reinterpret_cast<float*>(slots + a.nslots * kABytes);     // [halves][128][cap + 1] candidate v
+  int32_t* li = reinterpret_cast<int32_t*>(lk + halves * kBM * lstride);  // [halves][128][cap + 1] candidate index
+  float* scratch = reinterpret_cast<float*>(li + halves * kBM * lstride);  // [4*halves warps][32][kScrStride]
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 4 * halves * 32 * kScrStride);
   uint64_t* empty = full + kBars;
   uint64_t* tfull = empty + kBars;  // kTBufs TMEM buffers
@@ -428,8 +505,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
     const double pmax = __longlong_as_double(static_cast<long long>(*a.pmax_bits));
     float* scr = scratch + (ew * 32 + lane) * kScrStride;  // this lane's hot-chunk values
-    float* mk = lk + half * a.cap * kBM + row;  // this query's column of its half's list (stride kBM)
-    int32_t* mi = li + half * a.cap * kBM + row;
+    float* wk0 = lk + (half * kBM + quarter * 32) * lstride;  // this warp's 32 buffers (lane l: + l * lstride)
+    int32_t* wi0 = li + (half * kBM + quarter * 32) * lstride;
+    float* bk = wk0 + lane * lstride;  // this query's buffer
+    int32_t* bi = wi0 + lane * lstride;
     const int h0 = half * (kBN / 32) / halves, h1 = (half + 1) * (kBN / 32) / halves;  // its chunks
     int buf = 0;
     uint32_t tphase = 0;
@@ -442,19 +521,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       const double eps = (2 * a.DP + 32) * 2.384185791015625e-7 * (nq_hat + pmax * pmax) * 1.001 + 9.5367431640625e-7;
       const int64_t excl = a.excl != nullptr ? (valid ? a.excl[q] : -1)
                                              : (a.self_offset >= 0 ? q + a.self_offset : -1);
-      // Candidate state (shared memory, column `row`, stride kBM):
-      //   heap[0..hn)   max-heap by D~ of the kk smallest so far (root = T~)
-      //   wb[0..wn)     window buffer: points with T~ < D~ <= W = T~ + 2E(T~)
-      // Every point of the exact top-kk is in heap u wb at all times.
-      float* hk = mk;
-      int32_t* hi = mi;
-      float* wk = mk + a.kk * kBM;
-      int32_t* wi_ = mi + a.kk * kBM;
-      const int wcap = a.cap - a.kk;
-      int hn = 0, wn = 0;
+      // Candidate state: bk/bi[0..cnt) = every point seen so far with v <= win (unsorted).
+      // win = +inf until the first compaction (cnt reaches cap >= kk + 29), then
+      // W(T~) - n^_q with T~ >= the kk-th smallest D~ seen, so the exact top-kk is inside.
+      int cnt = 0;
       bool over = false;
       float win = valid ? INFINITY : -INFINITY;  // admission bound on D~ - n^_q
-      float root = INFINITY;
       const int64_t pt_end = a.debug_G ? 1 : npt;
       for (int64_t pt = 0; pt < pt_end; ++pt) {
         mbar_wait(&tfull[buf], tphase);
@@ -515,80 +587,40 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
                   make_float4(-2.0f * __uint_as_float(r[c + 4]), -2.0f * __uint_as_float(r[c + 5]),
                               -2.0f * __uint_as_float(r[c + 6]), -2.0f * __uint_as_float(r[c + 7]));
             }
-            if (mask == 0) continue;
-            while (mask != 0) {
-              const int c = __ffs(mask) - 1;
-              mask &= mask - 1;
-              const float v = scr[c];
-              const int64_t j = j0 + c;
-              if (!(v <= win) || j == excl) continue;
-              if (hn < a.kk) {  // fill the heap (sift up)
-                int pos = hn++;
-                while (pos > 0) {
-                  const int par = (pos - 1) >> 1;
-                  const float pk = hk[par * kBM];
-                  if (pk >= v) break;
-                  hk[pos * kBM] = pk;
-                  hi[pos * kBM] = hi[par * kBM];
-                  pos = par;
-                }
-                hk[pos * kBM] = v;
-                hi[pos * kBM] = static_cast<int32_t>(j);
-                if (hn == a.kk) {
-                  root = hk[0];
-                  win = window_of(root + nqf, eta, eps) - nqf;
-                }
-                continue;
+            // admissions: append; a lane whose buffer is full stops with its remaining bits
+            // pending, the warp compacts those lanes' buffers one by one, and the lanes go on
+            for (;;) {
+              while (mask != 0 && cnt < a.cap) {
+                const int c = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const float v = scr[c];
+                const int64_t j = j0 + c;
+                if (!(v <= win) || j == excl) continue;
+                bk[cnt] = v;
+                bi[cnt] = static_cast<int32_t>(j);
+                ++cnt;
               }
-              float vk = v;  // the value that goes to the window buffer
-              int32_t vi = static_cast<int32_t>(j);
-              if (v < root) {  // replace the root, sift down; the old root moves to the buffer
-                vk = root;
-                vi = hi[0];
-                int pos = 0;
-                for (;;) {
-                  const int l = 2 * pos + 1;
-                  if (l >= a.kk) break;
-                  int ch2 = l;
-                  float ck = hk[l * kBM];
-                  if (l + 1 < a.kk) {
-                    const float rk = hk[(l + 1) * kBM];
-                    if (rk > ck) {
-                      ck = rk;
-                      ch2 = l + 1;
-                    }
+              uint32_t need = __ballot_sync(0xffffffffu, mask != 0);
+              if (need == 0) break;
+              while (need != 0) {
+                const int src = __ffs(need) - 1;
+                need &= need - 1;
+                const float s_nqf = __shfl_sync(0xffffffffu, nqf, src);
+                const double s_eta = __shfl_sync(0xffffffffu, eta, src);
+                const double s_eps = __shfl_sync(0xffffffffu, eps, src);
+                float nwin;
+                const int nn = compact_candidates(wk0 + src * lstride, wi0 + src * lstride, a.cap, a.kk, s_nqf,
+                                                  s_eta, s_eps, &nwin);
+                if (lane == src) {
+                  cnt = nn;
+                  win = nwin;
+                  if (nn >= a.cap) {  // the window alone fills the buffer: the query is redone exactly
+                    over = true;
+                    win = -INFINITY;
+                    mask = 0;
+                    cnt = 0;
                   }
-                  if (ck <= v) break;
-                  hk[pos * kBM] = ck;
-                  hi[pos * kBM] = hi[ch2 * kBM];
-                  pos = ch2;
                 }
-                hk[pos * kBM] = v;
-                hi[pos * kBM] = static_cast<int32_t>(j);
-                root = hk[0];
-                win = window_of(root + nqf, eta, eps) - nqf;
-              }
-              if (vk <= win) {
-                if (wn == wcap) {  // compact: drop entries that left the window
-                  int o = 0;
-                  for (int t = 0; t < wn; ++t) {
-                    const float tk = wk[t * kBM];
-                    if (tk <= win) {
-                      wk[o * kBM] = tk;
-                      wi_[o * kBM] = wi_[t * kBM];
-                      ++o;
-                    }
-                  }
-                  wn = o;
-                }
-                if (wn == wcap) {
-                  over = true;  // the query is redone exactly
-                  win = -INFINITY;
-                  continue;
-                }
-                wk[wn * kBM] = vk;
-                wi_[wn * kBM] = vi;
-                ++wn;
               }
             }
           }
@@ -600,9 +632,25 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           tphase ^= 1;
         }
       }
-      // candidates = heap u buffer (the exact top-kk is inside); the exact
-      // recheck and selection run in tc_recheck_kernel
-      if (!valid || a.debug_G) continue;
+      // candidates = the buffer (the exact top-kk is inside), trimmed once more to the final
+      // window; the exact recheck and selection run in tc_recheck_kernel
+      if (a.debug_G) continue;
+      {
+        uint32_t need = __ballot_sync(0xffffffffu, valid && !over && cnt > a.kk);
+        while (need != 0) {
+          const int src = __ffs(need) - 1;
+          need &= need - 1;
+          const float s_nqf = __shfl_sync(0xffffffffu, nqf, src);
+          const double s_eta = __shfl_sync(0xffffffffu, eta, src);
+          const double s_eps = __shfl_sync(0xffffffffu, eps, src);
+          const int s_cnt = __shfl_sync(0xffffffffu, cnt, src);
+          float nwin;
+          const int nn = compact_candidates(wk0 + src * lstride, wi0 + src * lstride, s_cnt, a.kk, s_nqf, s_eta,
+                                            s_eps, &nwin);
+          if (lane == src) cnt = nn;
+        }
+      }
+      if (!valid) continue;
       if (over) {
         const int32_t slot = atomicAdd(a.overflow, 1);
         a.overflow[1 + slot] = static_cast<int32_t>(q);
@@ -610,9 +658,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         continue;
       }
       int32_t* cq = a.cand + static_cast<int64_t>(half) * a.cap * a.nq + q;  // this half's rows
-      for (int t = 0; t < hn; ++t) cq[t * a.nq] = hi[t * kBM];
-      for (int t = 0; t < wn; ++t) cq[(hn + t) * a.nq] = wi_[t * kBM];
-      a.ccount[half * a.nq + q] = hn + wn;
+      for (int t = 0; t < cnt; ++t) cq[t * a.nq] = bi[t];
+      a.ccount[half * a.nq + q] = cnt;
     }
   }
   tc_fence_before();
@@ -781,12 +828,12 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   if (nq <= 0) return cudaSuccess;
   const int KB = (d + 3 + kBK - 1) / kBK;  // + 3 columns for the point-norm split
   const int DP = KB * kBK;
-  const int cap = std::min(kCapMax, ((kk + 29 + 3) / 4) * 4);
+  const int cap = std::min(kCapMax, ((kk + 29 + 31) / 32) * 32);  // 32 / 64 / 96 / 128: slack >= 29 over kk
   // 8 epilogue warps (two column halves with separate candidate lists) when both
   // lists fit next to the operand slots and the recheck's 128-candidate warp
   auto smem_for = [&](int hv, int nslots) {
     return static_cast<size_t>(1024) + static_cast<size_t>(nslots) * kABytes +
-           static_cast<size_t>(hv) * cap * kBM * 8 + sizeof(float) * 4 * hv * 32 * kScrStride + 256;
+           static_cast<size_t>(hv) * (cap + 1) * kBM * 8 + sizeof(float) * 4 * hv * 32 * kScrStride + 256;
   };
   // Only when the epilogue is the bound (DP == 64: resident query tile, cheap
   // recheck); for wide rows (KB > 1) the GEMM/TMA side and the doubled recheck dominate.

@@ -1,5 +1,5 @@
 """Run one stage of the path once on cuda:0 (for ncu captures):
-    python profiles/tools/run_stage.py --cfg 2 --n 200000 --stage precompute|predict|knn"""
+    python profiles/tools/run_stage.py --cfg 2 --n 200000 --stage precompute|predict|knn|knnrows [--rows R]"""
 import argparse
 import ctypes as C
 import sys
@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--nt", type=int, default=200000)
     ap.add_argument("--stage", default="precompute")
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--rows", type=int, default=0, help="knnrows: neighbour rows [0, rows) against all n points")
     a = ap.parse_args()
     import torch
     import paper_2205_10879_b200 as fm
@@ -37,6 +38,10 @@ def main():
             s = torch.cuda.current_stream()
             N.check(N.LIB.fmgp_query_knn_device(C.c_void_p(X.data_ptr()), a.n, i.d, C.c_void_p(X.data_ptr()), a.n,
                                                 i.k - 1, 0, C.c_void_p(S.data_ptr()), None, C.c_void_p(s.cuda_stream)))
+        if a.stage == "knnrows":
+            s = torch.cuda.current_stream()
+            N.check(N.LIB.fmgp_knn_rows_device(C.c_void_p(X.data_ptr()), a.n, i.d, i.k, 0, a.rows or a.n,
+                                               C.c_void_p(S.data_ptr()), C.c_void_p(s.cuda_stream)))
     torch.cuda.synchronize()
     print("ok")
 
