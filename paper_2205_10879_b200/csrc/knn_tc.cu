@@ -22,8 +22,10 @@
 //             rounding, subnormals included) and eps_q = (2 DP + 32) 2^-22
 //             (n^_q + max n^_p)(1+1e-3) + 2^-20 (fp32 accumulation of the dot and
 //             norm terms even with truncating adds, the norm split, n^_q in fp32).
-//   epilogue  per query an unsorted, append-only candidate buffer (cap entries, 32/64/128)
-//             holding every point seen so far with v <= win, win = W - n^_q,
+//   epilogue  per query an unsorted, append-only candidate buffer (wcap = 64/128/256 (v, index)
+//             pairs in a per-CTA global scratch area that stays in L2; an append is one
+//             fire-and-forget 8-byte store) holding every point seen so far with
+//             v <= win, win = W - n^_q,
 //             W = T~ + 2 E(T~), T~ >= the kk-th smallest D~ seen: every point of the
 //             exact top-kk is in the buffer at all times. An admission is one
 //             shared-memory append; when a query's buffer is full the WARP compacts
@@ -36,10 +38,12 @@
 //             coordinates, top-kk by (key, index) — the reference's order. A
 //             buffer a compaction cannot shrink flags its query for the fp64 brute force.
 // Roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer (one elected
-// lane), warps 2-5 epilogue (thread = TMEM lane = query). When both candidate
-// lists fit (cap <= 64, i.e. kk <= 35) and DP == 64, warps 6-9 form a second epilogue set:
-// each set takes half of every tile's columns with its own candidate buffer
-// per query, and the recheck merges the two candidate sets.
+// lane), warps 2-5 epilogue (thread = TMEM lane = query). The epilogue is
+// latency-bound with one warp per scheduler, and the candidate state no longer
+// lives in shared memory, so TWO CTAs run per SM (256 TMEM columns = 2
+// accumulator buffers each, ~85-115 KB of operand stages each): two independent
+// query tiles per SM, eight epilogue warps (FMGP_TC_CTAS=1: one CTA per SM
+// with deeper operand pipelines).
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
@@ -66,9 +70,10 @@ constexpr int kStagesMax = 4;    // ... and maximum (as many as shared memory le
 constexpr int kBStagesRes = 3;   // B-only stages when the query tile is resident (KB == 1), minimum
 constexpr int kBStagesResMax = 6;  // ... and maximum
 constexpr int kBars = kStagesMax > kBStagesResMax ? kStagesMax : kBStagesResMax;  // stage barriers
-constexpr int kTBufs = 4;        // TMEM accumulator buffers (4 x 128 columns)
-constexpr int kCapMax = 128;  // candidate-list capacity per query (kk <= kCapMax - 29)
-constexpr int kMaxThreads = 320;  // TMA + MMA + 4 or 8 epilogue warps (8: two column halves, lists fit twice)
+constexpr int kTBufs = 2;        // TMEM accumulator buffers per CTA (2 x 128 columns; two CTAs per SM)
+constexpr int kCapMax = 128;  // candidates per query handed to the recheck (kk <= kCapMax - 29)
+constexpr int kWcapMax = 256;  // working buffer entries per query (8 per lane in a compaction)
+constexpr int kMaxThreads = 192;  // TMA + MMA + 4 epilogue warps
 constexpr int kScrStride = 36;  // floats per lane scratch row (16 B aligned, spreads banks)
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
 constexpr uint32_t kBBytes = kBN * kBK * 2;  // 16 KB
@@ -277,7 +282,8 @@ struct TcArgs {
   const int32_t* excl;   // or per-query exclusion (nullable)
   int with_self;
   int wait_mode;         // producer-side wait (see mbar_wait_sleep)
-  int halves;            // 1: 4 epilogue warps; 2: 8 (each tile's columns split, separate lists)
+  int wcap;              // working candidate buffer entries per query (64 / 128 / 256)
+  uint2* gbuf;           // [gridDim.x][128][wcap] (v bits, index) working buffers (global scratch, L2)
   int stages;            // pipeline stages: A+B pairs (KB > 1, kStages .. kStagesMax) or B tiles
                          // (KB == 1, kBStagesRes .. kBStagesResMax)
   int nslots;            // 16 KB operand slots: 1 + stages (resident) or 2 * stages
@@ -307,42 +313,46 @@ __device__ __forceinline__ float ord2f(uint32_t u) {
   return __uint_as_float((u & 0x80000000u) ? (u ^ 0x80000000u) : ~u);
 }
 
-// Warp-cooperative compaction of ONE query's candidate buffer (sk / si: its n
-// entries, n <= 128, contiguous in shared memory). Every lane takes the entries
-// t = lane, lane + 32, ...; T = a value with at least kk entries <= T, found by
+// Warp-cooperative compaction of ONE query's candidate buffer (gb: its n
+// (v bits, index) entries, n <= kWcapMax, contiguous in the global scratch
+// area; read with ld.global.cg, so the entries other lanes appended or
+// compacted are seen from L2). Every lane takes the entries t = lane,
+// lane + 32, ...; T = a value with at least kk entries <= T, found by
 // bisection on the ordered key bits between the buffer's minimum and maximum
-// (stops at a count of kk or kk + 1: T is then the kk-th or (kk+1)-th smallest
-// v); the new admission bound is win = W(T + n^_q) - n^_q and the entries
-// above it are dropped (ballot-prefix compaction, order preserved). Returns
-// the new count; win_out = the new bound. All 32 lanes call it with the same
-// arguments (n >= kk).
-__device__ __noinline__ int compact_candidates(float* sk, int32_t* si, int n, int kk, float nqf, double eta, double eps,
-                                               float* win_out) {
+// (exact: T = the kk-th smallest v; otherwise it may stop at the (kk+1)-th);
+// the new admission bound is win = W(T + n^_q) - n^_q and the entries above it
+// are dropped (ballot-prefix compaction, order preserved). Returns the new
+// count; win_out = the new bound. All 32 lanes call it with the same arguments
+// (n >= kk).
+__device__ __noinline__ int compact_candidates(uint2* gb, int n, int kk, float nqf, double eta, double eps,
+                                               bool exact, float* win_out) {
+  constexpr int NE = kWcapMax / 32;
   const int lane = threadIdx.x & 31;
-  float f[4];
-  int32_t id[4];
-  uint32_t u[4];
+  uint2 e[NE];
+  uint32_t u[NE];
   uint32_t mn = 0xffffffffu, mx = 0u;
+  __syncwarp();
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
+  for (int s = 0; s < NE; ++s) {
     const int t = s * 32 + lane;
     const bool in = t < n;
-    f[s] = in ? sk[t] : INFINITY;
-    id[s] = in ? si[t] : 0;
-    u[s] = in ? f2ord(f[s]) : 0xffffffffu;
+    e[s] = in ? __ldcg(gb + t) : make_uint2(0x7f800000u, 0u);
+    u[s] = in ? f2ord(__uint_as_float(e[s].x)) : 0xffffffffu;
     mn = min(mn, u[s]);
     mx = in ? max(mx, u[s]) : mx;
   }
   __syncwarp();
   uint32_t H = __reduce_max_sync(0xffffffffu, mx);      // count(u <= H) = n >= kk
   uint32_t L = __reduce_min_sync(0xffffffffu, mn) - 1u;  // count(u <= L) = 0 < kk
-  for (int round = 0; round < 32 && H - L > 1u; ++round) {
+  for (int round = 0; round < 34 && H - L > 1u; ++round) {
     const uint32_t mid = L + ((H - L) >> 1);
-    const int c = __reduce_add_sync(0xffffffffu, (u[0] <= mid ? 1 : 0) + (u[1] <= mid ? 1 : 0) +
-                                                     (u[2] <= mid ? 1 : 0) + (u[3] <= mid ? 1 : 0));
+    int cl = 0;
+#pragma unroll
+    for (int s = 0; s < NE; ++s) cl += u[s] <= mid ? 1 : 0;
+    const int c = __reduce_add_sync(0xffffffffu, cl);
     if (c >= kk) {
       H = mid;
-      if (c <= kk + 1) break;
+      if (c == kk || (!exact && c == kk + 1)) break;
     } else {
       L = mid;
     }
@@ -350,15 +360,11 @@ __device__ __noinline__ int compact_candidates(float* sk, int32_t* si, int n, in
   const float win = window_of(ord2f(H) + nqf, eta, eps) - nqf;
   int base = 0;
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
+  for (int s = 0; s < NE; ++s) {
     if (s * 32 >= n) break;
-    const bool keep = s * 32 + lane < n && f[s] <= win;
+    const bool keep = s * 32 + lane < n && __uint_as_float(e[s].x) <= win;
     const uint32_t b = __ballot_sync(0xffffffffu, keep);
-    if (keep) {
-      const int pos = base + __popc(b & ((1u << lane) - 1u));
-      sk[pos] = f[s];
-      si[pos] = id[s];
-    }
+    if (keep) gb[base + __popc(b & ((1u << lane) - 1u))] = e[s];
     base += __popc(b);
   }
   __syncwarp();
@@ -366,7 +372,7 @@ __device__ __noinline__ int compact_candidates(float* sk, int32_t* si, int n, in
   return base;
 }
 
-__global__ void __launch_bounds__(kMaxThreads, 1)
+__global__ void __launch_bounds__(kMaxThreads, 2)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmP, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B operands) by offsetting the __shared__ pointer itself,
@@ -377,14 +383,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   uint8_t* slots = smem;
   const bool ares = a.KB == 1;
   const int nst = a.stages;
-  const int halves = a.halves;
-  // candidate buffers, one row per (half, query): cap entries + 1 pad (row stride odd: both the
-  // per-lane appends and the warp-cooperative compaction of one row are bank-conflict free)
-  const int lstride = a.cap + 1;
-  float* lk = reinterpret_cast<float*>(slots + a.nslots * kABytes);     // [halves][128][cap + 1] candidate v
-  int32_t* li = reinterpret_cast<int32_t*>(lk + halves * kBM * lstride);  // [halves][128][cap + 1] candidate index
-  float* scratch = reinterpret_cast<float*>(li + halves * kBM * lstride);  // [4*halves warps][32][kScrStride]
-  uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 4 * halves * 32 * kScrStride);
+  float* scratch = reinterpret_cast<float*>(slots + a.nslots * kABytes);  // [4 warps][32][kScrStride]
+  uint64_t* full = reinterpret_cast<uint64_t*>(scratch + 4 * 32 * kScrStride);
   uint64_t* empty = full + kBars;
   uint64_t* tfull = empty + kBars;  // kTBufs TMEM buffers
   uint64_t* tempty = tfull + kTBufs;
@@ -404,7 +404,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     }
     for (int b = 0; b < kTBufs; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128 * halves);
+      mbar_init(&tempty[b], 128);
     }
     mbar_init(afull, 1);
     mbar_init(aempty, 1);
@@ -499,17 +499,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   } else {
     // ---------------- epilogue: thread = TMEM lane = query row of the tile
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int ew = warp - 2;       // epilogue warp 0 .. 4*halves-1
-    const int half = ew >> 2;      // which column half of every tile (and which list set) it owns
+    const int ew = warp - 2;       // epilogue warp 0 .. 3
     const int row = quarter * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
     const double pmax = __longlong_as_double(static_cast<long long>(*a.pmax_bits));
     float* scr = scratch + (ew * 32 + lane) * kScrStride;  // this lane's hot-chunk values
-    float* wk0 = lk + (half * kBM + quarter * 32) * lstride;  // this warp's 32 buffers (lane l: + l * lstride)
-    int32_t* wi0 = li + (half * kBM + quarter * 32) * lstride;
-    float* bk = wk0 + lane * lstride;  // this query's buffer
-    int32_t* bi = wi0 + lane * lstride;
-    const int h0 = half * (kBN / 32) / halves, h1 = (half + 1) * (kBN / 32) / halves;  // its chunks
+    // this warp's 32 candidate buffers in the CTA's global scratch area (lane l: + l * wcap)
+    uint2* wb0 = a.gbuf + (static_cast<int64_t>(blockIdx.x) * kBM + quarter * 32) * a.wcap;
+    uint2* gb = wb0 + lane * a.wcap;  // this query's buffer
+    constexpr int h0 = 0, h1 = kBN / 32;
     int buf = 0;
     uint32_t tphase = 0;
     for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
@@ -521,8 +519,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       const double eps = (2 * a.DP + 32) * 2.384185791015625e-7 * (nq_hat + pmax * pmax) * 1.001 + 9.5367431640625e-7;
       const int64_t excl = a.excl != nullptr ? (valid ? a.excl[q] : -1)
                                              : (a.self_offset >= 0 ? q + a.self_offset : -1);
-      // Candidate state: bk/bi[0..cnt) = every point seen so far with v <= win (unsorted).
-      // win = +inf until the first compaction (cnt reaches cap >= kk + 29), then
+      // Candidate state: gb[0..cnt) = every point seen so far with v <= win (unsorted).
+      // win = +inf until the first compaction (cnt reaches wcap >= kk + 29), then
       // W(T~) - n^_q with T~ >= the kk-th smallest D~ seen, so the exact top-kk is inside.
       int cnt = 0;
       bool over = false;
@@ -533,16 +531,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         tc_fence_after();
         const uint32_t tbase = tmem_base + lane_addr + static_cast<uint32_t>(buf * kBN);
         const bool tail = (pt + 1) * kBN > a.np;  // columns past np hold TMA zero fill
-        // one 32-column chunk per iteration; the loop is deliberately not unrolled so
-        // the epilogue (chunk filter + admission + heap code) stays small in the I-cache
-#pragma unroll 1
-        for (int h = h0; h < h1; ++h) {
-          uint32_t r[32];
-          __syncwarp();  // tcgen05.ld is warp-collective; the admission loop diverges
-          tmem_ld32_nw(tbase + h * 32, r);
-          tmem_wait_ld();
+        // One 32-column chunk at a time, two register sets: the TMEM load of the next chunk
+        // is in flight while the current one is filtered (the epilogue warp is alone on its
+        // scheduler, so nothing else hides that latency).
+        auto process = [&](uint32_t (&r)[32], const int ch) {
           {
-            const int ch = h;
             const int64_t j0 = pt * kBN + ch * 32;
             if (tail) {  // NaN: never admitted, ignored by the max
 #pragma unroll
@@ -554,7 +547,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
                 for (int c = 0; c < 32; ++c)
                   a.debug_G[row * 256 + ch * 32 + c] =
                       j0 + c < a.np ? fmaf(-2.0f, __uint_as_float(r[c]), nqf) : 0.0f;
-              continue;
+              return;
             }
             // g_c = q^.p^ - n^_p/2 straight from TMEM; a chunk whose max g is below
             // -win/2 (for every lane) has nothing under the window
@@ -569,14 +562,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
                              fmaxf(fmaxf(__uint_as_float(r[c + 4]), __uint_as_float(r[c + 5])),
                                    fmaxf(__uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]))));
             }
-            if (!__any_sync(0xffffffffu, fmaxf(fmaxf(sm[0], sm[1]), fmaxf(sm[2], sm[3])) >= gthr)) continue;
+            // the four sub-chunk votes back to back (no branch between them)
+            uint32_t hot = 0;
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) hot |= (__any_sync(0xffffffffu, sm[q4] >= gthr) ? 1u : 0u) << q4;
+            if (hot == 0) return;
             // hot chunk: only the sub-chunks some lane needs get a per-lane bit mask, and
             // their v = -2g are parked in this lane's scratch row, so the admission
             // loop visits only the set bits
             uint32_t mask = 0;
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
-              if (!__any_sync(0xffffffffu, sm[q4] >= gthr)) continue;
+              if (((hot >> q4) & 1u) == 0) continue;
               const int c = 8 * q4;
 #pragma unroll
               for (int t = 0; t < 8; ++t) mask |= (__uint_as_float(r[c + t]) >= gthr ? 1u : 0u) << (c + t);
@@ -590,14 +587,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             // admissions: append; a lane whose buffer is full stops with its remaining bits
             // pending, the warp compacts those lanes' buffers one by one, and the lanes go on
             for (;;) {
-              while (mask != 0 && cnt < a.cap) {
+              while (mask != 0 && cnt < a.wcap) {
                 const int c = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const float v = scr[c];
                 const int64_t j = j0 + c;
                 if (!(v <= win) || j == excl) continue;
-                bk[cnt] = v;
-                bi[cnt] = static_cast<int32_t>(j);
+                gb[cnt] = make_uint2(__float_as_uint(v), static_cast<uint32_t>(j));
                 ++cnt;
               }
               uint32_t need = __ballot_sync(0xffffffffu, mask != 0);
@@ -609,12 +605,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
                 const double s_eta = __shfl_sync(0xffffffffu, eta, src);
                 const double s_eps = __shfl_sync(0xffffffffu, eps, src);
                 float nwin;
-                const int nn = compact_candidates(wk0 + src * lstride, wi0 + src * lstride, a.cap, a.kk, s_nqf,
-                                                  s_eta, s_eps, &nwin);
+                const int nn = compact_candidates(wb0 + src * a.wcap, a.wcap, a.kk, s_nqf, s_eta, s_eps, false,
+                                                  &nwin);
                 if (lane == src) {
                   cnt = nn;
                   win = nwin;
-                  if (nn >= a.cap) {  // the window alone fills the buffer: the query is redone exactly
+                  if (nn > a.wcap - 32) {  // the window alone (nearly) fills the buffer: the query is redone exactly
                     over = true;
                     win = -INFINITY;
                     mask = 0;
@@ -623,6 +619,24 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
                 }
               }
             }
+          }
+        };
+        {
+          uint32_t ra[32], rb[32];
+          __syncwarp();  // tcgen05.ld is warp-collective; the admission loop diverges
+          tmem_ld32_nw(tbase + h0 * 32, ra);
+#pragma unroll 1
+          for (int h = h0; h < h1; h += 2) {
+            tmem_wait_ld();
+            __syncwarp();
+            tmem_ld32_nw(tbase + (h + 1) * 32, rb);
+            process(ra, h);
+            tmem_wait_ld();
+            if (h + 2 < h1) {
+              __syncwarp();
+              tmem_ld32_nw(tbase + (h + 2) * 32, ra);
+            }
+            process(rb, h + 1);
           }
         }
         tc_fence_before();
@@ -633,7 +647,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         }
       }
       // candidates = the buffer (the exact top-kk is inside), trimmed once more to the final
-      // window; the exact recheck and selection run in tc_recheck_kernel
+      // window (exact kk-th smallest); the exact recheck and selection run in tc_recheck_kernel
       if (a.debug_G) continue;
       {
         uint32_t need = __ballot_sync(0xffffffffu, valid && !over && cnt > a.kk);
@@ -645,21 +659,22 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           const double s_eps = __shfl_sync(0xffffffffu, eps, src);
           const int s_cnt = __shfl_sync(0xffffffffu, cnt, src);
           float nwin;
-          const int nn = compact_candidates(wk0 + src * lstride, wi0 + src * lstride, s_cnt, a.kk, s_nqf, s_eta,
-                                            s_eps, &nwin);
+          const int nn = compact_candidates(wb0 + src * a.wcap, s_cnt, a.kk, s_nqf, s_eta, s_eps, true, &nwin);
           if (lane == src) cnt = nn;
         }
       }
+      __syncwarp();
       if (!valid) continue;
+      if (cnt > a.cap) over = true;  // more candidates inside the final window than the recheck takes
       if (over) {
         const int32_t slot = atomicAdd(a.overflow, 1);
         a.overflow[1 + slot] = static_cast<int32_t>(q);
-        a.ccount[half * a.nq + q] = -1;
+        a.ccount[q] = -1;
         continue;
       }
-      int32_t* cq = a.cand + static_cast<int64_t>(half) * a.cap * a.nq + q;  // this half's rows
-      for (int t = 0; t < cnt; ++t) cq[t * a.nq] = bi[t];
-      a.ccount[half * a.nq + q] = cnt;
+      int32_t* cq = a.cand + q;
+      for (int t = 0; t < cnt; ++t) cq[t * a.nq] = static_cast<int32_t>(__ldcg(gb + t).y);
+      a.ccount[q] = cnt;
     }
   }
   tc_fence_before();
@@ -828,26 +843,28 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   if (nq <= 0) return cudaSuccess;
   const int KB = (d + 3 + kBK - 1) / kBK;  // + 3 columns for the point-norm split
   const int DP = KB * kBK;
-  const int cap = std::min(kCapMax, ((kk + 29 + 31) / 32) * 32);  // 32 / 64 / 96 / 128: slack >= 29 over kk
-  // 8 epilogue warps (two column halves with separate candidate lists) when both
-  // lists fit next to the operand slots and the recheck's 128-candidate warp
-  auto smem_for = [&](int hv, int nslots) {
-    return static_cast<size_t>(1024) + static_cast<size_t>(nslots) * kABytes +
-           static_cast<size_t>(hv) * (cap + 1) * kBM * 8 + sizeof(float) * 4 * hv * 32 * kScrStride + 256;
+  const int cap = kCapMax;  // candidates per query the recheck takes (rows of `cand`)
+  // working buffer per query: the first wcap points are all admitted, then every compaction
+  // leaves >= kk entries, so the slack wcap - kk sets how often a query compacts
+  const int wcap = kk > 64 ? kWcapMax : (kk > 16 ? 128 : 64);
+  // Two CTAs per SM (the epilogue is latency-bound with one warp per scheduler); each gets
+  // half of the SM's shared memory for its operand stages. FMGP_TC_CTAS=1: one CTA per SM.
+  // With no more query tiles than SMs a second CTA per SM has nothing to run: one CTA, deep stages.
+  const char* cta_env = std::getenv("FMGP_TC_CTAS");
+  const int ctas = (cta_env != nullptr && cta_env[0] == '1') || (nq + kBM - 1) / kBM <= num_sms ? 1 : 2;
+  const size_t smem_cap = ctas == 2 ? (233472 - 2 * 1024) / 2 : 232448;
+  auto smem_for = [&](int nslots) {
+    return static_cast<size_t>(1024) + static_cast<size_t>(nslots) * kABytes + sizeof(float) * 4 * 32 * kScrStride + 256;
   };
-  // Only when the epilogue is the bound (DP == 64: resident query tile, cheap
-  // recheck); for wide rows (KB > 1) the GEMM/TMA side and the doubled recheck dominate.
-  const int halves = (KB == 1 && 2 * cap <= 128 && smem_for(2, 1 + kBStagesRes) <= 232448) ? 2 : 1;
-  // As many operand stages in flight as the candidate lists leave room for
-  // (the TMA round trip from L2 is several MMA k-blocks long): (A, B) k-block
-  // pairs for wide rows, B tiles when the query tile is resident.
-  // FMGP_TC_STAGES overrides (A/B checks).
+  // As many operand stages in flight as fit (the TMA round trip from L2 is several MMA
+  // k-blocks long): (A, B) k-block pairs for wide rows, B tiles when the query tile is
+  // resident. FMGP_TC_STAGES overrides (A/B checks).
   const char* st_env = std::getenv("FMGP_TC_STAGES");
   const int smin = KB > 1 ? kStages : kBStagesRes, smax = KB > 1 ? kStagesMax : kBStagesResMax;
   const int want = st_env != nullptr ? std::atoi(st_env) : smax;
   int stages = smin;
   for (int st = std::min(std::max(want, smin), smax); st >= smin; --st)
-    if (smem_for(halves, KB > 1 ? 2 * st : 1 + st) <= 232448) {
+    if (smem_for(KB > 1 ? 2 * st : 1 + st) <= smem_cap) {
       stages = st;
       break;
     }
@@ -856,14 +873,18 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   float* qn = nullptr;
   double* sums = nullptr;
   int32_t *cand = nullptr, *ccount = nullptr, *ovf = nullptr;
+  uint2* gbuf = nullptr;
+  const int64_t nqt = (nq + kBM - 1) / kBM;
+  const int grid = debug_G ? 1 : static_cast<int>(std::min<int64_t>(nqt, static_cast<int64_t>(num_sms) * ctas));
   unsigned long long* bits = nullptr;  // [0] maxabs, [1] pmax, [2] max ||p - mu||^2
   cudaError_t err = cudaMallocAsync(&Qh, sizeof(__half) * nq * DP, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&Ph, sizeof(__half) * np * DP, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&qn, sizeof(float) * nq, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&sums, sizeof(double) * d, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&bits, sizeof(unsigned long long) * 3, s);
-  if (err == cudaSuccess) err = cudaMallocAsync(&cand, sizeof(int32_t) * nq * cap * halves, s);
-  if (err == cudaSuccess) err = cudaMallocAsync(&ccount, sizeof(int32_t) * nq * halves, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&cand, sizeof(int32_t) * nq * cap, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&ccount, sizeof(int32_t) * nq, s);
+  if (err == cudaSuccess) err = cudaMallocAsync(&gbuf, sizeof(uint2) * static_cast<size_t>(grid) * kBM * wcap, s);
   if (err == cudaSuccess) err = cudaMallocAsync(&ovf, sizeof(int32_t) * (nq + 1), s);
   if (err != cudaSuccess) return err;
   cudaMemsetAsync(sums, 0, sizeof(double) * d, s);
@@ -890,7 +911,8 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.KB = KB;
   a.kk = kk;
   a.cap = cap;
-  a.halves = halves;
+  a.wcap = wcap;
+  a.gbuf = gbuf;
   a.stages = stages;
   a.nslots = nslots;
   a.self_offset = self_offset;
@@ -912,19 +934,17 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   a.maxabs_bits = bits;
   a.pmax_bits = bits + 1;
   a.debug_G = debug_G;
-  const size_t smem = smem_for(halves, nslots);
+  const size_t smem = smem_for(nslots);
   err = cudaFuncSetAttribute(knn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
-  const int64_t nqt = (nq + kBM - 1) / kBM;
-  const int grid = static_cast<int>(nqt < num_sms ? nqt : num_sms);
-  knn_tc_kernel<<<debug_G ? 1 : grid, 64 + 128 * halves, smem, s>>>(mq, mp, a);
+  knn_tc_kernel<<<grid, kMaxThreads, smem, s>>>(mq, mp, a);
   note_launches(1);
   err = cudaGetLastError();
   if (err == cudaSuccess && debug_G == nullptr) {
     const int64_t blocks = (nq + kRecheckWarps - 1) / kRecheckWarps;
     tc_recheck_kernel<<<static_cast<unsigned>(blocks < num_sms * 16 ? blocks : num_sms * 16), kRecheckWarps * 32, 0,
                         s>>>(
-        Q, P, d, nq, kk, cand, ccount, halves, cap, with_self, self_offset, out, out_d);
+        Q, P, d, nq, kk, cand, ccount, 1, cap, with_self, self_offset, out, out_d);
     note_launches(1);
     err = cudaGetLastError();
   }
@@ -934,8 +954,8 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
     err = cudaMemcpyAsync(&novf, ovf, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     if (err == cudaSuccess) err = cudaStreamSynchronize(s);
     if (err == cudaSuccess && std::getenv("FMGP_TC_STATS") != nullptr)
-      std::fprintf(stderr, "knn_tc: nq=%lld np=%lld kk=%d cap=%d overflowed=%d\n", static_cast<long long>(nq),
-                   static_cast<long long>(np), kk, cap, novf);
+      std::fprintf(stderr, "knn_tc: nq=%lld np=%lld kk=%d wcap=%d ctas/SM=%d stages=%d overflowed=%d\n",
+                   static_cast<long long>(nq), static_cast<long long>(np), kk, wcap, ctas, stages, novf);
     if (err == cudaSuccess && novf > 0) {
       double *Qg = nullptr, *rd = nullptr;
       int32_t *eg = nullptr, *rows = nullptr;
@@ -957,7 +977,7 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   }
   for (void* p : {static_cast<void*>(Qh), static_cast<void*>(Ph), static_cast<void*>(qn),
                   static_cast<void*>(sums), static_cast<void*>(bits), static_cast<void*>(cand), static_cast<void*>(ccount),
-                  static_cast<void*>(ovf)})
+                  static_cast<void*>(ovf), static_cast<void*>(gbuf)})
     cudaFreeAsync(p, s);
   return err;
 }
