@@ -168,14 +168,21 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
                             (static_cast<uint32_t>(kBM >> 4) << 24);
 
-__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_ld64_nw(uint32_t taddr, uint32_t (&r)[64]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, "
+      "%32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, "
+      "%48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
         "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]),
+        "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]),
+        "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+        "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]),
+        "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -507,7 +514,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     // this warp's 32 candidate buffers in the CTA's global scratch area (lane l: + l * wcap)
     uint2* wb0 = a.gbuf + (static_cast<int64_t>(blockIdx.x) * kBM + quarter * 32) * a.wcap;
     uint2* gb = wb0 + lane * a.wcap;  // this query's buffer
-    constexpr int h0 = 0, h1 = kBN / 32;
     int buf = 0;
     uint32_t tphase = 0;
     for (int64_t qt = blockIdx.x; qt < nqt; qt += gridDim.x) {
@@ -531,113 +537,98 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         tc_fence_after();
         const uint32_t tbase = tmem_base + lane_addr + static_cast<uint32_t>(buf * kBN);
         const bool tail = (pt + 1) * kBN > a.np;  // columns past np hold TMA zero fill
-        // One 32-column chunk at a time, two register sets: the TMEM load of the next chunk
-        // is in flight while the current one is filtered (the epilogue warp is alone on its
-        // scheduler, so nothing else hides that latency).
-        auto process = [&](uint32_t (&r)[32], const int ch) {
-          {
-            const int64_t j0 = pt * kBN + ch * 32;
-            if (tail) {  // NaN: never admitted, ignored by the max
+        // 64 columns per step (tcgen05.ld x64): the filter of a step is one dependent chain
+        // (load -> eight 8-column maxima -> eight votes -> branch) and the epilogue warp has
+        // at most one other warp on its scheduler to hide it, so fewer, wider steps.
+        // Admissions of one 32-column half: per-lane bit mask of the hot sub-chunks, their
+        // v = -2g parked in this lane's scratch row, so the append loop visits only set bits;
+        // a lane whose buffer is full stops with its remaining bits pending, the warp
+        // compacts those lanes' buffers one by one, and the lanes go on.
+        auto admit_half = [&](uint32_t (&r)[64], const int off, const uint32_t hot4, const int64_t j0,
+                              const float gthr) {
+          uint32_t mask = 0;
 #pragma unroll
-              for (int c = 0; c < 32; ++c)
-                if (j0 + c >= a.np) r[c] = 0x7fffffffu;
+          for (int q4 = 0; q4 < 4; ++q4) {
+            if (((hot4 >> q4) & 1u) == 0) continue;
+            const int c = 8 * q4, o = off + c;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) mask |= (__uint_as_float(r[o + t]) >= gthr ? 1u : 0u) << (c + t);
+            *reinterpret_cast<float4*>(scr + c) =
+                make_float4(-2.0f * __uint_as_float(r[o]), -2.0f * __uint_as_float(r[o + 1]),
+                            -2.0f * __uint_as_float(r[o + 2]), -2.0f * __uint_as_float(r[o + 3]));
+            *reinterpret_cast<float4*>(scr + c + 4) =
+                make_float4(-2.0f * __uint_as_float(r[o + 4]), -2.0f * __uint_as_float(r[o + 5]),
+                            -2.0f * __uint_as_float(r[o + 6]), -2.0f * __uint_as_float(r[o + 7]));
+          }
+          for (;;) {
+            while (mask != 0 && cnt < a.wcap) {
+              const int c = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const float v = scr[c];
+              const int64_t j = j0 + c;
+              if (!(v <= win) || j == excl) continue;
+              gb[cnt] = make_uint2(__float_as_uint(v), static_cast<uint32_t>(j));
+              ++cnt;
             }
-            if (a.debug_G) {
-              if (qt == 0)
-                for (int c = 0; c < 32; ++c)
-                  a.debug_G[row * 256 + ch * 32 + c] =
-                      j0 + c < a.np ? fmaf(-2.0f, __uint_as_float(r[c]), nqf) : 0.0f;
-              return;
-            }
-            // g_c = q^.p^ - n^_p/2 straight from TMEM; a chunk whose max g is below
-            // -win/2 (for every lane) has nothing under the window
-            const float gthr = -0.5f * win;  // v <= win  <=>  g >= -win/2 (exact scaling)
-            // per-lane maxima of the four 8-column sub-chunks
-            float sm[4];
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              const int c = 8 * q4;
-              sm[q4] = fmaxf(fmaxf(fmaxf(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
-                                   fmaxf(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]))),
-                             fmaxf(fmaxf(__uint_as_float(r[c + 4]), __uint_as_float(r[c + 5])),
-                                   fmaxf(__uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]))));
-            }
-            // the four sub-chunk votes back to back (no branch between them)
-            uint32_t hot = 0;
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) hot |= (__any_sync(0xffffffffu, sm[q4] >= gthr) ? 1u : 0u) << q4;
-            if (hot == 0) return;
-            // hot chunk: only the sub-chunks some lane needs get a per-lane bit mask, and
-            // their v = -2g are parked in this lane's scratch row, so the admission
-            // loop visits only the set bits
-            uint32_t mask = 0;
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              if (((hot >> q4) & 1u) == 0) continue;
-              const int c = 8 * q4;
-#pragma unroll
-              for (int t = 0; t < 8; ++t) mask |= (__uint_as_float(r[c + t]) >= gthr ? 1u : 0u) << (c + t);
-              *reinterpret_cast<float4*>(scr + c) =
-                  make_float4(-2.0f * __uint_as_float(r[c]), -2.0f * __uint_as_float(r[c + 1]),
-                              -2.0f * __uint_as_float(r[c + 2]), -2.0f * __uint_as_float(r[c + 3]));
-              *reinterpret_cast<float4*>(scr + c + 4) =
-                  make_float4(-2.0f * __uint_as_float(r[c + 4]), -2.0f * __uint_as_float(r[c + 5]),
-                              -2.0f * __uint_as_float(r[c + 6]), -2.0f * __uint_as_float(r[c + 7]));
-            }
-            // admissions: append; a lane whose buffer is full stops with its remaining bits
-            // pending, the warp compacts those lanes' buffers one by one, and the lanes go on
-            for (;;) {
-              while (mask != 0 && cnt < a.wcap) {
-                const int c = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const float v = scr[c];
-                const int64_t j = j0 + c;
-                if (!(v <= win) || j == excl) continue;
-                gb[cnt] = make_uint2(__float_as_uint(v), static_cast<uint32_t>(j));
-                ++cnt;
-              }
-              uint32_t need = __ballot_sync(0xffffffffu, mask != 0);
-              if (need == 0) break;
-              while (need != 0) {
-                const int src = __ffs(need) - 1;
-                need &= need - 1;
-                const float s_nqf = __shfl_sync(0xffffffffu, nqf, src);
-                const double s_eta = __shfl_sync(0xffffffffu, eta, src);
-                const double s_eps = __shfl_sync(0xffffffffu, eps, src);
-                float nwin;
-                const int nn = compact_candidates(wb0 + src * a.wcap, a.wcap, a.kk, s_nqf, s_eta, s_eps, false,
-                                                  &nwin);
-                if (lane == src) {
-                  cnt = nn;
-                  win = nwin;
-                  if (nn > a.wcap - 32) {  // the window alone (nearly) fills the buffer: the query is redone exactly
-                    over = true;
-                    win = -INFINITY;
-                    mask = 0;
-                    cnt = 0;
-                  }
+            uint32_t need = __ballot_sync(0xffffffffu, mask != 0);
+            if (need == 0) break;
+            while (need != 0) {
+              const int src = __ffs(need) - 1;
+              need &= need - 1;
+              const float s_nqf = __shfl_sync(0xffffffffu, nqf, src);
+              const double s_eta = __shfl_sync(0xffffffffu, eta, src);
+              const double s_eps = __shfl_sync(0xffffffffu, eps, src);
+              float nwin;
+              const int nn = compact_candidates(wb0 + src * a.wcap, a.wcap, a.kk, s_nqf, s_eta, s_eps, false, &nwin);
+              if (lane == src) {
+                cnt = nn;
+                win = nwin;
+                if (nn > a.wcap - 32) {  // the window alone (nearly) fills the buffer: the query is redone exactly
+                  over = true;
+                  win = -INFINITY;
+                  mask = 0;
+                  cnt = 0;
                 }
               }
             }
           }
         };
-        {
-          uint32_t ra[32], rb[32];
-          __syncwarp();  // tcgen05.ld is warp-collective; the admission loop diverges
-          tmem_ld32_nw(tbase + h0 * 32, ra);
 #pragma unroll 1
-          for (int h = h0; h < h1; h += 2) {
-            tmem_wait_ld();
-            __syncwarp();
-            tmem_ld32_nw(tbase + (h + 1) * 32, rb);
-            process(ra, h);
-            tmem_wait_ld();
-            if (h + 2 < h1) {
-              __syncwarp();
-              tmem_ld32_nw(tbase + (h + 2) * 32, ra);
-            }
-            process(rb, h + 1);
+        for (int h = 0; h < kBN / 64; ++h) {
+          uint32_t r[64];
+          __syncwarp();  // tcgen05.ld is warp-collective; the admission loop diverges
+          tmem_ld64_nw(tbase + h * 64, r);
+          tmem_wait_ld();
+          const int64_t j0 = pt * kBN + h * 64;
+          if (tail) {  // NaN: never admitted, ignored by the max
+#pragma unroll
+            for (int c = 0; c < 64; ++c)
+              if (j0 + c >= a.np) r[c] = 0x7fffffffu;
           }
+          if (a.debug_G) {
+            if (qt == 0)
+              for (int c = 0; c < 64; ++c)
+                a.debug_G[row * 256 + h * 64 + c] = j0 + c < a.np ? fmaf(-2.0f, __uint_as_float(r[c]), nqf) : 0.0f;
+            continue;
+          }
+          // g_c = q^.p^ - n^_p/2 straight from TMEM; an 8-column sub-chunk whose max g is
+          // below -win/2 (for every lane) has nothing under the window
+          const float gthr = -0.5f * win;  // v <= win  <=>  g >= -win/2 (exact scaling)
+          uint32_t hot = 0;
+#pragma unroll
+          for (int q8 = 0; q8 < 8; ++q8) {
+            const int c = 8 * q8;
+            const float m8 = fmaxf(fmaxf(fmaxf(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
+                                         fmaxf(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]))),
+                                   fmaxf(fmaxf(__uint_as_float(r[c + 4]), __uint_as_float(r[c + 5])),
+                                         fmaxf(__uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]))));
+            hot |= (__any_sync(0xffffffffu, m8 >= gthr) ? 1u : 0u) << q8;
+          }
+          if (hot == 0) continue;
+          if ((hot & 15u) != 0) admit_half(r, 0, hot & 15u, j0, gthr);
+          // the second half sees the bound the first half's compactions may have tightened
+          // through `win` only at the append (v <= win); gthr stays the looser, still valid bound
+          if ((hot >> 4) != 0) admit_half(r, 32, hot >> 4, j0 + 32, gthr);
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
