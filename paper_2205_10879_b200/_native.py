@@ -1,16 +1,17 @@
 """ctypes binding of the C ABI in include/fmgp_b200.h (libfmgp_b200.so).
 
-The library is loaded from this package's lib/ directory only; if it is
-missing the import fails loudly — there is no Python or CPU fallback for any
+The library is loaded from this package's lib/ directory (or the A/B variant
+build named by FMGP_LIB) only; if it is missing the import fails loudly — there is no Python or CPU fallback for any
 compute entry point.
 """
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_DIR = Path(__file__).resolve().parent / "lib"
-LIB_PATH = LIB_DIR / "libfmgp_b200.so"
+LIB_PATH = Path(os.environ["FMGP_LIB"]) if os.environ.get("FMGP_LIB") else LIB_DIR / "libfmgp_b200.so"  # FMGP_LIB: an A/B variant build
 
 FMGP_OK, FMGP_EINVAL, FMGP_ENUMERIC, FMGP_ECUDA = 0, 1, 2, 3
 

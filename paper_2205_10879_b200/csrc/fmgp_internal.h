@@ -155,7 +155,7 @@ cudaError_t predict_grid(const double* X, int64_t n, int d, const int32_t* S, co
 namespace fmgp {
 
 // DMMA-blocked variant for the small-d shapes (d in {2, 3}, k in {30, 50},
-// m = 1, closed-form kernels); FMGP_SOLVE_DM selects it.
+// m = 1, closed-form kernels): the default there; FMGP_SOLVE_DM=0 falls back to the register solve.
 bool fused_solve_dm_supported(int k, int d, int m, const KParams& kp);
 cudaError_t fused_solve_dm(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows,
                            int64_t row_begin, int k, const KParams& kp, double* C, unsigned long long* fail_min,

@@ -404,11 +404,13 @@ cudaError_t fused_solve(const double* X, const double* Y, int d, int m, const in
         return e;
       }
     }
+    // default: the DMMA-blocked solve where its shape is compiled in; FMGP_SOLVE_2D=1 / FMGP_SOLVE_DM=0
+    // select the 2-D cyclic / row-per-lane register solves (A/B and the parity tests of all three)
     const cudaError_t e =
-        fused_solve_dm_supported(k, d, m, kp)
-            ? fused_solve_dm(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order)
-            : (fused_solve_2d_supported(k, d, m, kp)
-                   ? fused_solve_2d(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order)
+        fused_solve_2d_supported(k, d, m, kp)
+            ? fused_solve_2d(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order)
+            : (fused_solve_dm_supported(k, d, m, kp)
+                   ? fused_solve_dm(X, Y, d, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order)
                    : fused_solve_reg(X, Y, d, m, S, nrows, row_begin, k, kp, C, fail_min, num_sms, stream, order));
     if (order != nullptr) cudaFreeAsync(order, stream);
     return e;

@@ -311,10 +311,9 @@ cudaError_t launch_2d_kind(const double* X, const double* Y, const int32_t* S, i
 }  // namespace
 
 bool fused_solve_2d_supported(int k, int d, int m, const KParams& kp) {
-  static const bool on = [] {  // FMGP_SOLVE_2D=1 selects it (A/B against the row-per-lane register solve)
-    const char* e = std::getenv("FMGP_SOLVE_2D");
-    return e != nullptr && e[0] == '1';
-  }();
+  // FMGP_SOLVE_2D=1 selects it (A/B against the other fused solves; read per call)
+  const char* e = std::getenv("FMGP_SOLVE_2D");
+  const bool on = e != nullptr && e[0] == '1';
   return on && m == 1 && (d == 2 || d == 3) && (k == 50 || k == 30) && (kp.kind == 1 || kp.nu_code <= 2);
 }
 

@@ -125,6 +125,9 @@ __device__ __forceinline__ bool dm_factor(double* A, const double* xs, const KPa
   bool bad = false;
 #pragma unroll
   for (int J = 0; J < NBC; ++J) {
+#if FMGP_DM_SYNCJ
+    __syncthreads();
+#endif
     double acc[NBR][2];
     // 1. -K(I, J): full tiles evaluated here, the rest from the packed copy
     double wc[2][D];
@@ -284,9 +287,21 @@ __device__ __forceinline__ void dm_back(const double* A, double dv0, double dv1,
   if (lane + 32 < K) Crow[lane + 32] = y1;
 }
 
-constexpr int kDmWarps = 4;
+#ifndef FMGP_DM_WARPS  // warps per CTA; with the per-row barrier below the CTA runs its rows in lockstep
+#define FMGP_DM_WARPS 16
+#endif
+#ifndef FMGP_DM_PP
+#define FMGP_DM_PP 3
+#endif
+#ifndef FMGP_DM_LOCKSTEP
+#define FMGP_DM_LOCKSTEP 1
+#endif
+#ifndef FMGP_DM_SYNCJ  // 1: the CTA's warps also meet at every block column of the factorisation
+#define FMGP_DM_SYNCJ 0
+#endif
+constexpr int kDmWarps = FMGP_DM_WARPS;
 #ifndef FMGP_DM_MINB
-#define FMGP_DM_MINB 4
+#define FMGP_DM_MINB 1
 #endif
 
 template <int K, int D, int KF>
@@ -311,30 +326,75 @@ solve_dm_kernel(const double* __restrict__ X, const double* __restrict__ Y, cons
   kn.s2 = -kp.s2;
   kn.diag = -kp.diag;
   const double cs = kernel_scale_build<KF>(kp);
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * warps; base < nrows;
-       base += static_cast<int64_t>(gridDim.x) * warps) {
-    __syncthreads();  // the CTA's warps start each row together (instruction-cache locality)
-    const int64_t it = base + warp;
-    if (it >= nrows) continue;
-    const int64_t r = order != nullptr ? order[it] : it;
+  // Software pipeline over the warp's rows: the gathers of row i + 1 (S row -> X rows, Y) are
+  // issued into registers while row i is solved — the S indices at the top of row i, the
+  // coordinates just before its backward solve, where few registers are live — so the
+  // dependent order -> S -> X chain (three DRAM/L2 round trips) is off the critical path.
+  constexpr int NX = (K * D + kWarp - 1) / kWarp;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * warps;
+  const int64_t it0 = static_cast<int64_t>(blockIdx.x) * warps + warp;
+  auto row_of = [&](int64_t it) -> int64_t {
+    if (it >= nrows) return -1;
+    return order != nullptr ? order[it] : it;
+  };
+  double xn[NX], yn0 = 0.0, yn1 = 0.0;
+  auto gather_xy = [&]() {  // from the indices staged in sr
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      const int e = lane + i * kWarp;
+      const int q = e / D, c = e - q * D;
+      xn[i] = e < K * D ? X[static_cast<int64_t>(sr[q]) * D + c] : 0.0;
+    }
+    yn0 = lane < K ? Y[sr[lane < K ? lane : 0]] : 0.0;
+    yn1 = lane + 32 < K ? Y[sr[lane + 32 < K ? lane + 32 : 0]] : 0.0;
+  };
+  int64_t r = row_of(it0), rn = row_of(it0 + stride);
+  if (r >= 0) {
     for (int q = lane; q < K; q += kWarp) sr[q] = S[r * K + q];
     __syncwarp();
-    for (int e = lane; e < K * D; e += kWarp) {
-      const int q = e / D, c = e - q * D;
-      xs[e] = X[static_cast<int64_t>(sr[q]) * D + c];
+    gather_xy();
+  }
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * warps; base < nrows; base += stride) {
+#if FMGP_DM_LOCKSTEP
+    __syncthreads();  // the CTA's warps start each row together (instruction-cache locality)
+#endif
+    const int64_t it = base + warp;
+#if FMGP_DM_SYNCJ
+    const bool active = it < nrows;  // a warp without a row still meets the CTA's barriers
+#else
+    if (it >= nrows) continue;
+    constexpr bool active = true;
+#endif
+    const int64_t rnn = row_of(it + 2 * stride);
+    int32_t s0n = 0, s1n = 0;
+    if (rn >= 0) {
+      if (lane < K) s0n = S[rn * K + lane];
+      if (lane + 32 < K) s1n = S[rn * K + lane + 32];
     }
-    // y of the neighbourhood, parked in the RHS row's slack until the build negates it in place
-    double yl0 = lane < K ? Y[sr[lane < K ? lane : 0]] : 0.0;
-    double yl1 = lane + 32 < K ? Y[sr[lane + 32 < K ? lane + 32 : 0]] : 0.0;
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+      if (lane + i * kWarp < K * D) xs[lane + i * kWarp] = xn[i];
+    const double yl0 = yn0, yl1 = yn1;
     __syncwarp();
     bool ok = false;
     double dv0 = 0.0, dv1 = 0.0;
-    for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
+#pragma unroll 1
+    for (int attempt = 0; attempt < 4; ++attempt) {
+      const bool need = active && !ok;
+#if FMGP_DM_SYNCJ
+      if (!__syncthreads_or(need ? 1 : 0)) break;
+      if (!need) {  // keep the barrier count of dm_factor
+        for (int J = 0; J < Sh::kNBC; ++J) __syncthreads();
+        continue;
+      }
+#else
+      if (!need) break;
+#endif
       // build: irregular pairs, diagonal, RHS
       {
         constexpr int NI = Sh::kNirr;
         constexpr int STEPS = (NI + kWarp - 1) / kWarp;
-        constexpr int PP = 3;  // pairs in flight per lane (independent sqrt/exp chains)
+        constexpr int PP = FMGP_DM_PP;  // pairs in flight per lane (independent sqrt/exp chains)
 #pragma unroll
         for (int s0 = 0; s0 < STEPS; s0 += PP) {
           uint32_t tw[PP];
@@ -369,13 +429,23 @@ solve_dm_kernel(const double* __restrict__ X, const double* __restrict__ Y, cons
       ok = dm_factor<K, D, KF>(A, xs, kn, cs, s_exp, lane, dv0, dv1);
       __syncwarp();
     }
-    if (!ok) {
+    // the next row's coordinates and responses: in flight during the backward solve
+    if (rn >= 0) {
+      if (lane < K) sr[lane] = s0n;
+      if (lane + 32 < K) sr[lane + 32] = s1n;
+      __syncwarp();
+      gather_xy();
+    }
+    if (!active) {
+    } else if (!ok) {
       if (lane == 0) atomicMin(fail_min, static_cast<unsigned long long>(row_begin + r));
       __syncwarp();
-      continue;
+    } else {
+      dm_back<K>(A, dv0, dv1, C + r * K, lane);
+      __syncwarp();
     }
-    dm_back<K>(A, dv0, dv1, C + r * K, lane);
-    __syncwarp();
+    r = rn;
+    rn = rnn;
   }
 }
 
@@ -415,8 +485,8 @@ cudaError_t launch_dm_kind(const double* X, const double* Y, const int32_t* S, i
 }  // namespace
 
 bool fused_solve_dm_supported(int k, int d, int m, const KParams& kp) {
-  const char* e = std::getenv("FMGP_SOLVE_DM");  // read per call: A/B in one process
-  const bool on = e != nullptr && e[0] == '1';
+  const char* e = std::getenv("FMGP_SOLVE_DM");  // read per call: A/B in one process; 0 = register solve
+  const bool on = !(e != nullptr && e[0] == '0');
   return on && m == 1 && (d == 2 || d == 3) && (k == 50 || k == 30) && (kp.kind == 1 || kp.nu_code <= 2);
 }
 
