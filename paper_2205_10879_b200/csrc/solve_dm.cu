@@ -111,6 +111,17 @@ __device__ __forceinline__ double dm_pair(const double (&u)[D], const double (&w
   return kernel_from_sq_build<KF>(acc, cs, kn, tab);
 }
 
+// 1/sqrt(x) for a pivot x > 0: MUFU seed (~2^-22) and ONE third-order step
+// y (1 + e/2 + 3 e^2/8), e = 1 - x y^2 (error ~ e^3: below rounding), four
+// dependent FP64 operations instead of the six of two Newton steps — the
+// pivot chain is the serial part of the panel factorisation.
+__device__ __forceinline__ double rsqrt_pivot3(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-(x * y), y, 1.0);
+  return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+
 __device__ __forceinline__ int dm_row(int r, int K) { return r < K ? dm_ro(r) : dm_ro(K); }
 
 // The blocked left-looking sweep (file header). Returns false iff some pivot
@@ -195,12 +206,15 @@ __device__ __forceinline__ bool dm_factor(double* A, const double* xs, const KPa
         }
       }
     }
+    // The pivot of column c + 1 is taken from its owner lane right after column c is scaled (on that
+    // lane the update of its own diagonal entry is la * la, no shuffle needed), so the next
+    // shuffle -> rsqrt chain runs under the rest of column c's updates.
+    double piv = -__shfl_sync(0xffffffffu, xa[0], 0);
 #pragma unroll
     for (int c = 0; c < kMaxNc; ++c) {
       if (c < nc) {
-        const double piv = -__shfl_sync(0xffffffffu, xa[c], c);
         bad |= !(piv > 0.0);
-        const double inv = rsqrt_pivot(piv);
+        const double inv = rsqrt_pivot3(piv);
         const int col = 8 * J + c;
         if (col < 32) {
           if (lane == col) dv0 = inv;
@@ -214,6 +228,7 @@ __device__ __forceinline__ bool dm_factor(double* A, const double* xs, const KPa
           lb = xb[c] * -inv;
           xb[c] = lb;
         }
+        if (c + 1 < nc) piv = -__shfl_sync(0xffffffffu, fma(la, la, xa[c + 1 < kMaxNc ? c + 1 : c]), c + 1);
 #pragma unroll
         for (int c2 = c + 1; c2 < kMaxNc; ++c2) {
           if (c2 < nc) {
