@@ -116,12 +116,74 @@ int predict_device_impl(const double* X, const int32_t* S, const double* C, int6
   return FMGP_OK;
 }
 
+// Host-buffer batches that take the chunked, device-checked path of replica_predict_host:
+// the cell-grid predict (d <= 3) from 65536 test points up.
+bool predict_pipelined(const fmgp_model* mdl, int64_t nz) {
+  return mdl->d <= 3 && nz >= 65536 && !knn_force_brute();
+}
+
 // One replica's share of a host-buffer predict: H2D of the test points, the
 // walk / 1-NN + gather-kernel-dot, D2H of the means (and 1-NN indices).
 int replica_predict_host(const fmgp_model* mdl, const fmgp_model_replica& r, const double* Z, int64_t nz, double* out,
                          int32_t* nn_out) {
   if (nz <= 0) return FMGP_OK;
   FMGP_CUDA(cudaSetDevice(r.device));
+  if (predict_pipelined(mdl, nz)) {
+    // Large low-d batches go through in chunks on three streams: the H2D copy of chunk i + 1 and
+    // the D2H copy of chunk i - 1 overlap chunk i's kernels. The finiteness check of Z (done by the
+    // caller on the host for small batches) runs on the device copy instead of a host scan of the
+    // whole batch: non-finite coordinates are counted and zeroed in the device copy (so the cell
+    // sort and the walk run on valid points), and a non-zero count becomes the error return after
+    // the final synchronise. Per-point results do not depend on the chunking.
+    constexpr int kStreams = 3;
+    const int64_t chunk = std::max<int64_t>(262144, (nz + 7) / 8);
+    const int nchunks = static_cast<int>((nz + chunk - 1) / chunk);
+    Stream st[kStreams];
+    for (auto& q : st) FMGP_CUDA(q.create());
+    DevBuf<double> dZ, dO;
+    DevBuf<int32_t> dN;
+    DevBuf<unsigned int> bad;
+    FMGP_CUDA(dZ.alloc(static_cast<size_t>(nz) * mdl->d, st[0].s));
+    FMGP_CUDA(dO.alloc(static_cast<size_t>(nz) * mdl->m, st[0].s));
+    if (nn_out) FMGP_CUDA(dN.alloc(static_cast<size_t>(nz), st[0].s));
+    FMGP_CUDA(bad.alloc(static_cast<size_t>(nchunks), st[0].s));
+    cudaEvent_t ready = nullptr;
+    FMGP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    FMGP_CUDA(cudaEventRecord(ready, st[0].s));
+    for (int q = 1; q < kStreams; ++q) FMGP_CUDA(cudaStreamWaitEvent(st[q].s, ready, 0));
+    const int sms = num_sms_current();
+    int rc = FMGP_OK;
+    for (int c = 0; c < nchunks && rc == FMGP_OK; ++c) {
+      cudaStream_t q = st[c % kStreams].s;
+      const int64_t b = c * chunk, e = std::min<int64_t>(nz, b + chunk);
+      double* z = dZ.p + b * mdl->d;
+      cudaError_t ce = cudaMemcpyAsync(z, Z + b * mdl->d, sizeof(double) * (e - b) * mdl->d, cudaMemcpyHostToDevice, q);
+      if (ce == cudaSuccess) ce = fmgp::nonfinite_zero_launch(z, (e - b) * mdl->d, bad.p + c, sms, q);
+      if (ce != cudaSuccess) {
+        rc = cuda_fail(ce, "fmgp_model_predict");
+        break;
+      }
+      rc = predict_device_impl(r.X, r.S, r.C, mdl->n, mdl->d, mdl->k, mdl->m, mdl->kp, r.mo, z, e - b,
+                               dO.p + b * mdl->m, nn_out ? dN.p + b : nullptr, q, r.grid);
+      if (rc != FMGP_OK) break;
+      ce = cudaMemcpyAsync(out + b * mdl->m, dO.p + b * mdl->m, sizeof(double) * (e - b) * mdl->m,
+                           cudaMemcpyDeviceToHost, q);
+      if (ce == cudaSuccess && nn_out)
+        ce = cudaMemcpyAsync(nn_out + b, dN.p + b, sizeof(int32_t) * (e - b), cudaMemcpyDeviceToHost, q);
+      if (ce != cudaSuccess) rc = cuda_fail(ce, "fmgp_model_predict");
+    }
+    std::vector<unsigned int> hbad(static_cast<size_t>(nchunks), 0u);
+    for (auto& q : st) {
+      const cudaError_t ce = cudaStreamSynchronize(q.s);
+      if (ce != cudaSuccess && rc == FMGP_OK) rc = cuda_fail(ce, "fmgp_model_predict");
+    }
+    cudaEventDestroy(ready);
+    if (rc != FMGP_OK) return rc;
+    FMGP_CUDA(cudaMemcpy(hbad.data(), bad.p, sizeof(unsigned int) * nchunks, cudaMemcpyDeviceToHost));
+    for (unsigned int v : hbad)
+      if (v != 0) return fail(FMGP_EINVAL, "fast_predict: non-finite test point");
+    return FMGP_OK;
+  }
   Stream st;
   FMGP_CUDA(st.create());
   DevBuf<double> dZ, dO;
@@ -801,9 +863,11 @@ int fmgp_model_predict(const fmgp_model* mdl, const double* Z, int64_t nz, doubl
   if (nz <= 0) return FMGP_OK;
   // a test point must have a nearest training point (the reference returns -1
   // from nearest_training_point for a NaN query and indexes with it)
-  if (!all_finite(Z, nz * mdl->d)) return fail(FMGP_EINVAL, "fast_predict: non-finite test point");
-  DeviceGuard dg;
   const int g = static_cast<int>(mdl->reps.size());
+  const int64_t per_rep = (g == 1 || nz < 4096) ? nz : (nz + g - 1) / g;
+  if (!predict_pipelined(mdl, per_rep) && !all_finite(Z, nz * mdl->d))  // else: checked on the device copy
+    return fail(FMGP_EINVAL, "fast_predict: non-finite test point");
+  DeviceGuard dg;
   // small batches (e.g. fast_predict_one) stay on one replica
   if (g == 1 || nz < 4096) return replica_predict_host(mdl, mdl->reps[0], Z, nz, out, nn_out);
   // test points split contiguously over the replicas (one host thread each)

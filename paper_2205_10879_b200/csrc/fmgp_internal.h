@@ -48,6 +48,8 @@ cudaError_t sqrt_inplace_launch(double* v, int64_t n, cudaStream_t stream);
 cudaError_t self_rows_launch(int32_t* S, int64_t nrows, int64_t row_begin, cudaStream_t stream);
 cudaError_t nonfinite_count_launch(const double* v, int64_t n, unsigned int* count, int num_sms,
                                    cudaStream_t stream);
+// ... and replace them by 0 in place (v is the caller's own device copy).
+cudaError_t nonfinite_zero_launch(double* v, int64_t n, unsigned int* count, int num_sms, cudaStream_t stream);
 cudaError_t distances_launch(const double* P, int d, const double* q, const int32_t* idx, int64_t cnt, double* out,
                              cudaStream_t stream);
 

@@ -152,7 +152,9 @@ __global__ void grid_params_kernel(const unsigned long long* __restrict__ mm, in
 
 __device__ __forceinline__ int cell_coord(double x, double lo, double inv_h, int G) {
   double f = floor(__dmul_rn(__dsub_rn(x, lo), inv_h));
-  int c = f < 0.0 ? 0 : (f >= static_cast<double>(G) ? G - 1 : static_cast<int>(f));
+  // !(f >= 0) also takes NaN to cell 0 (a NaN coordinate reaches here on the device-pointer
+  // entry points; the query kernels give such a point no neighbour)
+  int c = !(f >= 0.0) ? 0 : (f >= static_cast<double>(G) ? G - 1 : static_cast<int>(f));
   return c;
 }
 
@@ -482,6 +484,22 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
       for (int t = 0; t < D; ++t) q[t] = Q[w * D + t];
       orow = qout != nullptr ? qout[w] : w;
       if (excl_arr != nullptr) self = excl_arr[orow];
+    }
+    {
+      // a non-finite query ranks no point (the host entry points reject it with FMGP_EINVAL):
+      // the row is INT_MAX / inf, no walk
+      bool qfin = true;
+#pragma unroll
+      for (int t = 0; t < D; ++t) qfin = qfin && (__double2hiint(q[t]) & 0x7ff00000) != 0x7ff00000;
+      if (!qfin) {
+        const int width = kk + (with_self ? 1 : 0);
+        if (with_self && lane == 0) out[orow * width] = self;
+        for (int t = lane; t < kk; t += 32) {
+          out[orow * width + (with_self ? 1 : 0) + t] = INT_MAX;
+          if (out_d) out_d[orow * kk + t] = INFINITY;
+        }
+        continue;
+      }
     }
     int c[3];
     cell_key<D>(q, g, c);
@@ -1054,9 +1072,14 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
     const int64_t orow = !has ? 0 : (qout != nullptr ? qout[w0 + lane] : w0 + lane);
     Cand best{INFINITY, INT_MAX};
     int32_t bpos = 0;  // grid position of best (the grid-ordered model's row)
-    bool certified = !has;
+    // a non-finite test point has no nearest neighbour (every key is NaN or inf): no search,
+    // nn = -1 and NaN means below (the host entry points reject such batches with FMGP_EINVAL)
+    bool qfin = true;
+#pragma unroll
+    for (int t = 0; t < D; ++t) qfin = qfin && (__double2hiint(q[t]) & 0x7ff00000) != 0x7ff00000;
+    bool certified = !has || !qfin;
     if constexpr (kThreadNN) {
-      if (has) {
+      if (has && qfin) {
         int c[3];
         cell_key<D>(q, g, c);
         const int x0 = max(c[0] - 1, 0), x1 = min(c[0] + 1, g.G[0] - 1);

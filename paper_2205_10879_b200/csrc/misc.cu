@@ -56,6 +56,22 @@ __global__ void nonfinite_kernel(const double* __restrict__ v, int64_t n, unsign
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(count, bad);
 }
 
+// The same count on a buffer the caller owns, replacing each non-finite value by 0: the
+// kernels that follow (cell sort, walk) then run on valid coordinates, and the caller
+// turns a non-zero count into the error return after its final synchronise.
+__global__ void nonfinite_zero_kernel(double* __restrict__ v, int64_t n, unsigned int* __restrict__ count) {
+  unsigned int bad = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if ((__double2hiint(v[i]) & 0x7ff00000) == 0x7ff00000) {
+      v[i] = 0.0;
+      ++bad;
+    }
+  }
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(count, bad);
+}
+
 __global__ void self_rows_kernel(int32_t* __restrict__ S, int64_t nrows, int64_t row_begin) {
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nrows;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -117,6 +133,16 @@ cudaError_t nonfinite_count_launch(const double* v, int64_t n, unsigned int* cou
   int64_t blocks = (n + 255) / 256;
   if (blocks > static_cast<int64_t>(num_sms) * 8) blocks = static_cast<int64_t>(num_sms) * 8;
   nonfinite_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(v, n, count);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t nonfinite_zero_launch(double* v, int64_t n, unsigned int* count, int num_sms, cudaStream_t stream) {
+  cudaError_t err = cudaMemsetAsync(count, 0, sizeof(unsigned int), stream);
+  if (err != cudaSuccess || n <= 0) return err;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > static_cast<int64_t>(num_sms) * 8) blocks = static_cast<int64_t>(num_sms) * 8;
+  nonfinite_zero_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(v, n, count);
   note_launches(1);
   return cudaGetLastError();
 }
