@@ -280,18 +280,30 @@ __device__ __forceinline__ double kernel_from_sq(double acc, const KParams& p) {
 // refinement, and exp(-a) rounds with the 1.5*2^52 shift instead of
 // FRND/F2I and folds 2^-(m>>6) into the table value's exponent field.
 //
-// sqrt(x) for finite x >= 0: MUFU rsqrt seed (~2^-22), one Goldschmidt step
-// (~2^-43), one Newton correction of the root (< 1 ulp + rounding). x == 0
-// gives NaN (0 * inf); every caller replaces the d == 0 entry by the nugget.
+// sqrt(x) for finite x >= 0: MUFU rsqrt seed (~2^-22) and one third-order
+// correction (< 1 ulp + rounding). x == 0 gives NaN (0 * inf); every caller
+// replaces the d == 0 entry by the nugget.
+#ifndef FMGP_SQRT_BUILD3
+#define FMGP_SQRT_BUILD3 1
+#endif
 __device__ __forceinline__ double sqrt_build(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#if FMGP_SQRT_BUILD3
+  // one third-order step: r = x y, e = 1 - r y (exact residual of the rounded r),
+  // sqrt(x) = r / sqrt(1 - e) = r (1 + e/2 + 3 e^2/8 + O(e^3)), e ~ 2^-22: five FP64
+  // operations, four of them dependent, instead of seven (A/B: FMGP_SQRT_BUILD3=0)
+  const double r = x * y;
+  const double e = fma(-r, y, 1.0);
+  return fma(r * e, fma(e, 0.375, 0.5), r);
+#else
   double r = x * y, h = 0.5 * y;
   const double e = fma(-r, h, 0.5);
   r = fma(r, e, r);
   h = fma(h, e, h);
   const double dd = fma(-r, r, x);
   return fma(dd, h, r);
+#endif
 }
 
 // 1/sqrt(x) for a Cholesky pivot x > 0: MUFU seed and two Newton steps
