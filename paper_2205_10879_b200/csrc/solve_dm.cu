@@ -134,26 +134,45 @@ __device__ __forceinline__ bool dm_factor(double* A, const double* xs, const KPa
   const int g = lane >> 2, t = lane & 3;
   double F[NBR][2 * NBC];
   bool bad = false;
+  // -K of the full tiles of one block column, evaluated from the coordinates. The tiles of
+  // block column J + 1 are evaluated inside the panel step of block column J (FMGP_DM_AHEAD):
+  // independent FP64 work that runs under the panel's serial pivot chain.
+  double accn[NBR][2];
+  auto eval_full = [&](const int Jn) {
+    double wc[2][D];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int c = 0; c < D; ++c) wc[e][c] = xs[(8 * Jn + 2 * t + e < K ? 8 * Jn + 2 * t + e : 0) * D + c];
+#pragma unroll
+    for (int I = 0; I < NBR; ++I) {
+      if (I >= Jn && Sh::full(I, Jn)) {
+        double ur[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) ur[c] = xs[(8 * I + g) * D + c];
+        accn[I][0] = dm_pair<D, KF>(ur, wc[0], cs, kn, tab);
+        accn[I][1] = dm_pair<D, KF>(ur, wc[1], cs, kn, tab);
+      }
+    }
+  };
+#if FMGP_DM_AHEAD
+  eval_full(0);
+#endif
 #pragma unroll
   for (int J = 0; J < NBC; ++J) {
 #if FMGP_DM_SYNCJ
     __syncthreads();
 #endif
     double acc[NBR][2];
-    // 1. -K(I, J): full tiles evaluated here, the rest from the packed copy
-    double wc[2][D];
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-#pragma unroll
-      for (int c = 0; c < D; ++c) wc[e][c] = xs[(8 * J + 2 * t + e < K ? 8 * J + 2 * t + e : 0) * D + c];
+    // 1. -K(I, J): full tiles from the coordinates, the rest from the packed copy
+#if !FMGP_DM_AHEAD
+    eval_full(J);
+#endif
 #pragma unroll
     for (int I = J; I < NBR; ++I) {
       if (Sh::full(I, J)) {
-        double ur[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) ur[c] = xs[(8 * I + g) * D + c];
-        acc[I][0] = dm_pair<D, KF>(ur, wc[0], cs, kn, tab);
-        acc[I][1] = dm_pair<D, KF>(ur, wc[1], cs, kn, tab);
+        acc[I][0] = accn[I][0];
+        acc[I][1] = accn[I][1];
       } else {
         const int r = 8 * I + g;
         const double2 v = *reinterpret_cast<const double2*>(A + dm_row(r, K) + 8 * J + 2 * t);
@@ -206,6 +225,9 @@ __device__ __forceinline__ bool dm_factor(double* A, const double* xs, const KPa
         }
       }
     }
+#if FMGP_DM_AHEAD
+    if (J + 1 < NBC) eval_full(J + 1);
+#endif
     // The pivot of column c + 1 is taken from its owner lane right after column c is scaled (on that
     // lane the update of its own diagonal entry is la * la, no shuffle needed), so the next
     // shuffle -> rsqrt chain runs under the rest of column c's updates.
@@ -310,6 +332,9 @@ __device__ __forceinline__ void dm_back(const double* A, double dv0, double dv1,
 #endif
 #ifndef FMGP_DM_LOCKSTEP
 #define FMGP_DM_LOCKSTEP 1
+#endif
+#ifndef FMGP_DM_AHEAD  // 1: the next block column's full tiles are evaluated under the current panel (A/B: no gain)
+#define FMGP_DM_AHEAD 0
 #endif
 #ifndef FMGP_DM_SYNCJ  // 1: the CTA's warps also meet at every block column of the factorisation
 #define FMGP_DM_SYNCJ 0
