@@ -487,8 +487,8 @@ def main():
     hbm, hbm_src = hbm_peak()
     # measured DRAM traffic of the same kernels (committed ncu capture of this command), scaled to the step
     tr = load_json(REPO / "profiles" / "r02" / "traffic.json") or {}
-    tr_solve = tr.get(f"solve_reg_kernel<{k},{m},{d}>") if info.cfg == 5 else None
-    tr_pred = tr.get(f"grid_predict_kernel<{d},3,1>") if info.cfg == 5 else None
+    tr_solve = tr.get("solve_cfg5") if info.cfg == 5 else None
+    tr_pred = tr.get("predict_cfg5") if info.cfg == 5 else None
     rows_per_rank = (n + ws - 1) // ws
     roof = None
     if solve_ms is not None and knn_ms is not None:
@@ -500,7 +500,7 @@ def main():
                     "traffic": ((tr_solve["dram_read_bytes"] + tr_solve["dram_write_bytes"]) / tr_solve["rows_per_launch"]
                                 * rows_per_rank) if tr_solve else None,
                     "traffic_unit": "DRAM bytes for the step's rows (ncu per-launch bytes scaled by rows)",
-                    "traffic_source": "profiles/r02/traffic.json" if tr_solve else None,
+                    "traffic_source": f"profiles/r02/traffic.json ({tr_solve.get('kernel')})" if tr_solve else None,
                     "fp64_pipe_active_pct_ncu": tr_solve.get("fp64_pipe_active_pct") if tr_solve else None,
                     "work": f"{solve_flops_per_row(info):.0f} fp64 flops per training row (SURVEY 8(d): k^3/3 + "
                             f"2k^2m + 3d k(k-1)/2; the k(k-1)/2 kernel evaluations are not counted) x {rows_per_rank} "

@@ -1048,7 +1048,7 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
                     const int32_t* __restrict__ qout, const double* __restrict__ X, const int32_t* __restrict__ S,
                     const double* __restrict__ Cf, int k, int m, KParams kp, const double* __restrict__ mean_offset,
                     double* __restrict__ out, int32_t* __restrict__ nn_out, const int32_t* __restrict__ pos_of,
-                    const int32_t* __restrict__ s_pos, const double* __restrict__ c_perm) {
+                    const int32_t* __restrict__ s_pos, const double* __restrict__ c_perm, int lane_dot) {
   __shared__ int32_t s_beg[kQueryThreads / 32][kSlots];
   __shared__ int32_t s_pre[kQueryThreads / 32][kSlots + 1];
   __shared__ double s_exp[FMGP_BUILD_TAB_N];
@@ -1123,6 +1123,49 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
     if (S == nullptr) continue;  // nearest-only walk (NeighborIndex::nearest_training_point)
     if (has && !found)  // no candidate ranked (non-finite or overflowing z): NaN means, no gather
       for (int cc = 0; cc < m; ++cc) out[orow * m + cc] = __longlong_as_double(0x7ff8000000000000ll);
+    if (fast && lane_dot) {
+      // Gather-kernel-dot, one lane per test point (the lane that found the point's nearest
+      // row walks that row itself): no shuffles, no reduction tree, every lane busy for all k
+      // neighbours (a warp spread over one point's k = 50 neighbours fills 50 of 64 lane slots
+      // and pays a 5-step reduction per point). Two neighbours per step: one 8-byte load of
+      // the S row, one 16-byte load of the C row (each 32-byte sector is consumed by adjacent
+      // steps, so the rows stream through L1 once), two coordinate gathers, two evaluations
+      // into two accumulators. Sum order: sequential within each parity, as the reference's
+      // loop up to rounding (tolerance 1e-9, tested).
+      const bool perm = s_pos != nullptr;
+      const int32_t* Sr = perm ? s_pos : S;
+      const double* Cr = perm ? c_perm : Cf;
+      const double* Xr = perm ? pts : X;
+      const bool ok = has && found;
+      const int64_t j = ok ? (perm ? bpos : best.i) : 0;
+      const int2* srow = reinterpret_cast<const int2*>(Sr + j * k);
+      const double2* crow = reinterpret_cast<const double2*>(Cr + j * k);
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 2
+      for (int t = 0; t < (k >> 1); ++t) {
+        const int2 nb = __ldg(srow + t);
+        const double2 cv = __ldg(crow + t);
+        double xa[D], xb[D];
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+          xa[u] = __ldg(&Xr[static_cast<int64_t>(nb.x) * D + u]);
+          xb[u] = __ldg(&Xr[static_cast<int64_t>(nb.y) * D + u]);
+        }
+        double da = q[0] - xa[0], db = q[0] - xb[0];
+        double sa = da * da, sb = db * db;
+#pragma unroll
+        for (int u = 1; u < D; ++u) {
+          da = q[u] - xa[u];
+          db = q[u] - xb[u];
+          sa = fma(da, da, sa);
+          sb = fma(db, db, sb);
+        }
+        acc0 = fma(kernel_from_sq_build<KF>(sa, kc, kp, s_exp), cv.x, acc0);
+        acc1 = fma(kernel_from_sq_build<KF>(sb, kc, kp, s_exp), cv.y, acc1);
+      }
+      if (ok) out[orow] = (acc0 + acc1) + mean_offset[0];
+      continue;
+    }
     if (fast) {
       const int t0 = lane, t1 = lane + kWarp;
       const bool h0 = t0 < k, h1 = t1 < k;
@@ -1528,17 +1571,24 @@ cudaError_t run_predict_grid(const PredictGridCache& g, const double* X, const i
     const char* e = std::getenv("FMGP_PGRID_WARP");
     return e != nullptr && e[0] == '1';
   }();
+  // lane-per-point gather-kernel-dot (FMGP_PGRID_LANEDOT=0: a warp per point's neighbours, A/B);
+  // needs an even k and 8- / 16-byte aligned S / C rows for its vector loads
+  const char* ld_env = std::getenv("FMGP_PGRID_LANEDOT");
+  const int32_t* s_rows = use_perm ? sp : S;
+  const double* c_rows = use_perm ? cp : Cf;
+  const int lane_dot = !(ld_env != nullptr && ld_env[0] == '0') && (k & 1) == 0 && S != nullptr &&
+                       (reinterpret_cast<uintptr_t>(s_rows) & 7) == 0 && (reinterpret_cast<uintptr_t>(c_rows) & 15) == 0;
   switch (kp.kind == 1 ? 0 : 1 + kp.nu_code) {  // kernel_code(), evaluated on the host
 #define FMGP_PRED_CASE(KF)                                                                                      \
   case KF:                                                                                                      \
     if (warp_nn)                                                                                                \
       grid_predict_kernel<D, KF, false><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                \
           g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out,    \
-          g.pos_of, sp, cp);                                                                                    \
+          g.pos_of, sp, cp, lane_dot);                                                                                  \
     else                                                                                                        \
       grid_predict_kernel<D, KF, true><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(                 \
           g.gp, g.pb.pts, g.pb.pid, g.pb.cstart, nz, Qs, qo, X, S, Cf, k, m, kp, mean_offset_dev, out, nn_out,    \
-          g.pos_of, sp, cp);                                                                                    \
+          g.pos_of, sp, cp, lane_dot);                                                                                  \
     break;
     FMGP_PRED_CASE(0)
     FMGP_PRED_CASE(1)
