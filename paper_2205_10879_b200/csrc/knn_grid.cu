@@ -367,6 +367,10 @@ __device__ __forceinline__ double outside_lb_sq(const GridParams& g, const doubl
 }
 
 constexpr int kQueryThreads = 256;
+#ifndef FMGP_LANEDOT_UNROLL
+#define FMGP_LANEDOT_UNROLL 4
+#endif
+constexpr int kLaneDotUnroll = FMGP_LANEDOT_UNROLL;  // neighbour pairs per unrolled step of the lane-per-point dot
 constexpr int kSlots = 64;  // ranges per chunk: 2 per lane (one cell-row per lane)
 #ifndef FMGP_INSERT_MAX
 #define FMGP_INSERT_MAX 4
@@ -1141,7 +1145,7 @@ grid_predict_kernel(const GridParams* __restrict__ gpp, const double* __restrict
       const int2* srow = reinterpret_cast<const int2*>(Sr + j * k);
       const double2* crow = reinterpret_cast<const double2*>(Cr + j * k);
       double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll 2
+#pragma unroll kLaneDotUnroll
       for (int t = 0; t < (k >> 1); ++t) {
         const int2 nb = __ldg(srow + t);
         const double2 cv = __ldg(crow + t);
