@@ -170,7 +170,8 @@ Cyclic make_cyclic(int64_t n, int g) {
   Cyclic cy;
   cy.n = n;
   cy.g = g;
-  cy.pc = std::max<int64_t>(1, (n + static_cast<int64_t>(g) * rounds - 1) / (static_cast<int64_t>(g) * rounds));
+  const int rd = g == 1 ? 1 : rounds;  // a group of one has nothing to exchange: one round
+  cy.pc = std::max<int64_t>(1, (n + static_cast<int64_t>(g) * rd - 1) / (static_cast<int64_t>(g) * rd));
   return cy;
 }
 

@@ -69,6 +69,8 @@ def cyclic_blocks(n: int, world: int, rounds: int = 4) -> tuple[int, list[list[t
     fmgp_group_rows): blocks of pc = ceil(n / (world * rounds)) rows dealt
     round-robin; round c is rows [c*world*pc, (c+1)*world*pc) and member r owns
     its block c*world + r. Returns pc and, per round, every member's [b, e)."""
+    if world == 1:
+        rounds = 1  # nothing to exchange: one round (as csrc/group.cu)
     pc = max(1, -(-n // (world * rounds)))
     out = []
     c = 0
