@@ -1580,7 +1580,8 @@ cudaError_t run_predict_grid(const PredictGridCache& g, const double* X, const i
   const char* ld_env = std::getenv("FMGP_PGRID_LANEDOT");
   const int32_t* s_rows = use_perm ? sp : S;
   const double* c_rows = use_perm ? cp : Cf;
-  const int lane_dot = !(ld_env != nullptr && ld_env[0] == '0') && (k & 1) == 0 && S != nullptr &&
+  // (and the cell-ordered model replica: without it the lanes' rows are scattered over the model)
+  const int lane_dot = !(ld_env != nullptr && ld_env[0] == '0') && use_perm && (k & 1) == 0 && S != nullptr &&
                        (reinterpret_cast<uintptr_t>(s_rows) & 7) == 0 && (reinterpret_cast<uintptr_t>(c_rows) & 15) == 0;
   switch (kp.kind == 1 ? 0 : 1 + kp.nu_code) {  // kernel_code(), evaluated on the host
 #define FMGP_PRED_CASE(KF)                                                                                      \
