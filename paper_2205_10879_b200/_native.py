@@ -136,6 +136,20 @@ def load() -> C.CDLL:
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `python -m paper_2205_10879_b200.build` "
             "(the FastMuyGPs B200 path has no CPU fallback)")
+    if not os.environ.get("FMGP_NCCL_LIB"):
+        # device groups dlopen NCCL lazily; in a Python process prefer the NCCL wheel torch is built
+        # against over an older system libnccl.so.2 (same SONAME: whichever loads first wins, and
+        # torch imported later would miss symbols in the older one)
+        import importlib.util
+        try:
+            spec = importlib.util.find_spec("nvidia.nccl")
+        except (ImportError, ValueError):
+            spec = None
+        for loc in (spec.submodule_search_locations if spec is not None and spec.submodule_search_locations else []):
+            cand = Path(loc) / "lib" / "libnccl.so.2"
+            if cand.exists():
+                os.environ["FMGP_NCCL_LIB"] = str(cand)
+                break
     lib = C.CDLL(str(LIB_PATH))
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)

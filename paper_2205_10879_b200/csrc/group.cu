@@ -24,7 +24,7 @@
 //    on one GPU) peer copies (cudaMemcpyPeerAsync) push each block to the
 //    other members.
 // NCCL is loaded at run time (dlopen "libnccl.so.2": the process's copy when
-// one is already loaded, e.g. torch's, else the system's), so the library has
+// one is already loaded, e.g. torch's, else FMGP_NCCL_LIB, else the system's), so the library has
 // no link-time NCCL dependency and single-GPU use never touches it.
 //
 // Every row's arithmetic is the single-GPU kernels' (knn_grid / knn_tc / fp64
@@ -72,7 +72,14 @@ struct NcclApi {
 NcclApi& nccl() {
   static NcclApi api = [] {
     NcclApi a;
+    // the process's copy if one is loaded; else FMGP_NCCL_LIB (the Python binding points it at the
+    // NCCL wheel torch was built against, so a later `import torch` in the same process does not find
+    // an older system libnccl under the same SONAME); else the system's
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (h == nullptr) {
+      const char* pth = std::getenv("FMGP_NCCL_LIB");
+      if (pth != nullptr && pth[0] != 0) h = dlopen(pth, RTLD_NOW | RTLD_LOCAL);
+    }
     if (h == nullptr) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (h == nullptr) {
       const char* e = dlerror();
