@@ -291,7 +291,10 @@ int member_precompute(CallCtx& cx, int mi, const double* X, const double* Y, int
     FMGP_CUDA(cudaEventRecord(tev[0], st.work));
   }
   if (k > 1) {
-    if (myrows > 0 && fmgp::knn_grid_supported(d, k - 1) && std::getenv("FMGP_KNN") == nullptr) {
+    if (cy.g == 1) {
+      // a group of one: the plain search over every row (walks the rows in cell order)
+      FMGP_CUDA(fmgp::knn_exact(X, n, X, n, d, k - 1, 0, nullptr, 1, S, nullptr, sms, st.work));
+    } else if (myrows > 0 && fmgp::knn_grid_supported(d, k - 1) && std::getenv("FMGP_KNN") == nullptr) {
       FMGP_CUDA(fmgp::knn_grid_rows_cyclic(X, n, d, k - 1, myrows, cy.pc, cy.g, r, S, sms, st.work));
     } else {
       for (int64_t c = 0; c < cy.rounds(); ++c) {
