@@ -376,6 +376,9 @@ constexpr int kSlots = 64;  // ranges per chunk: 2 per lane (one cell-row per la
 #define FMGP_INSERT_MAX 4
 #endif
 constexpr int kInsertMax = FMGP_INSERT_MAX;  // batches with at most this many admissions are inserted one by one
+#ifndef FMGP_GQ_SELECT  // 1: threshold selection of the first chunk (A/B: slower, see profiles/r02/ab_gq_select.txt)
+#define FMGP_GQ_SELECT 0
+#endif
 
 // Static cell visiting order for the warp kernel: every offset o of Chebyshev
 // radius <= R sorted by its static lower bound sb(o) = sum_t max(|o_t| - 1, 0)^2
@@ -466,6 +469,8 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
                   int kk, int with_self, int64_t row_offset, int32_t* __restrict__ out, double* __restrict__ out_d) {
   __shared__ int32_t s_beg[kQueryThreads / 32][kSlots];
   __shared__ int32_t s_pre[kQueryThreads / 32][kSlots + 1];
+  __shared__ double s_ck[E == 2 ? kQueryThreads / 32 : 1][64];  // first-chunk selection: the 64 kept candidates
+  __shared__ int32_t s_ci[E == 2 ? kQueryThreads / 32 : 1][64];
   const GridParams g = *gpp;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -550,7 +555,81 @@ grid_query_kernel(const GridParams* __restrict__ gpp, const double* __restrict__
         return cd;
       };
       int32_t base = 0;
-      if (fresh && total >= 64) {
+      bool selected = false;
+#if FMGP_GQ_SELECT
+      if constexpr (E == 2) {
+        if (fresh && total > 64 && total <= 128) {
+          // The list is empty and the first chunk (the 3^D block) holds 65..128 candidates,
+          // of which 64 can stay: instead of sorting all of them (a 64-network plus one
+          // 30-stage sort + merge per further batch), find a key value with exactly 64
+          // candidates at or below it by bisection (one redux per round), compact those 64
+          // through shared memory and sort only them. Exact: the 64 kept are the 64
+          // smallest keys; when no such value exists (a tie across the 64th / 65th key)
+          // or fewer than 64 candidates are valid, the sort path below runs instead.
+          Cand c4[4];
+#pragma unroll
+          for (int s4 = 0; s4 < 4; ++s4) c4[s4] = fetch(s4 * 32 + lane);
+          double mn = INFINITY, mx = 0.0;
+#pragma unroll
+          for (int s4 = 0; s4 < 4; ++s4) {
+            mn = fmin(mn, c4[s4].d);
+            mx = c4[s4].d < INFINITY ? fmax(mx, c4[s4].d) : mx;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          }
+          auto count_le = [&](double v) {
+            int cl = 0;
+#pragma unroll
+            for (int s4 = 0; s4 < 4; ++s4) cl += c4[s4].d <= v ? 1 : 0;
+            return __reduce_add_sync(0xffffffffu, cl);
+          };
+          double cut = mx;
+          int cnt = count_le(mx);  // the valid candidates (self and padding are inf)
+          if (cnt > 64) {
+            double lo = mn, hi = mx;  // count(<= lo) >= 1, count(<= hi) > 64
+            for (int round = 0; round < 24; ++round) {
+              const double mid = lo + 0.5 * (hi - lo);
+              if (!(mid > lo && mid < hi)) break;  // adjacent doubles: a tie across the boundary
+              cnt = count_le(mid);
+              cut = mid;
+              if (cnt == 64) break;
+              if (cnt < 64) lo = mid;
+              else hi = mid;
+            }
+          }
+          if (cnt == 64) {
+            double* ck = s_ck[wib];
+            int32_t* ci = s_ci[wib];
+            int pos0 = 0;
+#pragma unroll
+            for (int s4 = 0; s4 < 4; ++s4) {
+              const bool keep = c4[s4].d <= cut;
+              const unsigned bal = __ballot_sync(0xffffffffu, keep);
+              if (keep) {
+                const int pp = pos0 + __popc(bal & ((1u << lane) - 1u));
+                ck[pp] = c4[s4].d;
+                ci[pp] = c4[s4].i;
+              }
+              pos0 += __popc(bal);
+            }
+            __syncwarp();
+            Cand a = bitonic_sort32(Cand{ck[lane], ci[lane]}, lane);
+            Cand b2 = bitonic_sort32(Cand{ck[32 + lane], ci[32 + lane]}, lane);
+            merge32(a, b2, lane);
+            L[0] = a;
+            L[1] = b2;
+            thr = shfl_c(te == 0 ? L[0] : L[1], tl);
+            base = total;
+            selected = true;
+            __syncwarp();
+          }
+        }
+      }
+#endif
+      if (!selected && fresh && total >= 64) {
         // the list is empty: sort the first 64 candidates as one bitonic network
         // (two 32-sorts + one merge: 41 compare-exchange stages instead of the
         // 60 of two batch merges) and take them as the list
