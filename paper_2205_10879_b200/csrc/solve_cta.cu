@@ -8,8 +8,12 @@
 // latency-bound). Here the CTA's R = K + M threads own one row each of the
 // augmented matrix [K ; Y^T] in registers:
 //  * build: all K neighbour coordinates are staged once in shared memory
-//    (padded rows), the strict lower triangle is spread over the CTA through a
-//    pair table, entries land in a packed row-major triangle;
+//    (padded rows); for d >= 16 the squared distances come from a Gram matrix
+//    on the FP64 tensor cores (cta_gram: DMMA m8n8k4 over the 8 x 8 tiles of
+//    the lower triangle, coordinates centred at the neighbourhood's own point,
+//    exact recompute of near-duplicates), otherwise the strict lower triangle
+//    is spread over the CTA through a pair table; entries land in a packed
+//    row-major triangle;
 //  * factor: left-looking column sweep. For column j every row r > j forms
 //    s_r = a_rj - sum_{p<j} a_rp L_jp from its registers and the pivot row
 //    L_j. (a shared-memory 128-bit broadcast); the rows also keep a running
@@ -17,6 +21,8 @@
 //    as soon as it has L_{j+1,j}: one barrier per column. The RHS rows ride
 //    along (forward substitution);
 //  * backward solve: warp 0, x in registers, x_j broadcast by shuffle.
+#include <cstdlib>
+
 #include "fmgp_common.cuh"
 #include "fmgp_internal.h"
 
@@ -36,9 +42,13 @@ struct CtaShape {
   static constexpr int kPairs = K * (K - 1) / 2;
   static constexpr int kXsD = 48;                             // coordinate slice staged per pass
   static constexpr int kXsStride = kXsD + 2;  // = 2 mod 4 doubles: 128-bit loads of 8 lanes on distinct bank groups
-  static constexpr int kXs = ((K * kXsStride + 1) / 2) * 2;
-  // doubles: tri | xs | invd[K] | zbuf[M*K] | misc[2]; then uint32 pairs, int32 sr
-  static constexpr int kDoubles = kTri + kXs + ((K + 1) & ~1) + ((M * K + 1) & ~1) + 2;
+  // Gram build (d >= 16): rows of kXsD + 4 doubles (= 4 mod 16: the DMMA fragment load of lane (g, t),
+  // row 8 I + g, column 4 c + t, touches every 8-byte bank pair exactly twice: two wavefronts for 32 doubles)
+  static constexpr int kGsStride = kXsD + 4;
+  static constexpr int kXs = ((K * kGsStride + 1) / 2) * 2;
+  static constexpr int kNB = (K + 7) / 8;  // 8-row blocks of the Gram matrix
+  // doubles: tri | xs | invd[K] | zbuf[M*K] | nrm[K] | misc[2]; then uint32 pairs, int32 sr
+  static constexpr int kDoubles = kTri + kXs + ((K + 1) & ~1) + ((M * K + 1) & ~1) + ((K + 1) & ~1) + 2;
   static constexpr size_t kBytes = sizeof(double) * kDoubles + sizeof(uint32_t) * kPairs + sizeof(int32_t) * K;
 };
 
@@ -76,18 +86,86 @@ __device__ __forceinline__ void cta_pairs(const double* xs, const uint32_t* ptab
   }
 }
 
+__device__ __forceinline__ void dmma_c(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// Gram build of one coordinate slice (d >= 16; cfg4: d = 40, one slice): the squared distances of
+// the neighbourhood come from G = Xc Xc^T on the FP64 tensor cores, Xc = the staged coordinates
+// centred at the neighbourhood's own point (row 0), so |x|^2 is of the order of the distances and
+// d^2 = |a|^2 + |b|^2 - 2 a.b keeps its digits. The 8 x 8 tiles of the lower triangle are dealt
+// over the CTA's warps; lane (g, t) holds Xc[8 I + g][4 c + t], which is the A fragment of row
+// block I and the B fragment of row block J alike. Partial sums of G (and of the norms) go through
+// the packed triangle between slices; the last slice turns them into kernel values. A pair with
+// d^2 <= 1e-12 (|a|^2 + |b|^2) is recomputed as the exact sum of squared differences, so exact
+// duplicates keep the nugget bit for bit (kernel.cpp:58-60, :81-83). The direct difference loop
+// this replaces took ~25 k of the kernel's ~75 k warp instructions per neighbourhood at cfg4.
+template <int K, int M, int KF>
+__device__ __forceinline__ void cta_gram(const double* gs, const double* nrm, const KParams& kp, double* tri, int c0,
+                                         int dc4, int tid, bool last) {
+  using Sh = CtaShape<K, M>;
+  constexpr int NB = Sh::kNB;
+  constexpr int NT = NB * (NB + 1) / 2;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  for (int e = warp; e < NT; e += Sh::kThreads / 32) {
+    int I = static_cast<int>((sqrtf(8.0f * static_cast<float>(e) + 1.0f) - 1.0f) * 0.5f);
+    while (I * (I + 1) / 2 > e) --I;
+    while ((I + 1) * (I + 2) / 2 <= e) ++I;
+    const int J = e - I * (I + 1) / 2;
+    const int ra = 8 * I + g, rb = 8 * J + g;
+    const double* pa = gs + (ra < K ? ra : 0) * Sh::kGsStride + t;
+    const double* pb = gs + (rb < K ? rb : 0) * Sh::kGsStride + t;
+    double acc[2] = {0.0, 0.0};
+#pragma unroll 4
+    for (int c = 0; c < dc4; c += 4) dmma_c(acc, ra < K ? pa[c] : 0.0, rb < K ? pb[c] : 0.0);
+    // accumulator layout: row 8 I + g, columns 8 J + 2 t, + 1
+    const int col = 8 * J + 2 * t;
+    if (ra >= K) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cc = col + h;
+      if (cc >= ra) continue;  // strict lower triangle only (the diagonal is set with the jitter rung)
+      double* out = tri + ro_c(ra) + cc;
+      double gsum = acc[h];
+      if (c0 != 0) gsum += *out;
+      if (!last) {
+        *out = gsum;
+        continue;
+      }
+      const double na = nrm[ra], nb = nrm[cc];
+      double d2 = fma(-2.0, gsum, na + nb);
+      if (!(d2 > 1e-12 * (na + nb))) {  // (near-)duplicate: exact differences (this slice holds every dimension
+        d2 = 0.0;                        // when d <= kXsD; for wider rows the earlier slices are gone, so clamp)
+        if (c0 == 0) {
+          const double* xa = gs + ra * Sh::kGsStride;
+          const double* xb = gs + cc * Sh::kGsStride;
+          for (int c = 0; c < dc4; ++c) {
+            const double df = xa[c] - xb[c];
+            d2 = fma(df, df, d2);
+          }
+        }
+      }
+      *out = kernel_from_sq<KF>(d2, kp);
+    }
+  }
+}
+
 template <int K, int M>
 __global__ void __launch_bounds__(CtaShape<K, M>::kThreads, 1)
 solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
                  int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
-                 unsigned long long* __restrict__ fail_min) {
+                 unsigned long long* __restrict__ fail_min, int use_gram) {
   using Sh = CtaShape<K, M>;
   extern __shared__ double smem[];
   double* tri = smem;
   double* xs = tri + Sh::kTri;
   double* invd = xs + Sh::kXs;
   double* zbuf = invd + ((K + 1) & ~1);
-  double* misc = zbuf + ((M * K + 1) & ~1);  // [0] = failure flag
+  double* nrm = zbuf + ((M * K + 1) & ~1);  // Gram build: |x - x_0|^2 per neighbour
+  double* misc = nrm + ((K + 1) & ~1);      // [0] = failure flag
   uint32_t* ptab = reinterpret_cast<uint32_t*>(misc + 2);
   int32_t* sr = reinterpret_cast<int32_t*>(ptab + Sh::kPairs);
   const int tid = threadIdx.x;
@@ -109,7 +187,34 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
     bool ok = false;
     for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
       // ---- build K(S_r) into the packed triangle (sequential-in-t distance)
-      for (int c0 = 0; c0 < d; c0 += Sh::kXsD) {
+      // one slice only (d <= kXsD): the exact recompute of near-duplicates needs every dimension staged
+      const bool gram = use_gram && d >= 16 && d <= Sh::kXsD;
+      for (int c0 = 0; gram && c0 < d; c0 += Sh::kXsD) {
+        const int dc = min(Sh::kXsD, d - c0), dc4 = (dc + 3) & ~3;
+        const double* x0 = X + static_cast<int64_t>(sr[0]) * d + c0;  // centre: the neighbourhood's own point
+        for (int e = tid; e < K * dc4; e += Sh::kThreads) {
+          const int t = e / dc4, c = e - t * dc4;
+          xs[t * Sh::kGsStride + c] = c < dc ? X[static_cast<int64_t>(sr[t]) * d + c0 + c] - x0[c] : 0.0;
+        }
+        __syncthreads();
+        if (tid < K) {
+          double nn = c0 == 0 ? 0.0 : nrm[tid];
+          const double* xr = xs + tid * Sh::kGsStride;
+          for (int c = 0; c < dc4; ++c) nn = fma(xr[c], xr[c], nn);
+          nrm[tid] = nn;
+        }
+        __syncthreads();
+        const bool last = c0 + dc >= d;
+        switch (last ? kernel_code(kp) : 0) {  // uniform; the kind only matters in the last slice
+          case 0: cta_gram<K, M, 0>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
+          case 1: cta_gram<K, M, 1>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
+          case 2: cta_gram<K, M, 2>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
+          case 3: cta_gram<K, M, 3>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
+          default: cta_gram<K, M, 4>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
+        }
+        __syncthreads();
+      }
+      for (int c0 = 0; !gram && c0 < d; c0 += Sh::kXsD) {
         const int dc = min(Sh::kXsD, d - c0);
         for (int e = tid; e < K * dc; e += Sh::kThreads) {
           const int t = e / dc, c = e - t * dc;
@@ -248,8 +353,11 @@ cudaError_t launch_cta(const double* X, const double* Y, int d, const int32_t* S
   if (err != cudaSuccess) return err;
   if (per_sm < 1) per_sm = 1;
   const int64_t grid = std::min<int64_t>(nrows, static_cast<int64_t>(num_sms) * per_sm);
-  solve_cta_kernel<K, M><<<static_cast<unsigned>(grid), Sh::kThreads, Sh::kBytes, stream>>>(X, Y, d, S, nrows,
-                                                                                            row_begin, kp, C, fail_min);
+  // FMGP_SOLVE_GRAM=0: the direct difference build for every d (A/B, as in the register solve)
+  const char* ge = std::getenv("FMGP_SOLVE_GRAM");
+  const int use_gram = !(ge != nullptr && ge[0] == '0');
+  solve_cta_kernel<K, M><<<static_cast<unsigned>(grid), Sh::kThreads, Sh::kBytes, stream>>>(
+      X, Y, d, S, nrows, row_begin, kp, C, fail_min, use_gram);
   note_launches(1);
   return cudaGetLastError();
 }
