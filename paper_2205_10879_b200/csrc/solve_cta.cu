@@ -153,6 +153,123 @@ __device__ __forceinline__ void cta_gram(const double* gs, const double* nrm, co
   }
 }
 
+// Blocked factorisation in shared memory (M == 1; FMGP_CTA_BLOCKED=0 selects the row-per-thread
+// sweep below): the augmented matrix [K ; y^T] (row K = the RHS, kept in zbuf, so the
+// factorisation also does the forward substitution) is blocked 8 x 8 and factored left-looking
+// by block column J, in place in the packed triangle:
+//   1. update: tile (I, J) -= sum_{Q < 2J} F(I, Q) F(J, Q)^T on the FP64 tensor cores (DMMA
+//      m8n8k4), tiles dealt over the CTA's warps; F(I, Q) = lane (g, t) holding
+//      L[8I+g][4Q+t], read from the triangle; the (negated) fragments of row block J stay in
+//      registers for all of a warp's tiles;
+//   2. panel: thread i takes row 8J + i (down to the RHS row). Every thread factors the 8 x 8
+//      diagonal block itself, in registers (36 broadcast loads, no shuffles, no barrier between
+//      the pivots), then solves its own row against it and writes its 8 entries back.
+// Two barriers per block column (26 instead of the 100 of the column sweep), and the k^3/6
+// multiply-adds leave the scalar FP64 path with its shared-memory broadcasts.
+template <int K>
+__device__ __forceinline__ double* cta_row(double* tri, double* zrow, int r) { return r < K ? tri + ro_c(r) : zrow; }
+
+template <int K, int M>
+__device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, double* invd, double* misc, int tid) {
+  using Sh = CtaShape<K, M>;
+  constexpr int NBC = (K + 7) / 8;      // column blocks
+  constexpr int NBR = (K + 1 + 7) / 8;  // row blocks (rows 0 .. K; row K = RHS)
+  constexpr int NW = Sh::kThreads / 32;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll 1
+  for (int J = 0; J < NBC; ++J) {
+    const int c0 = 8 * J;
+    if (J > 0) {
+      // 1. update of block column J
+      double bq[2 * (NBC - 1)];
+      const int rb = c0 + g;  // the tile's column index this lane's B fragment belongs to
+      const double* pb = tri + ro_c(rb < K ? rb : 0) + t;
+#pragma unroll
+      for (int Q = 0; Q < 2 * (NBC - 1); ++Q) bq[Q] = (Q < 2 * J && rb < K) ? -pb[4 * Q] : 0.0;
+      for (int I = J + warp; I < NBR; I += NW) {
+        const int ra = 8 * I + g;
+        const bool rok = ra <= K;
+        double* prow = cta_row<K>(tri, zrow, rok ? ra : 0);
+        const int cc = c0 + 2 * t;
+        const int lim = ra < K ? ra + 1 : K;  // columns < lim exist in row ra
+        double acc[2];
+        acc[0] = rok && cc < lim ? prow[cc] : 0.0;
+        acc[1] = rok && cc + 1 < lim ? prow[cc + 1] : 0.0;
+        const double* pa = prow + t;
+#pragma unroll
+        for (int Q = 0; Q < 2 * (NBC - 1); ++Q)
+          if (Q < 2 * J) dmma_c(acc, rok ? pa[4 * Q] : 0.0, bq[Q]);
+        if (rok && cc < lim) prow[cc] = acc[0];
+        if (rok && cc + 1 < lim) prow[cc + 1] = acc[1];
+      }
+      __syncthreads();
+    }
+    // 2. panel: every thread factors the diagonal block, then solves its own row
+    const int nc = K - c0 < 8 ? K - c0 : 8;
+    double dblk[8][8];
+    double inv[8];
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c <= i; ++c) dblk[i][c] = i < nc ? tri[ro_c(i < nc ? c0 + i : c0) + c0 + c] : (i == c ? 1.0 : 0.0);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double piv = dblk[c][c];
+      bad = bad || !(piv > 0.0);
+      inv[c] = rsqrt(piv);
+      dblk[c][c] = piv * inv[c];
+#pragma unroll
+      for (int i = c + 1; i < 8; ++i) dblk[i][c] *= inv[c];
+#pragma unroll
+      for (int i = c + 1; i < 8; ++i)
+#pragma unroll
+        for (int c2 = c + 1; c2 <= i; ++c2) dblk[i][c2] = fma(-dblk[i][c], dblk[c2][c], dblk[i][c2]);
+    }
+    const int r = c0 + tid;
+    double x[8];
+    if (r <= K) {
+      double* prow = cta_row<K>(tri, zrow, r);
+      if (tid < 8) {  // a row of the diagonal block: its factor row (tid < nc here: r <= K and r < c0 + 8)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (i == tid)
+#pragma unroll
+            for (int c = 0; c <= i; ++c) x[c] = dblk[i][c];
+        if (r < K) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (c <= tid) prow[c0 + c] = x[c];
+        }
+      }
+      if (tid >= 8 || r == K) {  // a row below the block (or the RHS row inside the last block's span)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = c < nc ? prow[c0 + c] : 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          double v = x[c];
+#pragma unroll
+          for (int c2 = 0; c2 < c; ++c2) v = fma(-x[c2], dblk[c][c2], v);
+          x[c] = v * inv[c];
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < nc) prow[c0 + c] = x[c];
+      }
+    }
+    if (tid == 0) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < nc) invd[c0 + c] = inv[c];
+      if (bad) misc[0] = 1.0;
+    }
+    __syncthreads();
+  }
+}
+
 template <int K, int M>
 __global__ void __launch_bounds__(CtaShape<K, M>::kThreads, 1)
 solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
@@ -188,7 +305,7 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
     for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
       // ---- build K(S_r) into the packed triangle (sequential-in-t distance)
       // one slice only (d <= kXsD): the exact recompute of near-duplicates needs every dimension staged
-      const bool gram = use_gram && d >= 16 && d <= Sh::kXsD;
+      const bool gram = (use_gram & 1) && d >= 16 && d <= Sh::kXsD;
       for (int c0 = 0; gram && c0 < d; c0 += Sh::kXsD) {
         const int dc = min(Sh::kXsD, d - c0), dc4 = (dc + 3) & ~3;
         const double* x0 = X + static_cast<int64_t>(sr[0]) * d + c0;  // centre: the neighbourhood's own point
@@ -233,6 +350,19 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
         __syncthreads();
       }
       const double dg = jitter_c(kp.diag, attempt);
+      if (M == 1 && (use_gram & 2)) {
+        // ---- blocked DMMA factorisation in shared memory (cta_factor_blocked)
+        if (tid < K) {
+          tri[ro_c(tid) + tid] = dg;
+          zbuf[tid] = Y[static_cast<int64_t>(sr[tid]) * M];
+        }
+        if (tid == 0) misc[0] = 0.0;
+        __syncthreads();
+        cta_factor_blocked<K, M>(tri, zbuf, invd, misc, tid);
+        ok = misc[0] == 0.0;
+        __syncthreads();
+        continue;
+      }
       // ---- load the owned row into registers
       double a[K];
       double dacc = 0.0;
@@ -355,7 +485,8 @@ cudaError_t launch_cta(const double* X, const double* Y, int d, const int32_t* S
   const int64_t grid = std::min<int64_t>(nrows, static_cast<int64_t>(num_sms) * per_sm);
   // FMGP_SOLVE_GRAM=0: the direct difference build for every d (A/B, as in the register solve)
   const char* ge = std::getenv("FMGP_SOLVE_GRAM");
-  const int use_gram = !(ge != nullptr && ge[0] == '0');
+  const char* be = std::getenv("FMGP_CTA_BLOCKED");  // 0: row-per-thread column sweep instead of the blocked DMMA factor
+  const int use_gram = (!(ge != nullptr && ge[0] == '0') ? 1 : 0) | (!(be != nullptr && be[0] == '0') ? 2 : 0);
   solve_cta_kernel<K, M><<<static_cast<unsigned>(grid), Sh::kThreads, Sh::kBytes, stream>>>(
       X, Y, d, S, nrows, row_begin, kp, C, fail_min, use_gram);
   note_launches(1);
