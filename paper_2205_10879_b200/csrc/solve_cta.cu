@@ -102,25 +102,29 @@ __device__ __forceinline__ void dmma_c(double (&c)[2], double a, double b) {
 // d^2 <= 1e-12 (|a|^2 + |b|^2) is recomputed as the exact sum of squared differences, so exact
 // duplicates keep the nugget bit for bit (kernel.cpp:58-60, :81-83). The direct difference loop
 // this replaces took ~25 k of the kernel's ~75 k warp instructions per neighbourhood at cfg4.
-template <int K, int M, int KF>
+template <int K, int M, int KF, bool LEAN>
 __device__ __forceinline__ void cta_gram(const double* gs, const double* nrm, const KParams& kp, double* tri, int c0,
-                                         int dc4, int tid, bool last) {
+                                         int dc4, int tid, bool last, int gst, const double* __restrict__ X,
+                                         const int32_t* sr, int d) {
   using Sh = CtaShape<K, M>;
   constexpr int NB = Sh::kNB;
   constexpr int NT = NB * (NB + 1) / 2;
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  for (int e = warp; e < NT; e += Sh::kThreads / 32) {
-    int I = static_cast<int>((sqrtf(8.0f * static_cast<float>(e) + 1.0f) - 1.0f) * 0.5f);
-    while (I * (I + 1) / 2 > e) --I;
-    while ((I + 1) * (I + 2) / 2 <= e) ++I;
-    const int J = e - I * (I + 1) / 2;
+  // tile e = I (I + 1) / 2 + J, J <= I; a warp's tiles are NW apart, so (I, J) advance incrementally
+  int I = 0, J = warp;
+  for (int e = warp; e < NT; e += Sh::kThreads / 32, J += Sh::kThreads / 32) {
+    while (J > I) {
+      J -= I + 1;
+      ++I;
+    }
     const int ra = 8 * I + g, rb = 8 * J + g;
-    const double* pa = gs + (ra < K ? ra : 0) * Sh::kGsStride + t;
-    const double* pb = gs + (rb < K ? rb : 0) * Sh::kGsStride + t;
+    // rows past K read row 0: what they produce (rows >= K of the tile, columns >= K > ra) is never stored
+    const double* pa = gs + (ra < K ? ra : 0) * gst + t;
+    const double* pb = gs + (rb < K ? rb : 0) * gst + t;
     double acc[2] = {0.0, 0.0};
 #pragma unroll 4
-    for (int c = 0; c < dc4; c += 4) dmma_c(acc, ra < K ? pa[c] : 0.0, rb < K ? pb[c] : 0.0);
+    for (int c = 0; c < dc4; c += 4) dmma_c(acc, pa[c], pb[c]);
     // accumulator layout: row 8 I + g, columns 8 J + 2 t, + 1
     const int col = 8 * J + 2 * t;
     if (ra >= K) continue;
@@ -139,9 +143,16 @@ __device__ __forceinline__ void cta_gram(const double* gs, const double* nrm, co
       double d2 = fma(-2.0, gsum, na + nb);
       if (!(d2 > 1e-12 * (na + nb))) {  // (near-)duplicate: exact differences (this slice holds every dimension
         d2 = 0.0;                        // when d <= kXsD; for wider rows the earlier slices are gone, so clamp)
-        if (c0 == 0) {
-          const double* xa = gs + ra * Sh::kGsStride;
-          const double* xb = gs + cc * Sh::kGsStride;
+        if constexpr (LEAN) {            // lean layout: narrow slices, so the differences come from global memory
+          const double* xa = X + static_cast<int64_t>(sr[ra]) * d;
+          const double* xb = X + static_cast<int64_t>(sr[cc]) * d;
+          for (int c = 0; c < d; ++c) {
+            const double df = xa[c] - xb[c];
+            d2 = fma(df, df, d2);
+          }
+        } else if (c0 == 0) {
+          const double* xa = gs + ra * gst;
+          const double* xb = gs + cc * gst;
           for (int c = 0; c < dc4; ++c) {
             const double df = xa[c] - xb[c];
             d2 = fma(df, df, d2);
@@ -182,26 +193,39 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
     const int c0 = 8 * J;
     if (J > 0) {
       // 1. update of block column J
-      double bq[2 * (NBC - 1)];
+      // The warp's tiles I = J + warp + NW i (at most kTW of them) are updated together: per k-step one
+      // B fragment and kTW independent DMMA chains. Rows past the matrix read row 0 (rows > K of a
+      // tile and columns >= K of the block column are never stored), so no operand needs zeroing.
+      constexpr int kTW = (NBR - 1 + NW - 1) / NW;
       const int rb = c0 + g;  // the tile's column index this lane's B fragment belongs to
       const double* pb = tri + ro_c(rb < K ? rb : 0) + t;
+      const int cc = c0 + 2 * t;
+      double acc[kTW][2];
+      double* prow[kTW];
+      bool st0[kTW], st1[kTW];
 #pragma unroll
-      for (int Q = 0; Q < 2 * (NBC - 1); ++Q) bq[Q] = (Q < 2 * J && rb < K) ? -pb[4 * Q] : 0.0;
-      for (int I = J + warp; I < NBR; I += NW) {
+      for (int i = 0; i < kTW; ++i) {
+        const int I = J + warp + NW * i;
         const int ra = 8 * I + g;
-        const bool rok = ra <= K;
-        double* prow = cta_row<K>(tri, zrow, rok ? ra : 0);
-        const int cc = c0 + 2 * t;
+        const bool rok = I < NBR && ra <= K;
+        prow[i] = cta_row<K>(tri, zrow, rok ? ra : 0);
         const int lim = ra < K ? ra + 1 : K;  // columns < lim exist in row ra
-        double acc[2];
-        acc[0] = rok && cc < lim ? prow[cc] : 0.0;
-        acc[1] = rok && cc + 1 < lim ? prow[cc + 1] : 0.0;
-        const double* pa = prow + t;
+        st0[i] = rok && cc < lim;
+        st1[i] = rok && cc + 1 < lim;
+        acc[i][0] = st0[i] ? prow[i][cc] : 0.0;
+        acc[i][1] = st1[i] ? prow[i][cc + 1] : 0.0;
+      }
+#pragma unroll 2
+      for (int Q = 0; Q < 2 * J; ++Q) {
+        const double b = -pb[4 * Q];
 #pragma unroll
-        for (int Q = 0; Q < 2 * (NBC - 1); ++Q)
-          if (Q < 2 * J) dmma_c(acc, rok ? pa[4 * Q] : 0.0, bq[Q]);
-        if (rok && cc < lim) prow[cc] = acc[0];
-        if (rok && cc + 1 < lim) prow[cc + 1] = acc[1];
+        for (int i = 0; i < kTW; ++i)
+          if (J + warp + NW * i < NBR) dmma_c(acc[i], prow[i][4 * Q + t], b);  // warp-uniform
+      }
+#pragma unroll
+      for (int i = 0; i < kTW; ++i) {
+        if (st0[i]) prow[i][cc] = acc[i][0];
+        if (st1[i]) prow[i][cc + 1] = acc[i][1];
       }
       __syncthreads();
     }
@@ -218,7 +242,7 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
     for (int c = 0; c < 8; ++c) {
       const double piv = dblk[c][c];
       bad = bad || !(piv > 0.0);
-      inv[c] = rsqrt(piv);
+      inv[c] = rsqrt_pivot(piv);
       dblk[c][c] = piv * inv[c];
 #pragma unroll
       for (int i = c + 1; i < 8; ++i) dblk[i][c] *= inv[c];
@@ -239,11 +263,7 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
           if (i == tid)
 #pragma unroll
             for (int c = 0; c <= i; ++c) x[c] = dblk[i][c];
-        if (r < K) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            if (c <= tid) prow[c0 + c] = x[c];
-        }
+        // written back after the barrier below: the other warps may still be reading the unfactored block
       }
       if (tid >= 8 || r == K) {  // a row below the block (or the RHS row inside the last block's span)
 #pragma unroll
@@ -267,29 +287,49 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
       if (bad) misc[0] = 1.0;
     }
     __syncthreads();
+    // The factor rows of the diagonal block go in place only now: every thread loaded the unfactored block
+    // at the top of the panel without a barrier of its own, and no later block column reads these rows
+    // (left-looking: block column J' > J touches rows >= 8 J' only) until the backward solve.
+    if (tid < 8 && r < K) {
+      double* prow = tri + ro_c(r);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c <= tid) prow[c0 + c] = x[c];
+    }
   }
 }
 
-template <int K, int M>
-__global__ void __launch_bounds__(CtaShape<K, M>::kThreads, 1)
+#ifndef FMGP_CTA_LEAN_MINB  // CTAs per SM the lean kernel's registers are bounded for
+#define FMGP_CTA_LEAN_MINB 4
+#endif
+
+// LEAN (M == 1, Gram build + blocked factorisation, 16 <= d <= kXsD — cfg4): the same arithmetic with
+// a smaller footprint, so that more than two neighbourhoods are resident per SM (the kernel is bound
+// by the latency of its barriers and pivot chains, not by a pipe): no pair table, the coordinates
+// staged in narrow slices of `xsd` dimensions (rows of `gst` doubles; partial Gram sums go through the
+// triangle), and the row-per-thread sweep (100 doubles of registers per thread) compiled out.
+template <int K, int M, bool LEAN>
+__global__ void __launch_bounds__(CtaShape<K, M>::kThreads, LEAN ? FMGP_CTA_LEAN_MINB : 1)
 solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, const int32_t* __restrict__ S,
                  int64_t nrows, int64_t row_begin, KParams kp, double* __restrict__ C,
-                 unsigned long long* __restrict__ fail_min, int use_gram) {
+                 unsigned long long* __restrict__ fail_min, int use_gram, int xsd, int gst_arg) {
   using Sh = CtaShape<K, M>;
   extern __shared__ double smem[];
+  const int W = LEAN ? xsd : Sh::kXsD;             // dimensions staged per slice
+  const int gst = LEAN ? gst_arg : Sh::kGsStride;  // doubles per staged row (Gram build)
   double* tri = smem;
   double* xs = tri + Sh::kTri;
-  double* invd = xs + Sh::kXs;
+  double* invd = xs + (LEAN ? ((K * gst + 1) & ~1) : Sh::kXs);
   double* zbuf = invd + ((K + 1) & ~1);
   double* nrm = zbuf + ((M * K + 1) & ~1);  // Gram build: |x - x_0|^2 per neighbour
   double* misc = nrm + ((K + 1) & ~1);      // [0] = failure flag
   uint32_t* ptab = reinterpret_cast<uint32_t*>(misc + 2);
-  int32_t* sr = reinterpret_cast<int32_t*>(ptab + Sh::kPairs);
+  int32_t* sr = reinterpret_cast<int32_t*>(ptab + (LEAN ? 0 : Sh::kPairs));
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
 
-  for (int e = tid; e < Sh::kPairs; e += Sh::kThreads) {
+  for (int e = tid; !LEAN && e < Sh::kPairs; e += Sh::kThreads) {
     int i = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(e))) * 0.5f);
     while ((i * (i - 1)) / 2 > e) --i;
     while ((i * (i + 1)) / 2 <= e) ++i;
@@ -300,38 +340,45 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     __syncthreads();  // previous neighbourhood fully consumed
     for (int t = tid; t < K; t += Sh::kThreads) sr[t] = S[r * K + t];
+    // the next neighbourhood's index row: its coordinate rows are prefetched into L2 once this build is done
+    int32_t s_next = -1;
+    if (LEAN && tid < K && r + gridDim.x < nrows) s_next = S[(r + gridDim.x) * K + tid];
     __syncthreads();
     bool ok = false;
     for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
       // ---- build K(S_r) into the packed triangle (sequential-in-t distance)
       // one slice only (d <= kXsD): the exact recompute of near-duplicates needs every dimension staged
-      const bool gram = (use_gram & 1) && d >= 16 && d <= Sh::kXsD;
-      for (int c0 = 0; gram && c0 < d; c0 += Sh::kXsD) {
-        const int dc = min(Sh::kXsD, d - c0), dc4 = (dc + 3) & ~3;
+      const bool gram = LEAN || ((use_gram & 1) && d >= 16 && d <= Sh::kXsD);
+      for (int c0 = 0; gram && c0 < d; c0 += W) {
+        const int dc = min(W, d - c0), dc4 = (dc + 3) & ~3;
         const double* x0 = X + static_cast<int64_t>(sr[0]) * d + c0;  // centre: the neighbourhood's own point
-        for (int e = tid; e < K * dc4; e += Sh::kThreads) {
-          const int t = e / dc4, c = e - t * dc4;
-          xs[t * Sh::kGsStride + c] = c < dc ? X[static_cast<int64_t>(sr[t]) * d + c0 + c] - x0[c] : 0.0;
+        {  // 8, 16 or 32 threads per neighbour row (dc4 <= 48: at most two columns per thread)
+          const int sh = dc4 <= 8 ? 3 : (dc4 <= 16 ? 4 : 5);
+          const int cl = tid & ((1 << sh) - 1);
+          for (int t = tid >> sh; t < K; t += Sh::kThreads >> sh) {
+            const double* xr = X + static_cast<int64_t>(sr[t]) * d + c0;
+            for (int c = cl; c < dc4; c += 1 << sh) xs[t * gst + c] = c < dc ? xr[c] - x0[c] : 0.0;
+          }
         }
         __syncthreads();
         if (tid < K) {
           double nn = c0 == 0 ? 0.0 : nrm[tid];
-          const double* xr = xs + tid * Sh::kGsStride;
+          const double* xr = xs + tid * gst;
           for (int c = 0; c < dc4; ++c) nn = fma(xr[c], xr[c], nn);
           nrm[tid] = nn;
         }
         __syncthreads();
         const bool last = c0 + dc >= d;
         switch (last ? kernel_code(kp) : 0) {  // uniform; the kind only matters in the last slice
-          case 0: cta_gram<K, M, 0>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
-          case 1: cta_gram<K, M, 1>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
-          case 2: cta_gram<K, M, 2>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
-          case 3: cta_gram<K, M, 3>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
-          default: cta_gram<K, M, 4>(xs, nrm, kp, tri, c0, dc4, tid, last); break;
+          case 0: cta_gram<K, M, 0, LEAN>(xs, nrm, kp, tri, c0, dc4, tid, last, gst, X, sr, d); break;
+          case 1: cta_gram<K, M, 1, LEAN>(xs, nrm, kp, tri, c0, dc4, tid, last, gst, X, sr, d); break;
+          case 2: cta_gram<K, M, 2, LEAN>(xs, nrm, kp, tri, c0, dc4, tid, last, gst, X, sr, d); break;
+          case 3: cta_gram<K, M, 3, LEAN>(xs, nrm, kp, tri, c0, dc4, tid, last, gst, X, sr, d); break;
+          default: cta_gram<K, M, 4, LEAN>(xs, nrm, kp, tri, c0, dc4, tid, last, gst, X, sr, d); break;
         }
         __syncthreads();
       }
-      for (int c0 = 0; !gram && c0 < d; c0 += Sh::kXsD) {
+      for (int c0 = 0; !LEAN && !gram && c0 < d; c0 += Sh::kXsD) {
         const int dc = min(Sh::kXsD, d - c0);
         for (int e = tid; e < K * dc; e += Sh::kThreads) {
           const int t = e / dc, c = e - t * dc;
@@ -350,7 +397,13 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
         __syncthreads();
       }
       const double dg = jitter_c(kp.diag, attempt);
-      if (M == 1 && (use_gram & 2)) {
+      if (LEAN && s_next >= 0) {  // (X is far larger than L2 at cfg4: the staging gather above waits on DRAM)
+        const char* px = reinterpret_cast<const char*>(X + static_cast<int64_t>(s_next) * d);
+        for (int o = 0; o < d * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(px + o));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(Y + static_cast<int64_t>(s_next) * M));
+        s_next = -1;
+      }
+      if (LEAN || (M == 1 && (use_gram & 2))) {
         // ---- blocked DMMA factorisation in shared memory (cta_factor_blocked)
         if (tid < K) {
           tri[ro_c(tid) + tid] = dg;
@@ -363,6 +416,7 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
         __syncthreads();
         continue;
       }
+      if constexpr (!LEAN) {
       // ---- load the owned row into registers
       double a[K];
       double dacc = 0.0;
@@ -440,6 +494,7 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
         for (int p = 0; p < K; ++p) zbuf[c * K + p] = a[p];
       }
       __syncthreads();
+      }  // !LEAN
     }
     if (!ok) {
       if (tid == 0) atomicMin(fail_min, static_cast<unsigned long long>(row_begin + r));
@@ -475,20 +530,44 @@ template <int K, int M>
 cudaError_t launch_cta(const double* X, const double* Y, int d, const int32_t* S, int64_t nrows, int64_t row_begin,
                        const KParams& kp, double* C, unsigned long long* fail_min, int num_sms, cudaStream_t stream) {
   using Sh = CtaShape<K, M>;
-  cudaError_t err = cudaFuncSetAttribute(solve_cta_kernel<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(Sh::kBytes));
-  if (err != cudaSuccess) return err;
-  int per_sm = 0;
-  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_cta_kernel<K, M>, Sh::kThreads, Sh::kBytes);
-  if (err != cudaSuccess) return err;
-  if (per_sm < 1) per_sm = 1;
-  const int64_t grid = std::min<int64_t>(nrows, static_cast<int64_t>(num_sms) * per_sm);
   // FMGP_SOLVE_GRAM=0: the direct difference build for every d (A/B, as in the register solve)
   const char* ge = std::getenv("FMGP_SOLVE_GRAM");
   const char* be = std::getenv("FMGP_CTA_BLOCKED");  // 0: row-per-thread column sweep instead of the blocked DMMA factor
   const int use_gram = (!(ge != nullptr && ge[0] == '0') ? 1 : 0) | (!(be != nullptr && be[0] == '0') ? 2 : 0);
-  solve_cta_kernel<K, M><<<static_cast<unsigned>(grid), Sh::kThreads, Sh::kBytes, stream>>>(
-      X, Y, d, S, nrows, row_begin, kp, C, fail_min, use_gram);
+  if constexpr (M == 1) {
+    // FMGP_CTA_SLICE: dimensions staged per slice in the lean kernel (multiple of 4; 0 = the full-footprint kernel)
+    const char* se = std::getenv("FMGP_CTA_SLICE");
+    int xsd = se != nullptr ? std::atoi(se) : 24;
+    if (use_gram == 3 && d >= 16 && d <= Sh::kXsD && xsd > 0) {
+      xsd = std::min(Sh::kXsD, (xsd + 3) & ~3);
+      int gst = xsd + 4;  // = 4 or 12 mod 16 doubles: the fragment loads of a warp take two wavefronts
+      if (gst % 16 == 0 || gst % 16 == 8) gst += 4;
+      const size_t bytes = sizeof(double) * (Sh::kTri + ((K * gst + 1) & ~1) + 3 * ((K + 1) & ~1) + 2) +
+                           sizeof(int32_t) * K;
+      cudaError_t err = cudaFuncSetAttribute(solve_cta_kernel<K, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(bytes));
+      if (err != cudaSuccess) return err;
+      int per_sm = 0;
+      err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_cta_kernel<K, M, true>, Sh::kThreads, bytes);
+      if (err != cudaSuccess) return err;
+      if (per_sm < 1) per_sm = 1;
+      const int64_t grid = std::min<int64_t>(nrows, static_cast<int64_t>(num_sms) * per_sm);
+      solve_cta_kernel<K, M, true><<<static_cast<unsigned>(grid), Sh::kThreads, bytes, stream>>>(
+          X, Y, d, S, nrows, row_begin, kp, C, fail_min, use_gram, xsd, gst);
+      note_launches(1);
+      return cudaGetLastError();
+    }
+  }
+  cudaError_t err = cudaFuncSetAttribute(solve_cta_kernel<K, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Sh::kBytes));
+  if (err != cudaSuccess) return err;
+  int per_sm = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_cta_kernel<K, M, false>, Sh::kThreads, Sh::kBytes);
+  if (err != cudaSuccess) return err;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t grid = std::min<int64_t>(nrows, static_cast<int64_t>(num_sms) * per_sm);
+  solve_cta_kernel<K, M, false><<<static_cast<unsigned>(grid), Sh::kThreads, Sh::kBytes, stream>>>(
+      X, Y, d, S, nrows, row_begin, kp, C, fail_min, use_gram, 0, 0);
   note_launches(1);
   return cudaGetLastError();
 }

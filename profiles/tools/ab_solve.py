@@ -38,8 +38,12 @@ def main():
         res = {}
         outs = {}
         for var in a.variants.split(","):
-            os.environ["FMGP_SOLVE_DM"] = "1" if var == "dm" else "0"
-            os.environ["FMGP_SOLVE_2D"] = "1" if var == "2d" else "0"
+            if "=" in var:  # NAME=VALUE: a runtime switch of the default solve (e.g. FMGP_CTA_SLICE=0)
+                name, value = var.split("=", 1)
+                os.environ[name] = value
+            else:
+                os.environ["FMGP_SOLVE_DM"] = "1" if var == "dm" else "0"
+                os.environ["FMGP_SOLVE_2D"] = "1" if var == "2d" else "0"
             Cm = torch.empty((n, i.k, i.m), dtype=torch.float64, device="cuda")
             failed = C.c_int64(-1)
 
