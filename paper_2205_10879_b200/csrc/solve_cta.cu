@@ -337,13 +337,26 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
     ptab[e] = (static_cast<uint32_t>(ro_c(i) + p) << 16) | (static_cast<uint32_t>(i) << 8) | static_cast<uint32_t>(p);
   }
 
+  // LEAN: thread t < K carries entry t of the NEXT neighbourhood's index row in a register (loaded one
+  // neighbourhood ahead), so the row is in shared memory without a DRAM round trip, and that
+  // neighbourhood's coordinate rows are prefetched into L2 once the current build is done.
+  int32_t s_next = -1;
+  if (LEAN && tid < K && static_cast<int64_t>(blockIdx.x) < nrows) s_next = S[static_cast<int64_t>(blockIdx.x) * K + tid];
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     __syncthreads();  // previous neighbourhood fully consumed
-    for (int t = tid; t < K; t += Sh::kThreads) sr[t] = S[r * K + t];
-    // the next neighbourhood's index row: its coordinate rows are prefetched into L2 once this build is done
-    int32_t s_next = -1;
-    if (LEAN && tid < K && r + gridDim.x < nrows) s_next = S[(r + gridDim.x) * K + tid];
+    bool prefetch_due = false;
+    if constexpr (LEAN) {
+      if (tid < K) {
+        sr[tid] = s_next;
+        prefetch_due = r + gridDim.x < nrows;
+        if (prefetch_due) s_next = S[(r + gridDim.x) * K + tid];
+      }
+    } else {
+      for (int t = tid; t < K; t += Sh::kThreads) sr[t] = S[r * K + t];
+    }
     __syncthreads();
+    double y_mine = 0.0;  // this thread's response, in flight during the build
+    if (LEAN && tid < K) y_mine = Y[static_cast<int64_t>(sr[tid]) * M];
     bool ok = false;
     for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
       // ---- build K(S_r) into the packed triangle (sequential-in-t distance)
@@ -355,9 +368,27 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
         {  // 8, 16 or 32 threads per neighbour row (dc4 <= 48: at most two columns per thread)
           const int sh = dc4 <= 8 ? 3 : (dc4 <= 16 ? 4 : 5);
           const int cl = tid & ((1 << sh) - 1);
-          for (int t = tid >> sh; t < K; t += Sh::kThreads >> sh) {
-            const double* xr = X + static_cast<int64_t>(sr[t]) * d + c0;
-            for (int c = cl; c < dc4; c += 1 << sh) xs[t * gst + c] = c < dc ? xr[c] - x0[c] : 0.0;
+          const int rpp = Sh::kThreads >> sh;  // rows per pass of the CTA
+          const int ca = cl, cb = cl + (1 << sh);
+          const double x0a = ca < dc ? x0[ca] : 0.0, x0b = cb < dc ? x0[cb] : 0.0;
+          constexpr int RB = LEAN ? 13 : 2;  // rows in flight per thread: the gather is a chain of L2 / DRAM round trips otherwise
+          for (int tb = tid >> sh; tb < K; tb += RB * rpp) {
+            double va[RB], vb[RB];
+#pragma unroll
+            for (int i = 0; i < RB; ++i) {
+              const int t = tb + i * rpp;
+              const double* xr = X + static_cast<int64_t>(sr[t < K ? t : 0]) * d + c0;
+              va[i] = ca < dc ? xr[ca] : 0.0;
+              vb[i] = cb < dc ? xr[cb] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < RB; ++i) {
+              const int t = tb + i * rpp;
+              if (t < K) {
+                if (ca < dc4) xs[t * gst + ca] = va[i] - x0a;
+                if (cb < dc4) xs[t * gst + cb] = vb[i] - x0b;
+              }
+            }
           }
         }
         __syncthreads();
@@ -397,17 +428,17 @@ solve_cta_kernel(const double* __restrict__ X, const double* __restrict__ Y, int
         __syncthreads();
       }
       const double dg = jitter_c(kp.diag, attempt);
-      if (LEAN && s_next >= 0) {  // (X is far larger than L2 at cfg4: the staging gather above waits on DRAM)
+      if (LEAN && prefetch_due) {  // (X is far larger than L2 at cfg4: the staging gather would wait on DRAM)
         const char* px = reinterpret_cast<const char*>(X + static_cast<int64_t>(s_next) * d);
         for (int o = 0; o < d * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(px + o));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(Y + static_cast<int64_t>(s_next) * M));
-        s_next = -1;
+        prefetch_due = false;
       }
       if (LEAN || (M == 1 && (use_gram & 2))) {
         // ---- blocked DMMA factorisation in shared memory (cta_factor_blocked)
         if (tid < K) {
           tri[ro_c(tid) + tid] = dg;
-          zbuf[tid] = Y[static_cast<int64_t>(sr[tid]) * M];
+          zbuf[tid] = LEAN ? y_mine : Y[static_cast<int64_t>(sr[tid]) * M];
         }
         if (tid == 0) misc[0] = 0.0;
         __syncthreads();
