@@ -111,56 +111,90 @@ __device__ __forceinline__ void cta_gram(const double* gs, const double* nrm, co
   constexpr int NT = NB * (NB + 1) / 2;
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  // tile e = I (I + 1) / 2 + J, J <= I; a warp's tiles are NW apart, so (I, J) advance incrementally
+  // tile e = I (I + 1) / 2 + J, J <= I; a warp's tiles are NW apart, so (I, J) advance incrementally.
+  // kG tiles per step: kG independent DMMA chains, then their 2 kG entries per lane go through the
+  // kernel evaluation together (independent sqrt / exp chains).
+  constexpr int NW = Sh::kThreads / 32;
+  constexpr int kG = 3;
   int I = 0, J = warp;
-  for (int e = warp; e < NT; e += Sh::kThreads / 32, J += Sh::kThreads / 32) {
-    while (J > I) {
-      J -= I + 1;
-      ++I;
-    }
-    const int ra = 8 * I + g, rb = 8 * J + g;
-    // rows past K read row 0: what they produce (rows >= K of the tile, columns >= K > ra) is never stored
-    const double* pa = gs + (ra < K ? ra : 0) * gst + t;
-    const double* pb = gs + (rb < K ? rb : 0) * gst + t;
-    double acc[2] = {0.0, 0.0};
-#pragma unroll 4
-    for (int c = 0; c < dc4; c += 4) dmma_c(acc, pa[c], pb[c]);
-    // accumulator layout: row 8 I + g, columns 8 J + 2 t, + 1
-    const int col = 8 * J + 2 * t;
-    if (ra >= K) continue;
+  for (int e0 = warp; e0 < NT; e0 += kG * NW) {
+    const double* pa[kG];
+    const double* pb[kG];
+    int ra[kG], col[kG];
+    double acc[kG][2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int cc = col + h;
-      if (cc >= ra) continue;  // strict lower triangle only (the diagonal is set with the jitter rung)
-      double* out = tri + ro_c(ra) + cc;
-      double gsum = acc[h];
-      if (c0 != 0) gsum += *out;
-      if (!last) {
-        *out = gsum;
-        continue;
+    for (int i = 0; i < kG; ++i) {
+      while (J > I) {
+        J -= I + 1;
+        ++I;
       }
-      const double na = nrm[ra], nb = nrm[cc];
-      double d2 = fma(-2.0, gsum, na + nb);
-      if (!(d2 > 1e-12 * (na + nb))) {  // (near-)duplicate: exact differences (this slice holds every dimension
-        d2 = 0.0;                        // when d <= kXsD; for wider rows the earlier slices are gone, so clamp)
-        if constexpr (LEAN) {            // lean layout: narrow slices, so the differences come from global memory
-          const double* xa = X + static_cast<int64_t>(sr[ra]) * d;
-          const double* xb = X + static_cast<int64_t>(sr[cc]) * d;
-          for (int c = 0; c < d; ++c) {
-            const double df = xa[c] - xb[c];
-            d2 = fma(df, df, d2);
-          }
-        } else if (c0 == 0) {
-          const double* xa = gs + ra * gst;
-          const double* xb = gs + cc * gst;
-          for (int c = 0; c < dc4; ++c) {
-            const double df = xa[c] - xb[c];
-            d2 = fma(df, df, d2);
-          }
-        }
-      }
-      *out = kernel_from_sq<KF>(d2, kp);
+      const bool tv = e0 + i * NW < NT;  // past the last tile: row block 0 again, nothing stored
+      const int Ii = tv ? I : 0, Ji = tv ? J : 0;
+      const int rb = 8 * Ji + g;
+      ra[i] = tv ? 8 * Ii + g : K;
+      col[i] = 8 * Ji + 2 * t;
+      // rows past K read row 0: what they produce (rows >= K of the tile, columns >= K > ra) is never stored
+      pa[i] = gs + (ra[i] < K ? ra[i] : 0) * gst + t;
+      pb[i] = gs + (rb < K ? rb : 0) * gst + t;
+      acc[i][0] = 0.0;
+      acc[i][1] = 0.0;
+      J += NW;
     }
+#pragma unroll 2
+    for (int c = 0; c < dc4; c += 4) {
+#pragma unroll
+      for (int i = 0; i < kG; ++i) dmma_c(acc[i], pa[i][c], pb[i][c]);
+    }
+    // accumulator layout: row 8 I + g, columns 8 J + 2 t, + 1; strict lower triangle only (the diagonal is
+    // set with the jitter rung)
+    double* out[kG][2];
+    bool st[kG][2];
+    double val[kG][2];
+#pragma unroll
+    for (int i = 0; i < kG; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = col[i] + h;
+        st[i][h] = ra[i] < K && cc < ra[i];
+        out[i][h] = tri + (st[i][h] ? ro_c(ra[i]) + cc : 0);
+        double gsum = acc[i][h];
+        if (c0 != 0 && st[i][h]) gsum += *out[i][h];
+        val[i][h] = gsum;
+      }
+    if (last) {
+#pragma unroll
+      for (int i = 0; i < kG; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = col[i] + h;
+          const double na = nrm[st[i][h] ? ra[i] : 0], nb = nrm[st[i][h] ? cc : 0];
+          double d2 = fma(-2.0, val[i][h], na + nb);
+          if (st[i][h] && !(d2 > 1e-12 * (na + nb))) {  // (near-)duplicate: exact differences (the full-footprint
+            d2 = 0.0;  // layout holds every dimension when d <= kXsD; for wider rows the earlier slices are gone: clamp)
+            if constexpr (LEAN) {  // lean layout: narrow slices, so the differences come from global memory
+              const double* xa = X + static_cast<int64_t>(sr[ra[i]]) * d;
+              const double* xb = X + static_cast<int64_t>(sr[cc]) * d;
+              for (int c = 0; c < d; ++c) {
+                const double df = xa[c] - xb[c];
+                d2 = fma(df, df, d2);
+              }
+            } else if (c0 == 0) {
+              const double* xa = gs + ra[i] * gst;
+              const double* xb = gs + cc * gst;
+              for (int c = 0; c < dc4; ++c) {
+                const double df = xa[c] - xb[c];
+                d2 = fma(df, df, d2);
+              }
+            }
+          }
+          val[i][h] = kernel_from_sq<KF>(st[i][h] ? d2 : 1.0, kp);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kG; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (st[i][h]) *out[i][h] = val[i][h];
   }
 }
 
@@ -215,12 +249,25 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
         acc[i][0] = st0[i] ? prow[i][cc] : 0.0;
         acc[i][1] = st1[i] ? prow[i][cc + 1] : 0.0;
       }
+      static_assert(kTW <= 3, "tile-count dispatch below");
+      const int ntw = (NBR - J - warp + NW - 1) / NW;  // this warp's tiles (warp-uniform)
+      if (ntw >= 3) {
 #pragma unroll 2
-      for (int Q = 0; Q < 2 * J; ++Q) {
-        const double b = -pb[4 * Q];
+        for (int Q = 0; Q < 2 * J; ++Q) {
+          const double b = -pb[4 * Q];
 #pragma unroll
-        for (int i = 0; i < kTW; ++i)
-          if (J + warp + NW * i < NBR) dmma_c(acc[i], prow[i][4 * Q + t], b);  // warp-uniform
+          for (int i = 0; i < kTW; ++i) dmma_c(acc[i], prow[i][4 * Q + t], b);
+        }
+      } else if (ntw == 2) {
+#pragma unroll 2
+        for (int Q = 0; Q < 2 * J; ++Q) {
+          const double b = -pb[4 * Q];
+#pragma unroll
+          for (int i = 0; i < (kTW < 2 ? kTW : 2); ++i) dmma_c(acc[i], prow[i][4 * Q + t], b);
+        }
+      } else if (ntw == 1) {
+#pragma unroll 4
+        for (int Q = 0; Q < 2 * J; ++Q) dmma_c(acc[0], prow[0][4 * Q + t], -pb[4 * Q]);
       }
 #pragma unroll
       for (int i = 0; i < kTW; ++i) {
