@@ -86,6 +86,15 @@ __device__ __forceinline__ void cta_pairs(const double* xs, const uint32_t* ptab
   }
 }
 
+// 1/sqrt(x) for a pivot x > 0: MUFU seed (~2^-22) and one third-order step (as solve_dm.cu's rsqrt_pivot3:
+// four dependent FP64 operations; the pivot chain is the serial part of the panel)
+__device__ __forceinline__ double rsqrt_pivot3_c(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-(x * y), y, 1.0);
+  return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+
 __device__ __forceinline__ void dmma_c(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
       : "+d"(c[0]), "+d"(c[1])
@@ -276,8 +285,12 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
       }
       __syncthreads();
     }
-    // 2. panel: every thread factors the diagonal block, then solves its own row
+    // 2. panel: every thread factors the diagonal block, then solves its own row (a warp whose 32 rows are
+    // all past the RHS row has nothing to solve and skips the block too)
     const int nc = K - c0 < 8 ? K - c0 : 8;
+    const int r = c0 + tid;
+    double x[8];
+    if (c0 + 32 * warp <= K) {
     double dblk[8][8];
     double inv[8];
     bool bad = false;
@@ -289,7 +302,7 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
     for (int c = 0; c < 8; ++c) {
       const double piv = dblk[c][c];
       bad = bad || !(piv > 0.0);
-      inv[c] = rsqrt_pivot(piv);
+      inv[c] = rsqrt_pivot3_c(piv);
       dblk[c][c] = piv * inv[c];
 #pragma unroll
       for (int i = c + 1; i < 8; ++i) dblk[i][c] *= inv[c];
@@ -298,8 +311,6 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
 #pragma unroll
         for (int c2 = c + 1; c2 <= i; ++c2) dblk[i][c2] = fma(-dblk[i][c], dblk[c2][c], dblk[i][c2]);
     }
-    const int r = c0 + tid;
-    double x[8];
     if (r <= K) {
       double* prow = cta_row<K>(tri, zrow, r);
       if (tid < 8) {  // a row of the diagonal block: its factor row (tid < nc here: r <= K and r < c0 + 8)
@@ -316,11 +327,10 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
 #pragma unroll
         for (int c = 0; c < 8; ++c) x[c] = c < nc ? prow[c0 + c] : 0.0;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          double v = x[c];
+        for (int c = 0; c < 8; ++c) {  // right-looking: two dependent operations per column
+          x[c] *= inv[c];
 #pragma unroll
-          for (int c2 = 0; c2 < c; ++c2) v = fma(-x[c2], dblk[c][c2], v);
-          x[c] = v * inv[c];
+          for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], dblk[c2][c], x[c2]);
         }
 #pragma unroll
         for (int c = 0; c < 8; ++c)
@@ -333,6 +343,7 @@ __device__ __forceinline__ void cta_factor_blocked(double* tri, double* zrow, do
         if (c < nc) invd[c0 + c] = inv[c];
       if (bad) misc[0] = 1.0;
     }
+    }  // warps with rows
     __syncthreads();
     // The factor rows of the diagonal block go in place only now: every thread loaded the unfactored block
     // at the top of the panel without a barrier of its own, and no later block column reads these rows
