@@ -388,8 +388,20 @@ solve_dm_kernel(const double* __restrict__ X, const double* __restrict__ Y, cons
     yn0 = lane < K ? Y[sr[lane < K ? lane : 0]] : 0.0;
     yn1 = lane + 32 < K ? Y[sr[lane + 32 < K ? lane + 32 : 0]] : 0.0;
   };
+  // FMGP_DM_PREFETCH: 1 = the full register prefetch described above; 2 = only the next row's S entries are
+  // kept in registers (3: plus an L1 prefetch of its coordinate rows); 0 = every row gathers at its own start
+#ifndef FMGP_DM_PREFETCH
+#define FMGP_DM_PREFETCH 2
+#endif
   int64_t r = row_of(it0), rn = row_of(it0 + stride);
+#if FMGP_DM_PREFETCH >= 2
+  int32_t s0p = 0, s1p = 0;
   if (r >= 0) {
+    if (lane < K) s0p = S[r * K + lane];
+    if (lane + 32 < K) s1p = S[r * K + lane + 32];
+  }
+#endif
+  if (FMGP_DM_PREFETCH == 1 && r >= 0) {
     for (int q = lane; q < K; q += kWarp) sr[q] = S[r * K + q];
     __syncwarp();
     gather_xy();
@@ -405,12 +417,29 @@ solve_dm_kernel(const double* __restrict__ X, const double* __restrict__ Y, cons
     if (it >= nrows) continue;
     constexpr bool active = true;
 #endif
+#if FMGP_DM_PREFETCH == 1
     const int64_t rnn = row_of(it + 2 * stride);
     int32_t s0n = 0, s1n = 0;
     if (rn >= 0) {
       if (lane < K) s0n = S[rn * K + lane];
       if (lane + 32 < K) s1n = S[rn * K + lane + 32];
     }
+#elif FMGP_DM_PREFETCH >= 2
+    if (lane < K) sr[lane] = s0p;
+    if (lane + 32 < K) sr[lane + 32] = s1p;
+    __syncwarp();
+    gather_xy();
+    rn = row_of(it + stride);
+    if (rn >= 0) {  // in flight through the whole solve of this row
+      if (lane < K) s0p = S[rn * K + lane];
+      if (lane + 32 < K) s1p = S[rn * K + lane + 32];
+    }
+#else
+    r = row_of(it);
+    for (int q = lane; q < K; q += kWarp) sr[q] = S[r * K + q];
+    __syncwarp();
+    gather_xy();
+#endif
 #pragma unroll
     for (int i = 0; i < NX; ++i)
       if (lane + i * kWarp < K * D) xs[lane + i * kWarp] = xn[i];
@@ -469,6 +498,19 @@ solve_dm_kernel(const double* __restrict__ X, const double* __restrict__ Y, cons
       ok = dm_factor<K, D, KF>(A, xs, kn, cs, s_exp, lane, dv0, dv1);
       __syncwarp();
     }
+#if FMGP_DM_PREFETCH == 3
+    if (rn >= 0) {  // the next row's coordinate rows and responses towards L2 / L1 before the backward solve
+      if (lane < K) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(X + static_cast<int64_t>(s0p) * D));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(Y + s0p));
+      }
+      if (lane + 32 < K) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(X + static_cast<int64_t>(s1p) * D));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(Y + s1p));
+      }
+    }
+#endif
+#if FMGP_DM_PREFETCH == 1
     // the next row's coordinates and responses: in flight during the backward solve
     if (rn >= 0) {
       if (lane < K) sr[lane] = s0n;
@@ -476,6 +518,7 @@ solve_dm_kernel(const double* __restrict__ X, const double* __restrict__ Y, cons
       __syncwarp();
       gather_xy();
     }
+#endif
     if (!active) {
     } else if (!ok) {
       if (lane == 0) atomicMin(fail_min, static_cast<unsigned long long>(row_begin + r));
@@ -484,8 +527,12 @@ solve_dm_kernel(const double* __restrict__ X, const double* __restrict__ Y, cons
       dm_back<K>(A, dv0, dv1, C + r * K, lane);
       __syncwarp();
     }
+#if FMGP_DM_PREFETCH == 1
     r = rn;
     rn = rnn;
+#elif FMGP_DM_PREFETCH >= 2
+    r = rn;
+#endif
   }
 }
 
