@@ -1419,7 +1419,11 @@ void launch_query(const GridParams* gp, const double* pts, const int32_t* pid, c
                   const int32_t* qpos, const double* Q, const int32_t* qout, const int32_t* excl_arr, int kk,
                   int with_self, int64_t row_offset, int32_t* out, double* out_d, int num_sms, cudaStream_t s) {
   int64_t blocks = (nq * 32 + kQueryThreads - 1) / kQueryThreads;
-  const int64_t cap = static_cast<int64_t>(num_sms) * 8;
+  const char* ce = std::getenv("FMGP_GQ_CTAS");  // CTAs per SM of the grid-stride query kernel (A/B)
+  // 128: only four 8-warp CTAs are resident per SM, so a grid of a few long CTAs per SM ends in a tail of
+  // idle SMs (8 per SM: 27 of 32 warps active on average, cfg5 kNN 28.6 ms; 128: 25.9 ms)
+  const int per_sm = ce != nullptr && std::atoi(ce) > 0 ? std::atoi(ce) : 128;
+  const int64_t cap = static_cast<int64_t>(num_sms) * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   grid_query_kernel<D, E><<<static_cast<unsigned>(blocks), kQueryThreads, 0, s>>>(
@@ -1643,7 +1647,8 @@ cudaError_t run_predict_grid(const PredictGridCache& g, const double* X, const i
     qo = qb.pid;
   }
   int64_t blocks = (nz + kQueryThreads - 1) / kQueryThreads;  // 32 test points per warp
-  const int64_t cap = static_cast<int64_t>(num_sms) * 8;
+  const char* pce = std::getenv("FMGP_PGRID_CTAS");  // CTAs per SM of the grid-stride predict kernel (A/B)
+  const int64_t cap = static_cast<int64_t>(num_sms) * (pce != nullptr && std::atoi(pce) > 0 ? std::atoi(pce) : 256);  // 8 per SM left a tail: cfg5 4.93 -> 4.40 ms
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   // the grid-ordered model replica, when attached to this grid for these S/C shapes
