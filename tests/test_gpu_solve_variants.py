@@ -95,3 +95,31 @@ def test_variant_numeric_error_row(fm, port, monkeypatch, variant):
     with pytest.raises(fm.NumericError) as ei:
         fm.precompute(fm.TrainingSet(X, Y, 0.0), fm.FittedParams(p, fm.KernelKind.RBF), fm.NeighborIndex.build(X), k)
     assert ei.value.failed_row == eo.value.failed_row
+
+
+# k = 100 CTA solve (solve_cta.cu): the lean kernel at several slice widths (FMGP_CTA_SLICE: 8 -> four
+# neighbourhoods per SM, 24 -> three, the default), the full-footprint kernel (0) and the row-per-thread
+# sweep (FMGP_CTA_BLOCKED=0), each against the oracle; d = 16 / 48 are the ends of the Gram + lean domain,
+# d = 40 is cfg4's, d = 8 takes the pair-table build. A near-duplicate pair (offset 1e-6) takes the exact
+# recompute of the squared distance in the Gram builds.
+@pytest.mark.parametrize("env", [{"FMGP_CTA_SLICE": "0"}, {"FMGP_CTA_SLICE": "8"}, {"FMGP_CTA_SLICE": "16"},
+                                 {"FMGP_CTA_SLICE": "24"}, {"FMGP_CTA_SLICE": "40"},
+                                 {"FMGP_CTA_BLOCKED": "0"}], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
+@pytest.mark.parametrize("d", [8, 16, 40, 48])
+def test_cta_solve_layouts_match_oracle(fm, port, monkeypatch, env, d):
+    for k_, v in env.items():
+        monkeypatch.setenv(k_, v)
+    rng = np.random.default_rng(1000 + d)
+    n, k = 1500, 100
+    X = rng.standard_normal((n, d))
+    X[700] = X[10] + 1e-6          # near-duplicate pair (an exact duplicate would make the block singular)
+    Y = rng.standard_normal(n)
+    kind, sigma, rho, nu, tau = 1, 1.1, 3.0 * np.sqrt(d / 40.0), 2.5, 0.1
+    p = fm.KernelParams(sigma, rho, nu, tau)
+    model = fm.precompute(fm.TrainingSet(X, Y, 0.0), fm.FittedParams(p, fm.KernelKind(kind)),
+                          fm.NeighborIndex.build(X), k)
+    rows = np.unique(np.concatenate([np.arange(0, n, 7), [10, 700]]))
+    S_o, C_o = port.precompute_rows(X, Y[:, None], kind, sigma, rho, nu, tau, k, rows, threads=8)
+    assert np.array_equal(model.S[rows], S_o)
+    err = row_rel_err(model.C.reshape(n, k, -1)[rows], C_o)
+    assert err.max() <= C_TOL, (env, d, err.max())
