@@ -62,6 +62,12 @@ namespace fmgp {
 
 namespace {
 
+#ifndef FMGP_TC_RECHECK_CTAS  // CTAs per SM of the grid-stride recheck launch (a few long CTAs per SM leave a tail)
+#define FMGP_TC_RECHECK_CTAS 64
+#endif
+constexpr int kRecheckCtas = FMGP_TC_RECHECK_CTAS;
+
+
 constexpr int kBM = 128;  // queries per tile (TMEM lanes)
 constexpr int kBN = 128;  // reference points per tile (TMEM columns per buffer)
 constexpr int kBK = 64;   // fp16 dims per k-block (one 128 B swizzle row)
@@ -933,7 +939,7 @@ cudaError_t knn_tc(const double* Q, int64_t nq, const double* P, int64_t np, int
   err = cudaGetLastError();
   if (err == cudaSuccess && debug_G == nullptr) {
     const int64_t blocks = (nq + kRecheckWarps - 1) / kRecheckWarps;
-    tc_recheck_kernel<<<static_cast<unsigned>(blocks < num_sms * 16 ? blocks : num_sms * 16), kRecheckWarps * 32, 0,
+    tc_recheck_kernel<<<static_cast<unsigned>(blocks < num_sms * kRecheckCtas ? blocks : num_sms * kRecheckCtas), kRecheckWarps * 32, 0,
                         s>>>(
         Q, P, d, nq, kk, cand, ccount, 1, cap, with_self, self_offset, out, out_d);
     note_launches(1);

@@ -107,7 +107,7 @@ cudaError_t predict_gather(const double* X, const int32_t* S, const double* C, i
                            const int32_t* nn, double* out, int num_sms, cudaStream_t stream) {
   if (nz <= 0) return cudaSuccess;
   int64_t need = (nz + kPredWarps - 1) / kPredWarps;
-  int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(num_sms) * 8);
+  int64_t grid = std::min<int64_t>(need, static_cast<int64_t>(num_sms) * 64);  // many short CTAs: no tail of idle SMs
   predict_kernel<<<static_cast<unsigned>(grid), kPredWarps * kWarp, 0, stream>>>(X, S, C, d, k, m, kp,
                                                                                  mean_offset_dev, Z, nz, nn, out);
   note_launches(1);
