@@ -28,7 +28,10 @@ at N > 1; fmgp_model_predict for predict.
 Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events
 on the launching stream; L2 is flushed (256 MiB write) between timed steps,
 outside the events; barrier + synchronize around the timed region; the max
-over ranks is reported. Data: seeded synthetic inputs with the config's
+over ranks is reported. Before the warm-up the process idles for --settle
+seconds (default 20, reported as config.settle_s): run within seconds of a
+CPU-heavy process exiting (the reference arm), two or three of the first
+steps show 5-15 ms host-side stalls (profiles/r02/README.md), gone after 30 s. Data: seeded synthetic inputs with the config's
 shapes and distributions; the paper's datasets are not in
 the image. The CPU baselines are the reference's own TUs (oracle/_ref) on
 bounded samples of the same workload, on the box's host cores (rank 0, N=1).
@@ -60,6 +63,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--settle", type=float, default=20.0,
+                    help="seconds to idle before the warm-up (outside every timed region): for ~30 s after a CPU-heavy "
+                         "process such as the reference arm exits, a few steps show 5-15 ms host-side stalls")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="override n_train (debug; not a bench line)")
@@ -106,7 +112,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(float(os.environ.get("FMGP_BENCH_SMI_INTERVAL", "0.2")))
 
     def __enter__(self):
         self._t = threading.Thread(target=self._loop, daemon=True)
@@ -398,6 +404,9 @@ def main():
     dfma, dmma = C.c_double(0), C.c_double(0)
     N.check(N.LIB.fmgp_diag_fp64_peak(C.byref(dfma), C.byref(dmma)))
 
+    if args.settle > 0:  # see --settle; nothing is timed before or during this wait
+        time.sleep(args.settle)
+        sync_all()
     with ClockSampler(local) as clk:
         pre_ms, pre_all, pre_launch = timed(precompute_step, args.steps, args.warmup, stage_events=True)
         model = C.c_void_p()  # the device-resident model over this rank's full (all-gathered) S, C
@@ -522,7 +531,8 @@ def main():
         "config": {"workload": f"cfg{info.cfg}", "d": d, "n_train": n, "n_test": nt, "k": k, "m": m,
                    "kernel": "RBF" if info.kind == 1 else f"Matern nu={info.nu}",
                    "parallelism": f"rows block-cyclic over {ws} GPU(s), S/C all-gathered (NCCL, C++)",
-                   "l2": "flushed (256 MiB write) between timed steps"},
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "settle_s": args.settle},
         "predict": {"metric": "predict test-pts/s", "value": pred_value, "unit": "test-pts/s", "ms_per_step": pred_ms,
                     "roofline": {"bound": "hbm", "achieved": pred_gbs, "peak": hbm, "unit": "GB/s",
                                  "frac": pred_gbs / hbm, "peak_source": hbm_src,
