@@ -1,4 +1,4 @@
-TAG=r02_final_j
+TAG=r02_final_l
 O=gpurun_out
 mkdir -p $O
 python -m pytest tests -m gpu -q --durations=5 > $O/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu_$TAG.log
